@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark of the NRTO inner solve (one JSON line on rank 0).
+
+Workload: c5 -- a batch of Franka-shaped SOCP subproblems
+(n_x=14, n_u=7, T=100, n_g=4306 cones, E=2.12M ragged cone elements each),
+FullADMM engine, L_max=50 iterations with fixed_iters, per-GPU batch
+fixed (weak scaling; N=8 x 512 = 4096 = c5).  One step = one SL-iteration
+subproblem for the whole batch: nrto_refresh (setup S0-S2 from
+device-resident primitives) + nrto_inner_solve (S3-S10).  Working set per GPU
+is ~22 GB >> 126 MB L2, so no L2 flush is needed between steps.
+
+`--impl reference` times the CPU oracle (oracle/, as it stands) on a bounded
+sample of the same workload (one instance per step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+
+METRIC = "inner DR/ADMM iters/sec and SOC projections/sec per GPU; SL-iteration wall-clock"
+UNIT = "instance-iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch-per-gpu", type=int, default=512)
+    ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--workload", default="c5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev, self.rows, self.stop = dev, [], threading.Event()
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def workload_shape_stats(shape):
+    nx, nu = shape.n_x, shape.n_u
+    knot = np.asarray(shape.cone_knot, np.int64)
+    kind = np.asarray(shape.cone_kind)
+    st = kind == 0
+    E_s = int(((knot[st] + 1) * nx).sum())
+    E = E_s + int((~st).sum()) * nx
+    E_B = int((knot[st] * nu).sum()) + int((~st).sum()) * nu
+    return E, E_s, E_B
+
+
+def cpu_oracle_sample(cfg, L, n_inst=1, seed0=0):
+    """Time the oracle (as it stands) on n_inst instances x L iterations, 1 thread."""
+    from threadpoolctl import threadpool_limits
+    from gen import make_instance
+    from oracle import structured as st
+    from oracle.params import make_params
+    items = [make_instance(cfg, seed0 + i) for i in range(n_inst)]
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        for shape, data in items:
+            sp = st.StructuredProblem(shape, data)
+            st.fulladmm(sp, make_params(max_iter=L, fixed_iters=1))
+        dt = time.perf_counter() - t0
+    return n_inst * L / dt, dt
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# -------------------------------------------------------------- reference
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    L = args.iters
+    cfg = "c5" if args.workload == "c5" else args.workload
+    for _ in range(args.warmup):
+        cpu_oracle_sample(cfg, L, 1, seed0=0)
+    times = []
+    for s in range(args.steps):
+        v, dt = cpu_oracle_sample(cfg, L, 1, seed0=s + 1)
+        times.append(dt)
+    ms = 1000.0 * float(np.mean(times))
+    value = L / (ms / 1000.0)
+    sample = f"1 {cfg} instance x {L} FullADMM iterations (+ setup) per step, 1 host thread"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen/, seeded PCG64)",
+            "config": {"workload": f"{cfg}: Franka n_x=14 n_u=7 T=100 FullADMM L={L}",
+                       "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2603_02642_b200.build import build as _build, needs_build
+    if needs_build():
+        if rank == 0:
+            _build()
+        if world > 1:
+            dist.barrier()
+    from paper_2603_02642_b200 import nrto
+    from gen import make_batch
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    B, L = args.batch_per_gpu, args.iters
+    shape, batch = make_batch(args.workload, B, start=rank * B)
+    E, E_s, E_B = workload_shape_stats(shape)
+    data_dev = nrto.to_tensors(batch, device=dev)
+    solver = nrto.InnerSolver(shape, data_dev, max_iter=L, fixed_iters=1)
+    out = nrto.alloc_out(shape, B, solver.E, device=dev, full=True)
+    out.pop("nu"); out.pop("lam_nu")          # optional ragged outputs not requested
+    stream = torch.cuda.current_stream()
+
+    def step():
+        solver.refresh(data_dev)
+        solver.solve(nrto.NRTO_FULLADMM, out=out)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    solver.profile(True)
+    solver.profile_read()                      # clear
+    l0 = solver.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = solver.launches() - l0
+    prof = solver.profile_read()
+    solver.profile(False)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * L / (ms_max / 1000.0)
+
+    # ---- end to end through the C ABI with HOST buffers (H2D + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        data_host = nrto.to_tensors(batch, device="cpu", pinned=True)
+        out_h = nrto.alloc_out(shape, B, solver.E, device="cpu", pinned=True, full=True)
+        out_h.pop("nu"); out_h.pop("lam_nu")
+        h2d = sum(v.numel() * v.element_size() for v in data_host.values())
+        d2h = sum(v.numel() * v.element_size() for v in out_h.values())
+
+        def step_e2e():
+            solver.refresh(data_host, memory=nrto.NRTO_MEM_HOST)
+            solver.solve(nrto.NRTO_FULLADMM, out=out_h, memory=nrto.NRTO_MEM_HOST)
+
+        step_e2e()
+        torch.cuda.synchronize()
+        barrier()
+        ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev2.record(stream)
+        for _ in range(args.steps):
+            step_e2e()
+        ev3.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = ev2.elapsed_time(ev3) / args.steps
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ems = float(te.item())
+        e2e = {"value": world * B * L / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "sl_iteration_wall_clock_ms": ems}
+
+    # batch-wide residual statistics over NVLink (the only collective)
+    stats = torch.tensor([out["r_p"].max().item(), float(out["status"].ne(2).all().item())],
+                         dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+
+    if rank != 0:
+        return
+    peak, peak_kind = load_peaks()
+    pms, pn = prof["pass"]
+    bytes_per_launch = B * 8.0 * (2 * E + E_s + E_B)
+    achieved = bytes_per_launch / (pms / pn / 1000.0) / 1e9 if pn else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "pass_traffic.json")
+    if os.path.exists(tf):
+        try:
+            tj = json.load(open(tf))
+            if tj.get("batch") == B:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v1, dt = cpu_oracle_sample(args.workload, L, 1, seed0=0)
+        cpu = {"value": v1, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"1 {args.workload} instance x {L} FullADMM iterations incl. setup "
+                         f"({dt:.1f} s, 1 host thread)"}
+    kernel_ms = {k: (v[0] / args.steps) for k, v in prof.items()}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (gen/, seeded PCG64; no datasets or trained weights)",
+        "config": {"workload": f"{args.workload}: batch of Franka-shaped SOCP subproblems "
+                               f"(n_x=14, n_u=7, T=100, n_g={shape.n_g}, E={E}), FullADMM, "
+                               f"L={L} fixed iterations, {B} instances/GPU",
+                   "global_batch": world * B, "parallelism": f"instances sharded dp{world}",
+                   "l2": "inputs larger than L2 (working set ~%.0f GB/GPU)" % (
+                       B * 8 * (2 * E + E_B) / 1e9)},
+        "soc_projections_per_s": value * shape.n_g,
+        "cone_elements_per_s": value * E,
+        "sl_iteration_wall_clock_ms": (e2e or {}).get("sl_iteration_wall_clock_ms"),
+        "kernel_ms_per_step": kernel_ms,
+        "roofline": {"bound": "hbm", "kernel": "k_fa_pass (S3 forward map + S4 SOC projection + "
+                                                "S5 state update)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": bytes_per_launch},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "residuals": {"max_r_p": float(stats[0].item()), "all_finite": bool(stats[1].item())},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,216 @@
+/*
+ * nrto.h -- C ABI of the B200-native NRTO inner solver (libnrto.so).
+ *
+ * Solves, for a batch of independent robust trajectory-optimization problem
+ * instances, the SOCP subproblem of one successive-linearization (SL)
+ * iteration of cuNRTO (arXiv 2603.02642):
+ *
+ *   Problem 2
+ *     min  sum_k (u_hat_k + du_k)^T R_u^k (u_hat_k + du_k) + 1/2 k_v^T Q_v k_v
+ *     s.t. g_j + b_j^T du + p_j <= 0                       (g^lin,1; DESIGN R1)
+ *          || A_hat_j k_v + b_hat_j ||_2 <= p_j            j = 1..n_g
+ *          || F_u du ||_2 <= r_trust
+ *
+ * with two engines:
+ *   NRTO_FULLADMM  Algorithm 1: Block-1 SOC projection (13),
+ *                  Block-2 QP (14a) and gain update (14b), dual update (16).
+ *   NRTO_DR        the NRTO inner ADMM (5a)-(5c) whose (5a)
+ *                  subproblem (7) is solved by relaxed Douglas-Rachford
+ *                  (11a)-(11c) with the affine prox of P:930-964.
+ *
+ * The data of Problem 2 (F_u, F_zeta, A_hat_j, b_hat_j, Q_v; SM §I)
+ * is built ON THE DEVICE by nrto_setup from the SL-iteration primitives below
+ * (Jacobians, constraint gradients, Psi, weights).  Workload assumption
+ * (P:1483-1486): Gamma = I and S = blkdiag(S_0, ..., S_T), i.e. Psi is given
+ * as T+1 diagonal blocks Psi_k with Psi_k^T Psi_k = S_k^{-1}.
+ *
+ * Conventions
+ *   - All floating point is IEEE binary64 (double).  Precision of the paper is
+ *     unstated (DESIGN R17).
+ *   - Arrays are batch-major and instance-contiguous: X[b][...] with b in
+ *     [0, batch).  Matrices are row-major unless stated.  k_v is column-major
+ *     vec of K_k per time step: kv[b][k*n_u*n_x + i*n_u + m]
+ *     = (K_k)[m][i].
+ *   - Cone j is "state" (kind 0: g_j(x_{k_j}) <= 0, knot k_j in 1..T) or
+ *     "control" (kind 1: h_j linear in u_k, knot = k in 0..T-1; DESIGN R14).
+ *   - Ragged cone rows: state cone j stores the blocks 0..k_j of
+ *     its n_z = (T+1) n_x vector ((k_j+1) n_x doubles; blocks k > k_j are
+ *     identically zero); control cone j stores block k (n_x
+ *     doubles).  nrto_layout returns the offsets; E = total length.
+ *   - Every call is asynchronous on the stream it is given (a cudaStream_t
+ *     passed as void*, NULL = legacy default stream) unless a HOST memory
+ *     flag forces staging copies; results are valid after the stream syncs.
+ *
+ * Errors: functions return nrto_err; no C++ exception crosses the ABI.  On a
+ * non-OK return nrto_last_error() gives a thread-local message.  Per-instance
+ * non-convergence or non-finite iterates are reported in status[], never as
+ * an error.
+ */
+#ifndef NRTO_H_
+#define NRTO_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nrto_handle_s* nrto_handle;
+
+typedef enum {
+  NRTO_OK = 0,
+  NRTO_EINVAL = -1,   /* bad shape / argument (dimension rule violated)          */
+  NRTO_ENOTSPD = -2,  /* W_K not SPD, or a Riccati H_uu not SPD (setup error)     */
+  NRTO_ECUDA = -3,    /* CUDA runtime error (message has the CUDA string)        */
+  NRTO_ENOMEM = -4,   /* device allocation failed                               */
+  NRTO_ESTATE = -5    /* call order violated (e.g. solve on a destroyed handle)  */
+} nrto_err;
+
+typedef enum { NRTO_FULLADMM = 0, NRTO_DR = 1 } nrto_engine;
+
+/* per-instance outcome (status[b]) */
+typedef enum { NRTO_CONVERGED = 0, NRTO_MAX_ITERS = 1, NRTO_DIVERGED = 2 } nrto_inst_status;
+
+typedef enum { NRTO_MEM_DEVICE = 0, NRTO_MEM_HOST = 1 } nrto_mem;
+
+/* Shape shared by every instance of a batch (host memory). */
+typedef struct {
+  int32_t n_x, n_u, T, n_g, batch;  /* 1 <= n_x <= 32, 1 <= n_u <= n_x, T >= 1,
+                                       n_g >= 0, batch >= 1                     */
+  const int32_t* cone_knot;         /* [n_g] state: k_j in 1..T; control: k in 0..T-1 */
+  const int8_t* cone_kind;          /* [n_g] 0 = state row, 1 = control row      */
+} nrto_shape;
+
+/* SL-iteration primitives (read only during nrto_setup; caller-owned).
+ * memory = NRTO_MEM_DEVICE: device pointers; NRTO_MEM_HOST: host pointers
+ * (pinned preferred) that nrto_setup copies to the device itself.          */
+typedef struct {
+  int32_t memory;                   /* nrto_mem                                       */
+  const double* A;                  /* [b][T][n_x][n_x]  dx_{k+1} = A_k dx_k + B_k du_k */
+  const double* B;                  /* [b][T][n_x][n_u]                               */
+  const double* grad;               /* [b][n_g][n_x] state: d g_j / d x_{k_j};
+                                       control: h'_j in the first n_u slots          */
+  const double* g0;                 /* [b][n_g] g_j(x_hat) or h_j(u_hat)              */
+  const double* Psi;                /* [b][T+1][n_x][n_x] Psi_k, Psi_k^T Psi_k = S_k^-1 */
+  const double* tau;                /* [b] ellipsoid radius tau > 0       */
+  const double* W_K;                /* [b][T][n_u][n_u] R_K^T R_K (SPD)       */
+  const double* R_u;                /* [b][T][n_u][n_u] R_u^k (SPD)                   */
+  const double* u_hat;              /* [b][T][n_u]                                    */
+  const double* r_trust;            /* [b] trust-region radius >= 0                   */
+} nrto_data;
+
+/* Hyper-parameters (DESIGN §4 lists the paper lines and readings). */
+typedef struct {
+  double rho;        /* FullADMM penalty rho                          */
+  double rho_admm;   /* NRTO-ADMM penalty for the DR engine (R3)               */
+  double alpha_dr;   /* DR relaxation alpha in (0,1)                   */
+  double sigma_dr;   /* R_chi = sigma_dr I (R7)                                */
+  double r_s;        /* R_s = r_s I (R7)                                       */
+  double eps_p, eps_d;  /* r_p, r_d tolerances (R6)                */
+  double eps_dr;     /* DR fixed-point residual tolerance (R8)      */
+  double rho_qp, sigma_qp, alpha_qp;  /* (14a)/(5b) QP ADMM (R1)               */
+  int32_t max_iter;       /* FullADMM L_max                                   */
+  int32_t max_admm_iter;  /* NRTO-ADMM iterations (DR engine)                 */
+  int32_t max_dr_iter;    /* DR iterations per (5a)                           */
+  int32_t qp_iters;       /* QP ADMM iterations per (14a)/(5b), warm-started  */
+  int32_t check_every;    /* termination test cadence (R11)                   */
+  int32_t fixed_iters;    /* != 0: run exactly the maximum iteration counts   */
+} nrto_params;
+
+/* Caller-owned outputs.  Optional arrays may be NULL.                       */
+typedef struct {
+  int32_t memory;          /* nrto_mem of every pointer below                  */
+  double* kv;              /* [b][T*n_u*n_x]  k_v (column-major vec(K_k))      */
+  double* du;              /* [b][T*n_u]      delta u_hat                      */
+  double* p;               /* [b][n_g]        p                                */
+  double* p_tilde;         /* [b][n_g]        p~                               */
+  double* lam_p;           /* [b][n_g]  FullADMM: scaled lambda_p; DR: lambda  */
+  double* nu;              /* [b][E]  FullADMM nu (ragged), optional           */
+  double* lam_nu;          /* [b][E]  FullADMM scaled lambda_nu, optional      */
+  double* objective;       /* [b]  J of Problem 2 at (du, k_v), optional       */
+  double* margin_cone;     /* [b][n_g] p~_j - ||A_hat_j k_v + b_hat_j||, opt.  */
+  double* margin_lin;      /* [b][n_g] -(g_j + b_j^T du + p_j), optional       */
+  int32_t* iters;          /* [b] iterations run (ADMM iterations for DR)      */
+  int32_t* status;         /* [b] nrto_inst_status                             */
+  double* r_p;             /* [b] final ||p - p~||                             */
+  double* r_d;             /* [b] final rho ||p~^l - p~^(l-1)||                */
+} nrto_out;
+
+/* Fill p with the defaults of DESIGN §4 (rho=10, rho_admm=40, alpha_dr=0.9,
+ * sigma_dr=1e-6, r_s=1, eps_p=eps_d=1e-3, eps_dr=1e-4, rho_qp=1,
+ * sigma_qp=1e-6, alpha_qp=1.6, max_iter=40, max_admm_iter=40,
+ * max_dr_iter=100, qp_iters=10, check_every=1, fixed_iters=0). */
+void nrto_default_params(nrto_params* p);
+
+/* Ragged layout (host only, no CUDA).  E_out = sum_j L_j; offsets_out, if
+ * not NULL, receives n_g+1 offsets (offsets_out[j] = start of cone j).
+ * NRTO_EINVAL if a knot/kind violates the rules above. */
+nrto_err nrto_layout(const nrto_shape* shape, int64_t* E_out, int64_t* offsets_out);
+
+/* Setup (S0-S2 of SURVEY §8a) for one SL iteration: uploads/reads the
+ * primitives, builds on the device the ragged b_hat_{j,k}, b_{j,k} (costate
+ * sweeps), the per-step gain factors of M^{-1} = Q_v + rho sum_j
+ * A_hat_j^T A_hat_j (block diagonal in time, solved by a generalized
+ * eigen-decomposition chain) for both engines, and the Riccati factors of the
+ * QP.  All state lives in handle-owned device memory; the inputs may be freed
+ * once `stream` has synchronised.  *out receives a new handle. */
+nrto_err nrto_setup(const nrto_shape* shape, const nrto_data* data,
+                    const nrto_params* params, void* stream, nrto_handle* out);
+
+/* Re-runs setup on an existing handle for a new SL iteration of the same
+ * shape (new linearisation, same cone structure): uploads `data` and rebuilds
+ * every S0-S2 product in the handle's memory without reallocating.  The DR
+ * warm state is reset.  Errors as nrto_setup. */
+nrto_err nrto_refresh(nrto_handle h, const nrto_data* data, void* stream);
+
+/* Runs the inner solve with `engine` for every instance and writes `out`.
+ * FullADMM cold-starts every call (R10); the DR engine keeps its (chi~, s~)
+ * warm state in the handle across calls but restarts the outer ADMM.
+ * Iterations are counted per instance; a converged instance is frozen while
+ * others continue (R12). */
+nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_out* out,
+                          void* stream);
+
+/* Standalone (14b) for FullADMM, device pointers:
+ *   kv_next = q + calM kv_prev + calMbar nu
+ *           = M (Q_v kv_prev + rho sum_j A_hat_j^T (nu_j - b_hat_j))
+ * nu is ragged [b][E]; kv_prev, kv_next are [b][T*n_u*n_x]. */
+nrto_err nrto_gain_update(nrto_handle h, const double* nu, const double* kv_prev,
+                          double* kv_next, void* stream);
+
+/* Batched ragged SOC projection, SM Eq.(18), device pointers:
+ * for cone j with row y[off[j]..off[j+1]) and scalar t[j],
+ * (t_out[j], y_out[row]) = Pi_{||y|| <= t}(t[j], y[row]).  y_out may alias y. */
+nrto_err nrto_soc_project(const double* t, const double* y, const int64_t* offsets,
+                          int64_t n_cones, double* t_out, double* y_out, void* stream);
+
+/* Number of kernel launches issued by this handle since creation (host
+ * counter; used to report bench.py's gpu_launches). */
+int64_t nrto_launch_count(nrto_handle h);
+
+/* Kernel classes timed by the optional CUDA-event profiler. */
+typedef enum {
+  NRTO_K_PASS = 0,     /* fused cone pass: S3 forward map + S4 projection + S5 state update */
+  NRTO_K_ADJOINT = 1,  /* S7 adjoint reduction                                             */
+  NRTO_K_GAIN = 2,     /* S8 gain chain                                                    */
+  NRTO_K_QP = 3,       /* S9 QP (+ dual update, residuals S6)                              */
+  NRTO_K_OTHER = 4,    /* DR residual reduction, resets, finish                            */
+  NRTO_K_COUNT = 5
+} nrto_kernel_class;
+
+/* enable != 0: every launch of a timed class is bracketed by CUDA events on
+ * the launching stream; nrto_profile_read synchronises on them and returns
+ * the summed device time (ms) and the launch count of `kclass` since the
+ * last read (then clears that class). */
+nrto_err nrto_profile_enable(nrto_handle h, int32_t enable);
+nrto_err nrto_profile_read(nrto_handle h, int32_t kclass, double* total_ms, int64_t* launches);
+
+nrto_err nrto_destroy(nrto_handle h);
+
+/* Thread-local message for the last non-OK return (never NULL). */
+const char* nrto_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NRTO_H_ */

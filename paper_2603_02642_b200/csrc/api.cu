@@ -1,0 +1,432 @@
+// C ABI of libnrto (include/nrto.h): validation, layout, device allocation,
+// host orchestration of the inner loop.  No C++ exception crosses the ABI.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include "common.cuh"
+
+using namespace nrto;
+
+static thread_local std::string g_err = "ok";
+
+static nrto_err fail(nrto_err code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static nrto_err cuda_fail(cudaError_t e, const char* where) {
+  return fail(NRTO_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CK(call)                                               \
+  do {                                                         \
+    cudaError_t e_ = (call);                                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);        \
+  } while (0)
+
+extern "C" const char* nrto_last_error(void) { return g_err.c_str(); }
+
+extern "C" void nrto_default_params(nrto_params* p) {
+  if (!p) return;
+  p->rho = 10.0; p->rho_admm = 40.0; p->alpha_dr = 0.9; p->sigma_dr = 1e-6; p->r_s = 1.0;
+  p->eps_p = 1e-3; p->eps_d = 1e-3; p->eps_dr = 1e-4;
+  p->rho_qp = 1.0; p->sigma_qp = 1e-6; p->alpha_qp = 1.6;
+  p->max_iter = 40; p->max_admm_iter = 40; p->max_dr_iter = 100; p->qp_iters = 10;
+  p->check_every = 1; p->fixed_iters = 0;
+}
+
+static nrto_err check_shape(const nrto_shape* s) {
+  if (!s) return fail(NRTO_EINVAL, "shape is NULL");
+  if (s->n_x < 1 || s->n_x > 32) return fail(NRTO_EINVAL, "n_x must be in [1,32]");
+  if (s->n_u < 1 || s->n_u > s->n_x) return fail(NRTO_EINVAL, "n_u must be in [1,n_x]");
+  if (s->T < 1) return fail(NRTO_EINVAL, "T must be >= 1");
+  if (s->n_g < 0) return fail(NRTO_EINVAL, "n_g must be >= 0");
+  if (s->batch < 1) return fail(NRTO_EINVAL, "batch must be >= 1");
+  if (s->n_g > 0 && (!s->cone_knot || !s->cone_kind))
+    return fail(NRTO_EINVAL, "cone_knot / cone_kind are NULL");
+  for (int j = 0; j < s->n_g; ++j) {
+    const int k = s->cone_knot[j], kd = s->cone_kind[j];
+    if (kd == 0 && (k < 1 || k > s->T))
+      return fail(NRTO_EINVAL, "state cone " + std::to_string(j) + ": knot must be in 1..T");
+    if (kd == 1 && (k < 0 || k > s->T - 1))
+      return fail(NRTO_EINVAL, "control cone " + std::to_string(j) + ": knot must be in 0..T-1");
+    if (kd != 0 && kd != 1) return fail(NRTO_EINVAL, "cone_kind must be 0 or 1");
+  }
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_layout(const nrto_shape* s, int64_t* E_out, int64_t* off) {
+  nrto_err e = check_shape(s);
+  if (e != NRTO_OK) return e;
+  int64_t acc = 0;
+  for (int j = 0; j < s->n_g; ++j) {
+    if (off) off[j] = acc;
+    acc += (s->cone_kind[j] == 0) ? (int64_t)(s->cone_knot[j] + 1) * s->n_x : s->n_x;
+  }
+  if (off) off[s->n_g] = acc;
+  if (E_out) *E_out = acc;
+  return NRTO_OK;
+}
+
+template <class T>
+static nrto_err dalloc(nrto_handle_s* h, T** p, int64_t n) {
+  if (h->nallocs >= (int)(sizeof(h->allocs) / sizeof(h->allocs[0])))
+    return fail(NRTO_ENOMEM, "too many allocations");
+  void* q = nullptr;
+  const size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(NRTO_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  }
+  h->allocs[h->nallocs++] = q;
+  *p = (T*)q;
+  return NRTO_OK;
+}
+
+static void free_all(nrto_handle_s* h) {
+  for (int i = 0; i < h->nallocs; ++i) cudaFree(h->allocs[i]);
+  h->nallocs = 0;
+}
+
+#define AL(ptr, n)                                 \
+  do {                                             \
+    nrto_err e_ = dalloc(h, &(ptr), (int64_t)(n)); \
+    if (e_ != NRTO_OK) { free_all(h); delete h; return e_; } \
+  } while (0)
+
+extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
+                               const nrto_params* prm, void* stream, nrto_handle* out) {
+  if (!out) return fail(NRTO_EINVAL, "out handle pointer is NULL");
+  *out = nullptr;
+  nrto_err e = check_shape(s);
+  if (e != NRTO_OK) return e;
+  if (!data || !prm) return fail(NRTO_EINVAL, "data / params is NULL");
+  if (!data->A || !data->B || !data->Psi || !data->tau || !data->W_K || !data->R_u ||
+      !data->u_hat || !data->r_trust || (s->n_g > 0 && (!data->grad || !data->g0)))
+    return fail(NRTO_EINVAL, "a required data pointer is NULL");
+  if (prm->max_iter < 0 || prm->max_admm_iter < 0 || prm->max_dr_iter < 0 || prm->qp_iters < 0 ||
+      prm->check_every < 1)
+    return fail(NRTO_EINVAL, "iteration counts must be >= 0 and check_every >= 1");
+  if (!(prm->rho > 0) || !(prm->rho_admm > 0) || !(prm->rho_qp > 0) || !(prm->r_s > 0) ||
+      !(prm->sigma_dr >= 0) || !(prm->sigma_qp >= 0) || !(prm->alpha_dr > 0 && prm->alpha_dr < 2) ||
+      !(prm->alpha_qp > 0 && prm->alpha_qp < 2))
+    return fail(NRTO_EINVAL, "penalty / relaxation parameters out of range");
+  cudaStream_t st = (cudaStream_t)stream;
+
+  auto* h = new nrto_handle_s();
+  h->stream = st;
+  Dev& v = h->dev;
+  Dims& d = v.d;
+  d.nx = s->n_x; d.nu = s->n_u; d.T = s->T; d.ng = s->n_g; d.B = s->batch;
+  d.NK = d.T * d.nu * d.nx;
+  v.prm = *prm;
+  // ---- host-side layout and CSR lists
+  const int ng = d.ng, T = d.T, nx = d.nx, nu = d.nu;
+  std::vector<int64_t> off(ng + 1), offB(ng + 1);
+  int64_t eb = 0;
+  nrto_layout(s, &d.E, off.data());
+  for (int j = 0; j < ng; ++j) {
+    offB[j] = eb;
+    eb += (s->cone_kind[j] == 0) ? (int64_t)s->cone_knot[j] * nu : nu;
+  }
+  offB[ng] = eb;
+  d.EB = eb;
+  std::vector<int32_t> kptr(T + 1, 0), kcone, sptr(T + 2, 0), srow, cptr(T + 1, 0), crow;
+  for (int k = 0; k < T; ++k) {
+    kptr[k] = (int32_t)kcone.size();
+    for (int j = 0; j < ng; ++j) {
+      const bool st0 = s->cone_kind[j] == 0;
+      if ((st0 && s->cone_knot[j] > k) || (!st0 && s->cone_knot[j] == k)) kcone.push_back(j);
+    }
+  }
+  kptr[T] = (int32_t)kcone.size();
+  for (int k = 0; k <= T; ++k) {
+    sptr[k] = (int32_t)srow.size();
+    for (int j = 0; j < ng; ++j)
+      if (s->cone_kind[j] == 0 && s->cone_knot[j] == k) srow.push_back(j);
+  }
+  sptr[T + 1] = (int32_t)srow.size();
+  for (int k = 0; k < T; ++k) {
+    cptr[k] = (int32_t)crow.size();
+    for (int j = 0; j < ng; ++j)
+      if (s->cone_kind[j] == 1 && s->cone_knot[j] == k) crow.push_back(j);
+  }
+  cptr[T] = (int32_t)crow.size();
+  std::vector<int32_t> knot(s->cone_knot, s->cone_knot + ng), kind(ng);
+  for (int j = 0; j < ng; ++j) kind[j] = s->cone_kind[j];
+
+  const int64_t B = d.B;
+  int32_t *dknot, *dkind, *dkptr, *dkcone, *dsptr, *dsrow, *dcptr, *dcrow;
+  int64_t *doff, *doffB;
+  AL(dknot, ng); AL(dkind, ng); AL(doff, ng + 1); AL(doffB, ng + 1);
+  AL(dkptr, T + 1); AL(dkcone, kcone.size()); AL(dsptr, T + 2); AL(dsrow, srow.size());
+  AL(dcptr, T + 1); AL(dcrow, crow.size());
+  v.knot = dknot; v.kind = dkind; v.off = doff; v.offB = doffB; v.kptr = dkptr; v.kcone = dkcone;
+  v.sptr = dsptr; v.srow = dsrow; v.cptr = dcptr; v.crow = dcrow;
+  double *A, *Bm, *grad, *g0, *Psi, *tau, *W, *Ru, *uhat, *rtrust;
+  AL(A, B * T * nx * nx); AL(Bm, B * T * nx * nu); AL(grad, B * ng * nx); AL(g0, B * ng);
+  AL(Psi, B * (T + 1) * nx * nx); AL(tau, B); AL(W, B * T * nu * nu); AL(Ru, B * T * nu * nu);
+  AL(uhat, B * T * nu); AL(rtrust, B);
+  v.A = A; v.Bm = Bm; v.grad = grad; v.g0 = g0; v.Psi = Psi; v.tau = tau; v.W = W; v.Ru = Ru;
+  v.uhat = uhat; v.rtrust = rtrust;
+  AL(v.bhat, B * d.E); AL(v.Bd, B * d.EB); AL(v.Zb, B * T * nu * nx); AL(v.Lam, B * T * nu * nu);
+  AL(v.U, B * T * nx * nx);
+  for (EngineFactors* F : {&v.fa, &v.dr}) {
+    AL(F->V, B * T * nu * nu); AL(F->den, B * T * nu * nx); AL(F->Kf, B * T * nu * nx);
+    AL(F->Acl, B * T * nx * nx); AL(F->Hinv, B * T * nu * nu); AL(F->HB, B * T * nu * nx);
+  }
+  AL(v.Y, B * d.E); AL(v.s, B * ng); AL(v.tin, B * ng); AL(v.pt, B * ng); AL(v.ptprev, B * ng);
+  AL(v.p, B * ng); AL(v.lamp, B * ng); AL(v.K, B * d.NK); AL(v.Ccur, B * T * nx * nu);
+  AL(v.Cprev, B * T * nx * nu); AL(v.D, B * T * nx * nu); AL(v.Z, B * T * nu * nx);
+  AL(v.du, B * T * nu); AL(v.zl, B * ng); AL(v.yl, B * ng); AL(v.zb, B * (T + 1) * nx);
+  AL(v.yb, B * (T + 1) * nx); AL(v.rp, B * ng); AL(v.wq, B * ng); AL(v.rx, B * (T + 1) * nx);
+  AL(v.ru, B * T * nu); AL(v.kff, B * T * nu); AL(v.dxt, B * (T + 1) * nx); AL(v.dut, B * T * nu);
+  AL(v.Kt, B * d.NK); AL(v.pit, B * ng); AL(v.tt, B * ng); AL(v.rdr_part, B * ng); AL(v.rdr, B);
+  AL(v.dr_active, B); AL(v.status, B); AL(v.iters, B); AL(v.active, B); AL(v.r_p, B); AL(v.r_d, B);
+
+  // shape arrays (pageable host vectors: synchronous copies)
+  cudaError_t ce = cudaSuccess;
+  auto hup = [&](void* dst, const void* src, size_t bytes) {
+    if (ce == cudaSuccess && bytes) ce = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+  };
+  hup(dknot, knot.data(), ng * 4); hup(dkind, kind.data(), ng * 4);
+  hup(doff, off.data(), (ng + 1) * 8); hup(doffB, offB.data(), (ng + 1) * 8);
+  hup(dkptr, kptr.data(), (T + 1) * 4); hup(dkcone, kcone.data(), kcone.size() * 4);
+  hup(dsptr, sptr.data(), (T + 2) * 4); hup(dsrow, srow.data(), srow.size() * 4);
+  hup(dcptr, cptr.data(), (T + 1) * 4); hup(dcrow, crow.data(), crow.size() * 4);
+  if (ce != cudaSuccess) { free_all(h); delete h; return cuda_fail(ce, "nrto_setup shape upload"); }
+  nrto_err re = nrto_refresh(h, data, stream);
+  if (re != NRTO_OK) { free_all(h); delete h; return re; }
+  h->dr_fresh = 1;
+  *out = h;
+  return NRTO_OK;
+}
+
+
+extern "C" nrto_err nrto_refresh(nrto_handle h, const nrto_data* data, void* stream) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (!data) return fail(NRTO_EINVAL, "data is NULL");
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  const int ng = d.ng, T = d.T, nx = d.nx, nu = d.nu;
+  const int64_t B = d.B;
+  if (!data->A || !data->B || !data->Psi || !data->tau || !data->W_K || !data->R_u ||
+      !data->u_hat || !data->r_trust || (ng > 0 && (!data->grad || !data->g0)))
+    return fail(NRTO_EINVAL, "a required data pointer is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool hostin = data->memory == NRTO_MEM_HOST;
+  const size_t D8 = sizeof(double);
+  cudaError_t ce = cudaSuccess;
+  auto up = [&](const double* dst, const double* src, int64_t n) {
+    if (ce == cudaSuccess && n > 0)
+      ce = cudaMemcpyAsync((void*)dst, src, (size_t)n * D8,
+                           hostin ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st);
+  };
+  up(v.A, data->A, B * T * nx * nx); up(v.Bm, data->B, B * T * nx * nu);
+  up(v.grad, data->grad, B * ng * nx); up(v.g0, data->g0, B * ng);
+  up(v.Psi, data->Psi, B * (T + 1) * nx * nx); up(v.tau, data->tau, B);
+  up(v.W, data->W_K, B * T * nu * nu); up(v.Ru, data->R_u, B * T * nu * nu);
+  up(v.uhat, data->u_hat, B * T * nu); up(v.rtrust, data->r_trust, B);
+  if (ce != cudaSuccess) return cuda_fail(ce, "nrto_refresh upload");
+  ce = launch_setup(h, st);
+  if (ce != cudaSuccess) return cuda_fail(ce, "nrto_refresh kernels");
+  const int se = read_setup_error(st);   // synchronises the stream
+  ce = cudaGetLastError();
+  if (ce != cudaSuccess) return cuda_fail(ce, "nrto_refresh sync");
+  if (se) return fail(NRTO_ENOTSPD, se == 1 ? "W_K (+ sigma_dr/2) is not SPD" : "Riccati H_uu is not SPD");
+  h->dr_fresh = 1;
+  return NRTO_OK;
+}
+
+static cudaEvent_t prof_event(nrto_handle_s* h) {
+  cudaEvent_t e = nullptr;
+  if (!h->pool.empty()) { e = h->pool.back(); h->pool.pop_back(); return e; }
+  cudaEventCreate(&e);
+  return e;
+}
+
+static cudaError_t copy_out(void* dst, const void* src, size_t bytes, bool host, cudaStream_t st) {
+  if (!dst || bytes == 0) return cudaSuccess;
+  return cudaMemcpyAsync(dst, src, bytes, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                         st);
+}
+
+static int poll_active(nrto_handle_s* h, int32_t* dcount, int dr, cudaStream_t st, cudaError_t* ce) {
+  int32_t c = 0;
+  *ce = launch_count_active(h, dcount, dr, st);
+  if (*ce == cudaSuccess) *ce = cudaMemcpyAsync(&c, dcount, 4, cudaMemcpyDeviceToHost, st);
+  if (*ce == cudaSuccess) *ce = cudaStreamSynchronize(st);
+  return c;
+}
+
+extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_out* o,
+                                     void* stream) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (!o) return fail(NRTO_EINVAL, "out is NULL");
+  if (engine != NRTO_FULLADMM && engine != NRTO_DR) return fail(NRTO_EINVAL, "unknown engine");
+  cudaStream_t st = (cudaStream_t)stream;
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  const nrto_params& prm = v.prm;
+  const bool host = o->memory == NRTO_MEM_HOST;
+  const int64_t B = d.B;
+  const size_t D8 = sizeof(double);
+  // staging for kernel-written optional outputs when the caller wants host memory
+  double *nu_d = o->nu, *lam_d = o->lam_nu, *obj_d = o->objective, *mc_d = o->margin_cone,
+         *ml_d = o->margin_lin;
+  std::vector<void*> tmp;
+  auto stage = [&](double** p, int64_t n) -> nrto_err {
+    if (!*p || !host) return NRTO_OK;
+    void* q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, (size_t)std::max<int64_t>(n, 1) * D8, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(staging)");
+    tmp.push_back(q);
+    *p = (double*)q;
+    return NRTO_OK;
+  };
+  nrto_err ee;
+  if ((ee = stage(&nu_d, B * d.E)) != NRTO_OK) return ee;
+  if ((ee = stage(&lam_d, B * d.E)) != NRTO_OK) return ee;
+  if ((ee = stage(&obj_d, B)) != NRTO_OK) return ee;
+  if ((ee = stage(&mc_d, B * d.ng)) != NRTO_OK) return ee;
+  if ((ee = stage(&ml_d, B * d.ng)) != NRTO_OK) return ee;
+  int32_t* dcount = nullptr;
+  CK(cudaMallocAsync((void**)&dcount, 4, st));
+  tmp.push_back(dcount);
+
+  cudaError_t ce = cudaSuccess;
+  auto timed = [&](int cls, cudaError_t (*fn)(nrto_handle_s*, cudaStream_t)) -> cudaError_t {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (h->prof) { a = prof_event(h); b = prof_event(h); cudaEventRecord(a, st); }
+    cudaError_t e = fn(h, st);
+    if (h->prof) { cudaEventRecord(b, st); h->recs.push_back({cls, a, b}); }
+    return e;
+  };
+  auto timed_qp = [&](int eng, int l) -> cudaError_t {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (h->prof) { a = prof_event(h); b = prof_event(h); cudaEventRecord(a, st); }
+    cudaError_t e = launch_qp(h, eng, l, st);
+    if (h->prof) { cudaEventRecord(b, st); h->recs.push_back({NRTO_K_QP, a, b}); }
+    return e;
+  };
+  if (engine == NRTO_FULLADMM) {
+    CK(launch_fa_reset(h, st));
+    for (int l = 1; l <= prm.max_iter; ++l) {
+      CK(timed(NRTO_K_PASS, launch_fa_pass));
+      CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
+        return launch_adjoint(hh, hh->dev.Y, hh->dev.s, hh->dev.active, s2); }));
+      CK(timed(NRTO_K_GAIN, launch_fa_gain));
+      CK(timed_qp(NRTO_FULLADMM, l));
+      if (!prm.fixed_iters && l % prm.check_every == 0 && l < prm.max_iter) {
+        const int c = poll_active(h, dcount, 0, st, &ce);
+        if (ce != cudaSuccess) return cuda_fail(ce, "poll");
+        if (c == 0) break;
+      }
+    }
+  } else {
+    CK(launch_dr_reset(h, h->dr_fresh, st));
+    h->dr_fresh = 0;
+    for (int l = 1; l <= prm.max_admm_iter; ++l) {
+      CK(launch_dr_arm(h, st));
+      for (int m = 1; m <= prm.max_dr_iter; ++m) {
+        CK(timed(NRTO_K_GAIN, launch_dr_gain));
+        CK(timed(NRTO_K_PASS, launch_dr_pass));
+        CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
+          return launch_adjoint(hh, hh->dev.Y, nullptr, hh->dev.dr_active, s2); }));
+        CK(timed(NRTO_K_OTHER, launch_dr_reduce));
+        if (!prm.fixed_iters && (m % 4) == 0 && m < prm.max_dr_iter) {
+          const int c = poll_active(h, dcount, 1, st, &ce);
+          if (ce != cudaSuccess) return cuda_fail(ce, "poll");
+          if (c == 0) break;
+        }
+      }
+      CK(timed_qp(NRTO_DR, l));
+      if (!prm.fixed_iters && l % prm.check_every == 0 && l < prm.max_admm_iter) {
+        const int c = poll_active(h, dcount, 0, st, &ce);
+        if (ce != cudaSuccess) return cuda_fail(ce, "poll");
+        if (c == 0) break;
+      }
+    }
+  }
+  nrto_out od = *o;
+  od.nu = nu_d; od.lam_nu = lam_d; od.objective = obj_d; od.margin_cone = mc_d; od.margin_lin = ml_d;
+  CK(launch_finish(h, engine, &od, st));
+  CK(copy_out(o->kv, v.K, B * d.NK * D8, host, st));
+  CK(copy_out(o->du, v.du, B * d.T * d.nu * D8, host, st));
+  CK(copy_out(o->p, v.p, B * d.ng * D8, host, st));
+  CK(copy_out(o->p_tilde, v.pt, B * d.ng * D8, host, st));
+  CK(copy_out(o->lam_p, v.lamp, B * d.ng * D8, host, st));
+  CK(copy_out(o->iters, v.iters, B * 4, host, st));
+  CK(copy_out(o->status, v.status, B * 4, host, st));
+  CK(copy_out(o->r_p, v.r_p, B * D8, host, st));
+  CK(copy_out(o->r_d, v.r_d, B * D8, host, st));
+  if (host) {
+    CK(copy_out(o->nu, nu_d, B * d.E * D8, true, st));
+    CK(copy_out(o->lam_nu, lam_d, B * d.E * D8, true, st));
+    CK(copy_out(o->objective, obj_d, B * D8, true, st));
+    CK(copy_out(o->margin_cone, mc_d, B * d.ng * D8, true, st));
+    CK(copy_out(o->margin_lin, ml_d, B * d.ng * D8, true, st));
+  }
+  for (void* q : tmp) CK(cudaFreeAsync(q, st));
+  if (host) CK(cudaStreamSynchronize(st));
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_gain_update(nrto_handle h, const double* nu, const double* kv_prev,
+                                     double* kv_next, void* stream) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (!nu || !kv_prev || !kv_next) return fail(NRTO_EINVAL, "NULL argument");
+  CK(launch_gain_update(h, nu, kv_prev, kv_next, (cudaStream_t)stream));
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_soc_project(const double* t, const double* y, const int64_t* off,
+                                     int64_t n, double* to, double* yo, void* stream) {
+  if (n < 0) return fail(NRTO_EINVAL, "n_cones < 0");
+  if (n > 0 && (!t || !y || !off || !to || !yo)) return fail(NRTO_EINVAL, "NULL argument");
+  CK(launch_soc_project(t, y, off, n, to, yo, (cudaStream_t)stream));
+  return NRTO_OK;
+}
+
+extern "C" int64_t nrto_launch_count(nrto_handle h) { return h ? h->launches : 0; }
+
+extern "C" nrto_err nrto_destroy(nrto_handle h) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  cudaDeviceSynchronize();
+  for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  free_all(h);
+  delete h;
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_profile_enable(nrto_handle h, int32_t enable) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  h->prof = enable != 0;
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_profile_read(nrto_handle h, int32_t cls, double* total_ms,
+                                      int64_t* launches) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (cls < 0 || cls >= NRTO_K_COUNT) return fail(NRTO_EINVAL, "bad kernel class");
+  double tot = 0.0;
+  int64_t n = 0;
+  std::vector<nrto_prof_rec> keep;
+  for (auto& r : h->recs) {
+    if (r.cls != cls) { keep.push_back(r); continue; }
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    tot += ms;
+    ++n;
+    h->pool.push_back(r.a);
+    h->pool.push_back(r.b);
+  }
+  h->recs.swap(keep);
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = n;
+  return NRTO_OK;
+}

@@ -1,0 +1,140 @@
+// Internal declarations of libnrto (not part of the ABI; see include/nrto.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <vector>
+#include "../../include/nrto.h"
+
+namespace nrto {
+
+// Problem dimensions shared by every instance of a batch.
+struct Dims {
+  int nx, nu, T, ng, B;
+  int64_t E;    // ragged cone-row length (sum_j L_j)
+  int64_t EB;   // ragged B-data length (state: k_j n_u, control: n_u)
+  int NK;       // T n_u n_x
+};
+
+// Factors of one engine's per-step gain chain and QP Riccati sweep.
+struct EngineFactors {
+  double* V;     // [B][T][nu][nu]  generalized eigenvectors of (Lambda_k, W'_k)
+  double* den;   // [B][T][nu][nx]  1 / (2 + c tau sigma_a lambda_b)
+  double* Kf;    // [B][T][nu][nx]  Riccati feedback of the QP x-step
+  double* Acl;   // [B][T][nx][nx]  A_k - B_k Kf_k
+  double* Hinv;  // [B][T][nu][nu]  H_uu^{-1}
+  double* HB;    // [B][T][nu][nx]  H_uu^{-1} B_k^T
+};
+
+// Plain-old-data view of all device state, passed to kernels by value.
+struct Dev {
+  Dims d;
+  nrto_params prm;
+  // shape
+  const int32_t* knot; const int32_t* kind;
+  const int64_t* off; const int64_t* offB;
+  const int32_t* kptr; const int32_t* kcone;   // cones with a b-block at step k (k < T)
+  const int32_t* sptr; const int32_t* srow;    // state rows at knot k (k = 0..T)
+  const int32_t* cptr; const int32_t* crow;    // control rows at step k (k < T)
+  // primitives (device copies)
+  const double *A, *Bm, *grad, *g0, *Psi, *tau, *W, *Ru, *uhat, *rtrust;
+  // setup products
+  double* bhat;   // [B][E]  (control segments unused)
+  double* Bd;     // [B][EB]
+  double* Zb;     // [B][T][nu][nx]  sum_j b_{j,k} b_hat_{j,k}^T
+  double* Lam;    // [B][T][nu][nu]  sum_j b_{j,k} b_{j,k}^T
+  double* U;      // [B][T][nx][nx]  eigenvectors of Sigma_k = Psi_k^T Psi_k
+  EngineFactors fa, dr;
+  // iterate state
+  double* Y;      // [B][E] FullADMM: projection input y^l; DR: eta~
+  double* s;      // [B][ng] FullADMM: scale s^l of the last projection
+  double* tin;    // [B][ng] FullADMM: t = p + lam_p for the next projection
+  double* pt;     // [B][ng] p~ (FullADMM) / pi of the last prox (DR)
+  double* ptprev; // [B][ng]
+  double* p;      // [B][ng] QP x p-part (= p)
+  double* lamp;   // [B][ng] FullADMM lam_p (scaled) / DR lambda (unscaled)
+  double* K;      // [B][NK] k_v (column-major vec per step)
+  double* Ccur;   // [B][T][nx][nu]  sqrt(tau) Psi_k K_k^T for the current k_v
+  double* Cprev;  // [B][T][nx][nu]  for the previous k_v
+  double* D;      // [B][T][nx][nu]  2 Ccur - Cprev (FullADMM forward map)
+  double* Z;      // [B][T][nu][nx]  adjoint accumulator sum_j b (s y)^T
+  // QP state
+  double *du, *zl, *yl, *zb, *yb;     // [B][T][nu], [B][ng] x2, [B][T+1][nx] x2
+  double *rp, *wq, *rx, *ru, *kff, *dxt, *dut;  // scratch
+  // DR state
+  double *Kt, *pit, *tt, *rdr_part, *rdr;
+  int32_t* dr_active;
+  // per-instance control
+  int32_t *status, *iters, *active;
+  double *r_p, *r_d;
+};
+
+}  // namespace nrto
+
+struct nrto_prof_rec { int cls; cudaEvent_t a, b; };
+
+struct nrto_handle_s {
+  nrto::Dev dev;
+  int64_t launches = 0;
+  int dr_fresh = 1;
+  void* allocs[96];
+  int nallocs = 0;
+  cudaStream_t stream = 0;
+  // optional CUDA-event profiler (nrto_profile_enable)
+  int prof = 0;
+  std::vector<nrto_prof_rec> recs;
+  std::vector<cudaEvent_t> pool;
+};
+
+namespace nrto {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum for blockDim.x a multiple of 32 (<= 1024); all threads get it.
+__device__ __forceinline__ double block_sum(double v, double* sh /*[32]*/) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = (l < nw) ? sh[l] : 0.0;
+  r = warp_sum(r);
+  return r;
+}
+
+// SM Eq.(18): case order a <= t, a <= -t, otherwise (R13).
+// Returns t' and writes the scale s with y' = s y.
+__device__ __forceinline__ double soc_case(double t, double a, double* s) {
+  if (a <= t) { *s = 1.0; return t; }
+  if (a <= -t) { *s = 0.0; return 0.0; }
+  const double h = 0.5 * (t + a);
+  *s = h / a;
+  return h;
+}
+
+// Launchers (defined in the .cu files; return cudaGetLastError()).
+cudaError_t launch_setup(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_fa_reset(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_dr_reset(nrto_handle_s* h, int full, cudaStream_t st);
+cudaError_t launch_dr_arm(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_fa_pass(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_fa_gain(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_dr_gain(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_dr_pass(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_dr_reduce(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_qp(nrto_handle_s* h, int engine, int l, cudaStream_t st);
+cudaError_t launch_adjoint(nrto_handle_s* h, const double* y, const double* scale,
+                           const int32_t* act, cudaStream_t st);
+cudaError_t launch_finish(nrto_handle_s* h, int engine, const nrto_out* o, cudaStream_t st);
+cudaError_t launch_gain_update(nrto_handle_s* h, const double* nu, const double* kv_prev,
+                               double* kv_next, cudaStream_t st);
+cudaError_t launch_soc_project(const double* t, const double* y, const int64_t* off,
+                               int64_t n, double* to, double* yo, cudaStream_t st);
+cudaError_t launch_count_active(nrto_handle_s* h, int32_t* d_count, int dr, cudaStream_t st);
+int read_setup_error(cudaStream_t st);
+
+}  // namespace nrto

@@ -1,0 +1,518 @@
+// Per-iteration kernels of the inner loop and the
+// output/finish kernels.
+#include "common.cuh"
+
+namespace nrto {
+
+// Geometry of cone j's ragged row.
+struct ConeGeom {
+  int kind, knot, L, klo, nbB;
+  int64_t off, offB;
+};
+__device__ __forceinline__ ConeGeom cone_geom(const Dev& v, int j) {
+  ConeGeom g;
+  g.kind = v.kind[j];
+  g.knot = v.knot[j];
+  g.off = v.off[j];
+  g.offB = v.offB[j];
+  g.L = (g.kind == 0) ? (g.knot + 1) * v.d.nx : v.d.nx;
+  g.klo = (g.kind == 0) ? 0 : g.knot;
+  g.nbB = (g.kind == 0) ? g.knot : 1;
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// FullADMM fused pass: Block-1 (13) of iteration l, with the dual update (16)
+// of iteration l-1 folded in.  The stored per-cone row is the projection
+// input y^l = A_hat k_v^{l-1} + b_hat + lam_nu^{l-1}; with nu^{l-1} =
+// s^{l-1} y^{l-1} and (16), y^l = (2 C^{l-1} - C^{l-2}) b + b_hat +
+// (1 - s^{l-1}) y^{l-1}, where C_k = sqrt(tau) Psi_k K_k^T.
+// One warp per cone; norm by shuffle; closed-form projection.
+__global__ void k_fa_pass(Dev v) {
+  const Dims d = v.d;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= (int64_t)d.B * d.ng) return;
+  const int b = (int)(gw / d.ng), j = (int)(gw % d.ng);
+  if (!v.active[b]) return;
+  const int lane = threadIdx.x & 31;
+  const int nx = d.nx, nu = d.nu;
+  const ConeGeom g = cone_geom(v, j);
+  const int64_t ij = (int64_t)b * d.ng + j;
+  const double omsp = 1.0 - v.s[ij];
+  double* Y = v.Y + (int64_t)b * d.E + g.off;
+  const double* bh = v.bhat + (int64_t)b * d.E + g.off;
+  const double* Bd = v.Bd + (int64_t)b * d.EB + g.offB;
+  const double* Dm = v.D + (int64_t)b * d.T * nx * nu;
+  double n2 = 0.0;
+  for (int e = lane; e < g.L; e += 32) {
+    const int kb = e / nx, i = e - kb * nx;
+    double acc = (g.kind == 0) ? bh[e] : 0.0;
+    if (kb < g.nbB) {
+      const double* Dr = Dm + ((int64_t)(g.klo + kb) * nx + i) * nu;
+      const double* br = Bd + kb * nu;
+      for (int m = 0; m < nu; ++m) acc += Dr[m] * br[m];
+    }
+    const double y = acc + omsp * Y[e];
+    Y[e] = y;
+    n2 += y * y;
+  }
+  n2 = warp_sum(n2);
+  if (lane == 0) {
+    double s;
+    const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
+    v.s[ij] = s;
+    v.pt[ij] = tp;
+  }
+}
+
+// Adjoint reduction S7: Z_k[m][i] = sum_j scale_j b_{j,k}[m] y_{j,k}[i] over the
+// cones with a b-block at step k (fixed order).  With scale = s this is
+// sum_j b nu^T (FullADMM); with scale = NULL it is sum_j b eta~^T (DR).
+__global__ void k_adjoint(Dev v, const double* __restrict__ y, const double* __restrict__ scale,
+                          const int32_t* __restrict__ act) {
+  const Dims d = v.d;
+  const int b = blockIdx.x / d.T, k = blockIdx.x % d.T;
+  if (act && !act[b]) return;
+  const int nx = d.nx, nu = d.nu;
+  const double* yb = y + (int64_t)b * d.E;
+  const double* Bd = v.Bd + (int64_t)b * d.EB;
+  for (int o = threadIdx.x; o < nu * nx; o += blockDim.x) {
+    const int m = o / nx, i = o % nx;
+    double acc = 0.0;
+    for (int c = v.kptr[k]; c < v.kptr[k + 1]; ++c) {
+      const int j = v.kcone[c];
+      const int kb = (v.kind[j] == 0) ? k : 0;
+      double t = Bd[v.offB[j] + kb * nu + m] * yb[v.off[j] + kb * nx + i];
+      if (scale) t *= scale[(int64_t)b * d.ng + j];
+      acc += t;
+    }
+    v.Z[((int64_t)b * d.T + k) * nu * nx + o] = acc;
+  }
+}
+
+// Gain chain solve for one (instance, step): K = V [(V^T R U) ./ den] U^T,
+// R given in sR (nu x nx).  Uses scratch sX (nu x nx); nt threads cooperate.
+__device__ void chain_solve(const double* V, const double* U, const double* den,
+                            double* sR, double* sX, int nu, int nx, int tid, int nt) {
+  for (int r = tid; r < nu * nx; r += nt) {        // sX = V^T R
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+    for (int q = 0; q < nu; ++q) acc += V[q * nu + a] * sR[q * nx + c];
+    sX[r] = acc;
+  }
+  __syncthreads();
+  for (int r = tid; r < nu * nx; r += nt) {        // sR = (sX U) ./ den
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[q * nx + c];
+    sR[r] = acc * den[r];
+  }
+  __syncthreads();
+  for (int r = tid; r < nu * nx; r += nt) {        // sX = V sR
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+    for (int q = 0; q < nu; ++q) acc += V[a * nu + q] * sR[q * nx + c];
+    sX[r] = acc;
+  }
+  __syncthreads();
+  for (int r = tid; r < nu * nx; r += nt) {        // sR = sX U^T  (= K)
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[c * nx + q];
+    sR[r] = acc;
+  }
+  __syncthreads();
+}
+
+// FullADMM (14b) per (instance, step k):
+//   R = 2 W K^{l-1} + rho sqrt(tau) (Z - Zb) Psi_k   (= block k of
+//   Q_v k^{l-1} + rho sum_j A_hat_j^T (nu_j - b_hat_j))
+//   K^l = M_k R (chain), C^l = sqrt(tau) Psi_k K^lT, D = 2 C^l - C^{l-1}.
+// mode 0: in-loop (updates K, C, D).  mode 1: nrto_gain_update (kin -> kout).
+__global__ void k_fa_gain(Dev v, int mode, const double* kin, double* kout) {
+  extern __shared__ double sm[];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu;
+  const int b = blockIdx.x / d.T, k = blockIdx.x % d.T;
+  if (mode == 0 && !v.active[b]) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t bk = (int64_t)b * d.T + k;
+  double* sR = sm;
+  double* sX = sR + nu * nx;
+  double* sK = sX + nu * nx;
+  const double st = sqrt(v.tau[b]);
+  const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + k) * nx * nx;
+  const double* Wk = v.W + bk * nu * nu;
+  const double* Kp = (mode == 0 ? v.K : kin) + (int64_t)b * d.NK + (int64_t)k * nu * nx;
+  for (int r = tid; r < nu * nx; r += nt) {   // G = Z - Zb into sX ; K_prev into sK
+    sX[r] = v.Z[bk * nu * nx + r] - v.Zb[bk * nu * nx + r];
+    const int m = r / nx, i = r % nx;
+    sK[r] = Kp[i * nu + m];
+  }
+  __syncthreads();
+  const double rho = v.prm.rho;
+  for (int r = tid; r < nu * nx; r += nt) {
+    const int m = r / nx, i = r % nx;
+    double gp = 0.0, wk = 0.0;
+    for (int q = 0; q < nx; ++q) gp += sX[m * nx + q] * Pk[q * nx + i];
+    for (int q = 0; q < nu; ++q) wk += Wk[m * nu + q] * sK[q * nx + i];
+    sR[r] = 2.0 * wk + rho * st * gp;
+  }
+  __syncthreads();
+  chain_solve(v.fa.V + bk * nu * nu, v.U + bk * nx * nx, v.fa.den + bk * nu * nx, sR, sX,
+              nu, nx, tid, nt);
+  double* Ko = (mode == 0 ? v.K : kout) + (int64_t)b * d.NK + (int64_t)k * nu * nx;
+  for (int r = tid; r < nu * nx; r += nt) {
+    const int m = r / nx, i = r % nx;
+    Ko[i * nu + m] = sR[r];
+  }
+  if (mode != 0) return;
+  for (int r = tid; r < nx * nu; r += nt) {   // C = sqrt(tau) Psi K^T ; D = 2C - Cold
+    const int i = r / nu, m = r % nu;
+    double acc = 0.0;
+    for (int q = 0; q < nx; ++q) acc += Pk[i * nx + q] * sR[m * nx + q];
+    const double c = st * acc;
+    const int64_t idx = bk * nx * nu + r;
+    const double cold = v.Ccur[idx];
+    v.Cprev[idx] = cold;
+    v.Ccur[idx] = c;
+    v.D[idx] = 2.0 * c - cold;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// DR engine.  Affine prox (11a) via the Schur form of K_KKT (F3):
+//   (Q_v + sigma I + r_s sum A^T A) k = sigma k~ + r_s sum A^T (eta~ - b_hat)
+// per step k: R = sigma K~ + r_s sqrt(tau) (Z - Zb) Psi_k, chain with (W+sigma/2, r_s);
+// then chi~ += alpha (chi - chi~) for the k_v part (11c).
+__global__ void k_dr_gain(Dev v) {
+  extern __shared__ double sm[];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu;
+  const int b = blockIdx.x / d.T, k = blockIdx.x % d.T;
+  if (!v.active[b] || !v.dr_active[b]) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t bk = (int64_t)b * d.T + k;
+  double* sR = sm;
+  double* sX = sR + nu * nx;
+  const double st = sqrt(v.tau[b]);
+  const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + k) * nx * nx;
+  double* Kt = v.Kt + (int64_t)b * d.NK + (int64_t)k * nu * nx;
+  const double sg = v.prm.sigma_dr, rs = v.prm.r_s, al = v.prm.alpha_dr;
+  for (int r = tid; r < nu * nx; r += nt) sX[r] = v.Z[bk * nu * nx + r] - v.Zb[bk * nu * nx + r];
+  __syncthreads();
+  for (int r = tid; r < nu * nx; r += nt) {
+    const int m = r / nx, i = r % nx;
+    double gp = 0.0;
+    for (int q = 0; q < nx; ++q) gp += sX[m * nx + q] * Pk[q * nx + i];
+    sR[r] = sg * Kt[i * nu + m] + rs * st * gp;
+  }
+  __syncthreads();
+  chain_solve(v.dr.V + bk * nu * nu, v.U + bk * nx * nx, v.dr.den + bk * nu * nx, sR, sX,
+              nu, nx, tid, nt);
+  double* Ko = v.K + (int64_t)b * d.NK + (int64_t)k * nu * nx;
+  for (int r = tid; r < nu * nx; r += nt) {
+    const int m = r / nx, i = r % nx;
+    Ko[i * nu + m] = sR[r];
+    Kt[i * nu + m] += al * (sR[r] - Kt[i * nu + m]);
+  }
+  for (int r = tid; r < nx * nu; r += nt) {
+    const int i = r / nu, m = r % nu;
+    double acc = 0.0;
+    for (int q = 0; q < nx; ++q) acc += Pk[i * nx + q] * sR[m * nx + q];
+    v.Ccur[bk * nx * nu + r] = st * acc;
+  }
+}
+
+// DR cone step, one warp per cone:
+//   pi = (sigma pi~ + rho p + lambda + r_s t~)/(rho + sigma + r_s)  (p~ part of (11a))
+//   s = (pi, a), a = A_hat k + b_hat ; s_ref = 2 s - s~ ; s~ += alpha (Pi(s_ref) - s)
+//   pi~ += alpha (pi - pi~) ; r_dr partial = ||s~_new - s~||^2
+__global__ void k_dr_pass(Dev v) {
+  const Dims d = v.d;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= (int64_t)d.B * d.ng) return;
+  const int b = (int)(gw / d.ng), j = (int)(gw % d.ng);
+  if (!v.active[b] || !v.dr_active[b]) return;
+  const int lane = threadIdx.x & 31;
+  const int nx = d.nx, nu = d.nu;
+  const ConeGeom g = cone_geom(v, j);
+  const int64_t ij = (int64_t)b * d.ng + j;
+  const double sg = v.prm.sigma_dr, rs = v.prm.r_s, al = v.prm.alpha_dr, rho = v.prm.rho_admm;
+  const double pit = v.pit[ij], tt = v.tt[ij];
+  const double pi = (sg * pit + rho * v.p[ij] + v.lamp[ij] + rs * tt) / (rho + sg + rs);
+  double* Y = v.Y + (int64_t)b * d.E + g.off;
+  const double* bh = v.bhat + (int64_t)b * d.E + g.off;
+  const double* Bd = v.Bd + (int64_t)b * d.EB + g.offB;
+  const double* Cm = v.Ccur + (int64_t)b * d.T * nx * nu;
+  double n2 = 0.0;
+  for (int e = lane; e < g.L; e += 32) {
+    const int kb = e / nx, i = e - kb * nx;
+    double a = (g.kind == 0) ? bh[e] : 0.0;
+    if (kb < g.nbB) {
+      const double* Cr = Cm + ((int64_t)(g.klo + kb) * nx + i) * nu;
+      const double* br = Bd + kb * nu;
+      for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
+    }
+    const double er = 2.0 * a - Y[e];
+    n2 += er * er;
+  }
+  n2 = warp_sum(n2);
+  double sc;
+  const double tpi = soc_case(2.0 * pi - tt, sqrt(n2), &sc);
+  double d2 = 0.0;
+  for (int e = lane; e < g.L; e += 32) {
+    const int kb = e / nx, i = e - kb * nx;
+    double a = (g.kind == 0) ? bh[e] : 0.0;
+    if (kb < g.nbB) {
+      const double* Cr = Cm + ((int64_t)(g.klo + kb) * nx + i) * nu;
+      const double* br = Bd + kb * nu;
+      for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
+    }
+    const double et = Y[e];
+    const double er = 2.0 * a - et;
+    const double en = et + al * (sc * er - a);
+    Y[e] = en;
+    d2 += (en - et) * (en - et);
+  }
+  d2 = warp_sum(d2);
+  if (lane == 0) {
+    const double ttn = tt + al * (tpi - pi);
+    d2 += (ttn - tt) * (ttn - tt);
+    v.tt[ij] = ttn;
+    v.pit[ij] = pit + al * (pi - pit);
+    v.pt[ij] = pi;
+    v.rdr_part[ij] = d2;
+  }
+}
+
+// r_dr = ||s~^l - s~^{l-1}||_2 per instance; DR stop test.
+__global__ void k_dr_reduce(Dev v) {
+  __shared__ double sh[32];
+  const Dims d = v.d;
+  const int b = blockIdx.x;
+  if (!v.active[b] || !v.dr_active[b]) return;
+  double acc = 0.0;
+  for (int j = threadIdx.x; j < d.ng; j += blockDim.x) acc += v.rdr_part[(int64_t)b * d.ng + j];
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    const double r = sqrt(acc);
+    v.rdr[b] = r;
+    if (!v.prm.fixed_iters && r <= v.prm.eps_dr) v.dr_active[b] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Finish: per cone outputs.  FullADMM: nu^L = s y^L,
+// lam_nu^L = (1 - s) y^L + (C^L - C^{L-1}) b  ( = lam^{L-1} + a(k^L) - nu^L ).
+// Both engines: margin_cone = p~ - ||C^L b + b_hat||.
+__global__ void k_finish_cones(Dev v, int engine, double* nu_out, double* lam_out,
+                               double* mc_out) {
+  const Dims d = v.d;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= (int64_t)d.B * d.ng) return;
+  const int b = (int)(gw / d.ng), j = (int)(gw % d.ng);
+  const int lane = threadIdx.x & 31;
+  const int nx = d.nx, nu = d.nu;
+  const ConeGeom g = cone_geom(v, j);
+  const int64_t ij = (int64_t)b * d.ng + j;
+  const double* Y = v.Y + (int64_t)b * d.E + g.off;
+  const double* bh = v.bhat + (int64_t)b * d.E + g.off;
+  const double* Bd = v.Bd + (int64_t)b * d.EB + g.offB;
+  const double* Cc = v.Ccur + (int64_t)b * d.T * nx * nu;
+  const double* Cp = v.Cprev + (int64_t)b * d.T * nx * nu;
+  const double s = v.s[ij];
+  double n2 = 0.0;
+  for (int e = lane; e < g.L; e += 32) {
+    const int kb = e / nx, i = e - kb * nx;
+    double a = (g.kind == 0) ? bh[e] : 0.0, dlt = 0.0;
+    if (kb < g.nbB) {
+      const int64_t r = ((int64_t)(g.klo + kb) * nx + i) * nu;
+      const double* br = Bd + kb * nu;
+      for (int m = 0; m < nu; ++m) { a += Cc[r + m] * br[m]; dlt += (Cc[r + m] - Cp[r + m]) * br[m]; }
+    }
+    n2 += a * a;
+    if (engine == NRTO_FULLADMM) {
+      const double y = Y[e];
+      if (nu_out) nu_out[(int64_t)b * d.E + g.off + e] = s * y;
+      if (lam_out) lam_out[(int64_t)b * d.E + g.off + e] = (1.0 - s) * y + dlt;
+    }
+  }
+  n2 = warp_sum(n2);
+  if (lane == 0 && mc_out) mc_out[ij] = v.pt[ij] - sqrt(n2);
+}
+
+// Finish per instance: dx = F_u du by rollout, margin_lin, objective J.
+__global__ void k_finish_inst(Dev v, double* ml_out, double* obj_out) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu;
+  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  double* dx = sm;   // (T+1)*nx
+  const double* du = v.du + (int64_t)b * d.T * nu;
+  for (int r = tid; r < nx; r += nt) dx[r] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < d.T; ++k) {
+    const double* A = v.A + ((int64_t)b * d.T + k) * nx * nx;
+    const double* B = v.Bm + ((int64_t)b * d.T + k) * nx * nu;
+    for (int i = tid; i < nx; i += nt) {
+      double acc = 0.0;
+      for (int q = 0; q < nx; ++q) acc += A[i * nx + q] * dx[k * nx + q];
+      for (int q = 0; q < nu; ++q) acc += B[i * nu + q] * du[k * nu + q];
+      dx[(k + 1) * nx + i] = acc;
+    }
+    __syncthreads();
+  }
+  if (ml_out) {
+    const double* grad = v.grad + (int64_t)b * d.ng * nx;
+    for (int j = tid; j < d.ng; j += nt) {
+      const int k = v.knot[j];
+      double bd = 0.0;
+      if (v.kind[j] == 0) for (int q = 0; q < nx; ++q) bd += grad[j * nx + q] * dx[k * nx + q];
+      else for (int q = 0; q < nu; ++q) bd += grad[j * nx + q] * du[k * nu + q];
+      const int64_t ij = (int64_t)b * d.ng + j;
+      ml_out[ij] = -(v.g0[ij] + bd + v.p[ij]);
+    }
+  }
+  if (obj_out) {
+    double acc = 0.0;
+    for (int r = tid; r < d.T * nu; r += nt) {       // (u_hat + du)^T R_u (u_hat + du)
+      const int k = r / nu, m = r % nu;
+      const double* Ru = v.Ru + ((int64_t)b * d.T + k) * nu * nu;
+      const double* uh = v.uhat + ((int64_t)b * d.T + k) * nu;
+      double rr = 0.0;
+      for (int q = 0; q < nu; ++q) rr += Ru[m * nu + q] * (uh[q] + du[k * nu + q]);
+      acc += (uh[m] + du[k * nu + m]) * rr;
+    }
+    const double* Kb = v.K + (int64_t)b * d.NK;
+    for (int r = tid; r < d.NK; r += nt) {           // 1/2 k^T Q_v k = sum <K, W K>
+      const int k = r / (nu * nx), rem = r % (nu * nx), i = rem / nu, m = rem % nu;
+      const double* Wk = v.W + ((int64_t)b * d.T + k) * nu * nu;
+      double wk = 0.0;
+      for (int q = 0; q < nu; ++q) wk += Wk[m * nu + q] * Kb[k * nu * nx + i * nu + q];
+      acc += Kb[r] * wk;
+    }
+    acc = block_sum(acc, red);
+    if (tid == 0) obj_out[b] = acc;
+  }
+}
+
+__global__ void k_count_active(Dev v, int32_t* out, int dr) {
+  __shared__ double sh[32];
+  double c = 0.0;
+  for (int b = threadIdx.x; b < v.d.B; b += blockDim.x)
+    c += (v.active[b] && (!dr || v.dr_active[b])) ? 1.0 : 0.0;
+  c = block_sum(c, sh);
+  if (threadIdx.x == 0) *out = (int32_t)c;
+}
+
+// Standalone batched SOC projection (nrto_soc_project).
+__global__ void k_soc_project(const double* t, const double* y, const int64_t* off, int64_t n,
+                              double* to, double* yo) {
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t a = off[w], e = off[w + 1];
+  double n2 = 0.0;
+  for (int64_t r = a + lane; r < e; r += 32) n2 += y[r] * y[r];
+  n2 = warp_sum(n2);
+  double s;
+  const double tp = soc_case(t[w], sqrt(n2), &s);
+  for (int64_t r = a + lane; r < e; r += 32) yo[r] = s * y[r];
+  if (lane == 0) to[w] = tp;
+}
+
+// ---------------------------------------------------------------------------
+static inline unsigned warp_grid(int64_t warps, int wpb) {
+  return (unsigned)((warps + wpb - 1) / wpb);
+}
+
+cudaError_t launch_adjoint(nrto_handle_s* h, const double* y, const double* scale,
+                           const int32_t* act, cudaStream_t st) {
+  Dev& v = h->dev;
+  k_adjoint<<<v.d.B * v.d.T, 128, 0, st>>>(v, y, scale, act);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fa_pass(nrto_handle_s* h, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  if ((int64_t)d.B * d.ng > 0) {
+    k_fa_pass<<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(v);
+    h->launches++;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fa_gain(nrto_handle_s* h, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  k_fa_gain<<<d.B * d.T, 128, 3 * d.nu * d.nx * sizeof(double), st>>>(v, 0, nullptr, nullptr);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dr_gain(nrto_handle_s* h, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  k_dr_gain<<<d.B * d.T, 128, 2 * d.nu * d.nx * sizeof(double), st>>>(v);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dr_pass(nrto_handle_s* h, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  if ((int64_t)d.B * d.ng > 0) {
+    k_dr_pass<<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(v);
+    h->launches++;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dr_reduce(nrto_handle_s* h, cudaStream_t st) {
+  k_dr_reduce<<<h->dev.d.B, 128, 0, st>>>(h->dev);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finish(nrto_handle_s* h, int engine, const nrto_out* o, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  if ((int64_t)d.B * d.ng > 0) {
+    k_finish_cones<<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(
+        v, engine, o->nu, o->lam_nu, o->margin_cone);
+    h->launches++;
+  }
+  k_finish_inst<<<d.B, 128, (d.T + 1) * d.nx * sizeof(double), st>>>(v, o->margin_lin,
+                                                                      o->objective);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gain_update(nrto_handle_s* h, const double* nu, const double* kv_prev,
+                               double* kv_next, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  k_adjoint<<<d.B * d.T, 128, 0, st>>>(v, nu, nullptr, nullptr);
+  h->launches++;
+  k_fa_gain<<<d.B * d.T, 128, 3 * d.nu * d.nx * sizeof(double), st>>>(v, 1, kv_prev, kv_next);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_soc_project(const double* t, const double* y, const int64_t* off, int64_t n,
+                               double* to, double* yo, cudaStream_t st) {
+  if (n > 0) k_soc_project<<<warp_grid(n, 8), 256, 0, st>>>(t, y, off, n, to, yo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_active(nrto_handle_s* h, int32_t* d_count, int dr, cudaStream_t st) {
+  k_count_active<<<1, 256, 0, st>>>(h->dev, d_count, dr);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace nrto

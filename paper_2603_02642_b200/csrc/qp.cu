@@ -1,0 +1,263 @@
+// (14a) / (5b) QP by OSQP-form ADMM with a Riccati x-step (DESIGN R1),
+// fused with the dual update and the residual / termination test of the outer
+// iteration: FullADMM (16) + P:505-507, or NRTO-ADMM (5c).
+#include "common.cuh"
+
+namespace nrto {
+
+// One CTA per instance.  x = (du, p), z = (z_lin, z_ball), y dual.
+//   rhs_p = sigma p + rho v + rho_q z_lin - y_lin
+//   w     = rho_q z_lin - y_lin - beta rhs_p,           beta = rho_q/(rho+sigma+rho_q)
+//   (R~ + F_u^T Q~ F_u) du~ = r_u + F_u^T r_x  with r_u = sigma du - 2 R_u u_hat + scatter_ctrl(w),
+//                                                  r_x = scatter_state(w) + rho_q z_ball - y_ball
+//   p~' = (rhs_p - rho_q B du~)/(rho+sigma+rho_q),  z~ = (B du~ + p~', F_u du~)
+//   x <- a x~ + (1-a) x ; z <- Pi(a z~ + (1-a) z + y/rho_q) ; y += rho_q (a z~ + (1-a) z - z_new)
+__global__ void __launch_bounds__(128) k_qp(Dev v, int engine, int l) {
+  __shared__ double sv[2][32];
+  __shared__ double red[32];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, T = d.T, ng = d.ng;
+  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  if (!v.active[b]) return;
+  const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
+  const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
+  const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp, aq = v.prm.alpha_qp;
+  const double den = rho + sq + rq, beta = rq / den;
+  const int64_t bg = (int64_t)b * ng;
+  const double* grad = v.grad + bg * nx;
+  const double* g0 = v.g0 + bg;
+  double* p = v.p + bg; double* zl = v.zl + bg; double* yl = v.yl + bg;
+  double* rp = v.rp + bg; double* wq = v.wq + bg;
+  const double* pt = v.pt + bg; double* lam = v.lamp + bg;
+  double* zb = v.zb + (int64_t)b * (T + 1) * nx; double* yb = v.yb + (int64_t)b * (T + 1) * nx;
+  double* rx = v.rx + (int64_t)b * (T + 1) * nx; double* dxt = v.dxt + (int64_t)b * (T + 1) * nx;
+  double* du = v.du + (int64_t)b * T * nu; double* ru = v.ru + (int64_t)b * T * nu;
+  double* kff = v.kff + (int64_t)b * T * nu; double* dut = v.dut + (int64_t)b * T * nu;
+  const double* Ru = v.Ru + (int64_t)b * T * nu * nu;
+  const double* uh = v.uhat + (int64_t)b * T * nu;
+  const double* Bm = v.Bm + (int64_t)b * T * nx * nu;
+  const double* Kf = F.Kf + (int64_t)b * T * nu * nx;
+  const double* Acl = F.Acl + (int64_t)b * T * nx * nx;
+  const double* Hi = F.Hinv + (int64_t)b * T * nu * nu;
+  const double* HB = F.HB + (int64_t)b * T * nu * nx;
+  const double rtr = v.rtrust[b];
+  const double rinv = (engine == NRTO_FULLADMM) ? 1.0 : 1.0 / rho;
+
+  for (int it = 0; it < v.prm.qp_iters; ++it) {
+    for (int j = tid; j < ng; j += nt) {
+      const double vj = pt[j] - lam[j] * rinv;   // FullADMM: p~ - lam_p ; DR: p~ - lambda/rho
+      const double r = sq * p[j] + rho * vj + rq * zl[j] - yl[j];
+      rp[j] = r;
+      wq[j] = rq * zl[j] - yl[j] - beta * r;
+    }
+    __syncthreads();
+    for (int r = tid; r < (T + 1) * nx; r += nt) {
+      const int k = r / nx, i = r % nx;
+      double acc = 0.0;
+      if (k > 0) {
+        acc = rq * zb[r] - yb[r];
+        for (int q = v.sptr[k]; q < v.sptr[k + 1]; ++q) {
+          const int j = v.srow[q];
+          acc += grad[j * nx + i] * wq[j];
+        }
+      }
+      rx[r] = acc;
+    }
+    for (int r = tid; r < T * nu; r += nt) {
+      const int k = r / nu, m = r % nu;
+      double acc = sq * du[r];
+      for (int q = 0; q < nu; ++q) acc -= 2.0 * Ru[(k * nu + m) * nu + q] * uh[k * nu + q];
+      for (int q = v.cptr[k]; q < v.cptr[k + 1]; ++q) {
+        const int j = v.crow[q];
+        acc += grad[j * nx + m] * wq[j];
+      }
+      ru[r] = acc;
+    }
+    __syncthreads();
+    // backward sweep: s_k = r_x,k + Acl_k^T s_{k+1} - Kf_k^T r_u,k ;
+    //                 kff_k = H_uu^-1 r_u,k + H_uu^-1 B_k^T s_{k+1}
+    int cur = 0;
+    if (tid < nx) sv[0][tid] = rx[T * nx + tid];
+    __syncthreads();
+    for (int k = T - 1; k >= 0; --k) {
+      const double* s = sv[cur];
+      if (tid < nx) {
+        const double* Ac = Acl + (int64_t)k * nx * nx;
+        const double* Kk = Kf + (int64_t)k * nu * nx;
+        double acc = rx[k * nx + tid];
+        for (int r = 0; r < nx; ++r) acc += Ac[r * nx + tid] * s[r];
+        for (int m = 0; m < nu; ++m) acc -= Kk[m * nx + tid] * ru[k * nu + m];
+        sv[cur ^ 1][tid] = acc;
+      } else if (tid >= 32 && tid < 32 + nu) {
+        const int m = tid - 32;
+        const double* H = Hi + (int64_t)k * nu * nu;
+        const double* hb = HB + (int64_t)k * nu * nx;
+        double acc = 0.0;
+        for (int q = 0; q < nu; ++q) acc += H[m * nu + q] * ru[k * nu + q];
+        for (int r = 0; r < nx; ++r) acc += hb[m * nx + r] * s[r];
+        kff[k * nu + m] = acc;
+      }
+      __syncthreads();
+      cur ^= 1;
+    }
+    // forward sweep: du~_k = kff_k - Kf_k dx_k ; dx_{k+1} = Acl_k dx_k + B_k kff_k
+    if (tid < nx) dxt[tid] = 0.0;
+    __syncthreads();
+    for (int k = 0; k < T; ++k) {
+      const double* x = dxt + k * nx;
+      if (tid < nx) {
+        const double* Ac = Acl + (int64_t)k * nx * nx;
+        const double* Bk = Bm + (int64_t)k * nx * nu;
+        double acc = 0.0;
+        for (int r = 0; r < nx; ++r) acc += Ac[tid * nx + r] * x[r];
+        for (int m = 0; m < nu; ++m) acc += Bk[tid * nu + m] * kff[k * nu + m];
+        dxt[(k + 1) * nx + tid] = acc;
+      } else if (tid >= 32 && tid < 32 + nu) {
+        const int m = tid - 32;
+        const double* Kk = Kf + (int64_t)k * nu * nx;
+        double acc = kff[k * nu + m];
+        for (int r = 0; r < nx; ++r) acc -= Kk[m * nx + r] * x[r];
+        dut[k * nu + m] = acc;
+      }
+      __syncthreads();
+    }
+    // linear rows
+    for (int j = tid; j < ng; j += nt) {
+      const int k = v.knot[j];
+      double bd = 0.0;
+      if (v.kind[j] == 0) for (int q = 0; q < nx; ++q) bd += grad[j * nx + q] * dxt[k * nx + q];
+      else for (int q = 0; q < nu; ++q) bd += grad[j * nx + q] * dut[k * nu + q];
+      const double ptl = (rp[j] - rq * bd) / den;
+      const double ztl = bd + ptl;
+      p[j] = aq * ptl + (1.0 - aq) * p[j];
+      const double zh = aq * ztl + (1.0 - aq) * zl[j];
+      const double zn = fmin(zh + yl[j] / rq, -g0[j]);
+      yl[j] += rq * (zh - zn);
+      zl[j] = zn;
+    }
+    for (int r = tid; r < T * nu; r += nt) du[r] = aq * dut[r] + (1.0 - aq) * du[r];
+    __syncthreads();   // dxt is overwritten below
+    // trust-region ball on F_u du (all knots; knot 0 is identically 0)
+    double nb = 0.0;
+    for (int r = tid; r < (T + 1) * nx; r += nt) {
+      const double zh = aq * dxt[r] + (1.0 - aq) * zb[r];
+      dxt[r] = zh;
+      const double w = zh + yb[r] / rq;
+      nb += w * w;
+    }
+    nb = sqrt(block_sum(nb, red));
+    const double scl = (nb > rtr) ? rtr / nb : 1.0;
+    for (int r = tid; r < (T + 1) * nx; r += nt) {
+      const double zh = dxt[r];
+      const double zn = scl * (zh + yb[r] / rq);
+      yb[r] += rq * (zh - zn);
+      zb[r] = zn;
+    }
+    __syncthreads();
+  }
+  // ---- dual update + residuals of the outer iteration
+  double ap = 0.0, ad = 0.0;
+  double* tin = v.tin + bg;
+  double* ptp = v.ptprev + bg;
+  for (int j = tid; j < ng; j += nt) {
+    const double dp = p[j] - pt[j];
+    if (engine == NRTO_FULLADMM) {       // (16): lam_p += p - p~ ; next t = p + lam_p
+      lam[j] += dp;
+      tin[j] = p[j] + lam[j];
+    } else {                              // (5c): lambda += rho (p - p~)   (R4)
+      lam[j] += rho * dp;
+    }
+    ap += dp * dp;
+    const double dd = pt[j] - ptp[j];
+    ad += dd * dd;
+    ptp[j] = pt[j];
+  }
+  ap = block_sum(ap, red);
+  ad = block_sum(ad, red);
+  if (tid == 0) {
+    const double rpv = sqrt(ap), rdv = rho * sqrt(ad);
+    v.r_p[b] = rpv;
+    v.r_d[b] = rdv;
+    v.iters[b] = l;
+    if (!isfinite(rpv) || !isfinite(rdv)) {
+      v.status[b] = NRTO_DIVERGED;
+      v.active[b] = 0;
+    } else if (!v.prm.fixed_iters && (l % v.prm.check_every) == 0 && rpv <= v.prm.eps_p &&
+               rdv <= v.prm.eps_d) {
+      v.status[b] = NRTO_CONVERGED;
+      v.active[b] = 0;
+    }
+  }
+}
+
+cudaError_t launch_qp(nrto_handle_s* h, int engine, int l, cudaStream_t st) {
+  k_qp<<<h->dev.d.B, 128, 0, st>>>(h->dev, engine, l);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+__global__ void k_reset_inst(Dev v, int engine) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= v.d.B) return;
+  v.status[b] = NRTO_MAX_ITERS;
+  v.iters[b] = 0;
+  v.active[b] = 1;
+  v.dr_active[b] = 1;
+  v.r_p[b] = INFINITY;
+  v.r_d[b] = INFINITY;
+  v.rdr[b] = INFINITY;
+}
+
+__global__ void k_dr_arm(Dev v) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < v.d.B) v.dr_active[b] = v.active[b];
+}
+
+static cudaError_t zero(nrto_handle_s* h, double* p, int64_t n, cudaStream_t st) {
+  return cudaMemsetAsync(p, 0, n * sizeof(double), st);
+}
+
+cudaError_t launch_fa_reset(nrto_handle_s* h, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  const int64_t B = d.B;
+  zero(h, v.Y, B * d.E, st);
+  zero(h, v.s, B * d.ng, st); zero(h, v.tin, B * d.ng, st); zero(h, v.pt, B * d.ng, st);
+  zero(h, v.ptprev, B * d.ng, st); zero(h, v.p, B * d.ng, st); zero(h, v.lamp, B * d.ng, st);
+  zero(h, v.K, B * d.NK, st);
+  zero(h, v.Ccur, B * d.T * d.nx * d.nu, st); zero(h, v.Cprev, B * d.T * d.nx * d.nu, st);
+  zero(h, v.D, B * d.T * d.nx * d.nu, st);
+  zero(h, v.du, B * d.T * d.nu, st); zero(h, v.zl, B * d.ng, st); zero(h, v.yl, B * d.ng, st);
+  zero(h, v.zb, B * (d.T + 1) * d.nx, st); zero(h, v.yb, B * (d.T + 1) * d.nx, st);
+  k_reset_inst<<<(d.B + 127) / 128, 128, 0, st>>>(v, NRTO_FULLADMM);
+  h->launches++;
+  h->dr_fresh = 1;   // Y / Z now hold FullADMM state
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dr_reset(nrto_handle_s* h, int full, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  const int64_t B = d.B;
+  if (full) {          // DR warm state (chi~, s~) and Z = adjoint(eta~ = 0)
+    zero(h, v.Y, B * d.E, st); zero(h, v.tt, B * d.ng, st); zero(h, v.pit, B * d.ng, st);
+    zero(h, v.Kt, B * d.NK, st); zero(h, v.Z, B * d.T * d.nu * d.nx, st);
+  }
+  zero(h, v.pt, B * d.ng, st); zero(h, v.ptprev, B * d.ng, st); zero(h, v.p, B * d.ng, st);
+  zero(h, v.lamp, B * d.ng, st); zero(h, v.K, B * d.NK, st);
+  zero(h, v.Ccur, B * d.T * d.nx * d.nu, st); zero(h, v.Cprev, B * d.T * d.nx * d.nu, st);
+  zero(h, v.s, B * d.ng, st);
+  zero(h, v.du, B * d.T * d.nu, st); zero(h, v.zl, B * d.ng, st); zero(h, v.yl, B * d.ng, st);
+  zero(h, v.zb, B * (d.T + 1) * d.nx, st); zero(h, v.yb, B * (d.T + 1) * d.nx, st);
+  k_reset_inst<<<(d.B + 127) / 128, 128, 0, st>>>(v, NRTO_DR);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dr_arm(nrto_handle_s* h, cudaStream_t st) {
+  k_dr_arm<<<(h->dev.d.B + 127) / 128, 128, 0, st>>>(h->dev);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace nrto

