@@ -39,7 +39,7 @@ def gpu_solve(shape, batch, engine, memory=nrto.NRTO_MEM_DEVICE, **pkw):
 
 
 def single(shape, data):
-    return stack_instances([(shape, data)])
+    return stack_instances([(shape, data)])[1]
 
 
 def oracle_run(shape, data, engine, **pkw):
@@ -86,10 +86,11 @@ def test_soc_project_parity():
     to, yo = to.cpu().numpy(), yo.cpu().numpy()
     for j in range(len(lens)):
         tr, yr = proj_soc(t[j], y[off[j]:off[j + 1]])
-        assert to[j] == pytest.approx(tr, rel=1e-14, abs=1e-300)
-        np.testing.assert_allclose(yo[off[j]:off[j + 1]], yr, rtol=1e-14, atol=1e-300)
-    nrto.nrto_soc_project(dt[:0], dy, doff, to[:0] if False else torch.empty(0, device="cuda"),
-                          dy) if False else None
+        # the map is continuous: at a = +-t the reduction order of ||y|| may pick
+        # the neighbouring case, which differs by O(ulp * (|t| + a))
+        sc = 1e-14 * (abs(t[j]) + np.linalg.norm(y[off[j]:off[j + 1]]))
+        assert abs(to[j] - tr) <= sc + 1e-14 * abs(tr)
+        np.testing.assert_allclose(yo[off[j]:off[j + 1]], yr, rtol=1e-14, atol=sc)
 
 
 # ----------------------------------------------------------- gain update
