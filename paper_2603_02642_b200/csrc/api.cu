@@ -2,6 +2,7 @@
 // host orchestration of the inner loop.  No C++ exception crosses the ABI.
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -126,9 +127,10 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   std::vector<int64_t> off(ng + 1), offB(ng + 1);
   int64_t eb = 0;
   nrto_layout(s, &d.E, off.data());
+  d.nup = nu + (nu & 1);
   for (int j = 0; j < ng; ++j) {
     offB[j] = eb;
-    eb += (s->cone_kind[j] == 0) ? (int64_t)s->cone_knot[j] * nu : nu;
+    eb += (s->cone_kind[j] == 0) ? (int64_t)s->cone_knot[j] * d.nup : d.nup;
   }
   offB[ng] = eb;
   d.EB = eb;
@@ -155,6 +157,53 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   cptr[T] = (int32_t)crow.size();
   std::vector<int32_t> knot(s->cone_knot, s->cone_knot + ng), kind(ng);
   for (int j = 0; j < ng; ++j) kind[j] = s->cone_kind[j];
+  // ---- tiles of <= 8 cones with equal (kind, knot) for the fused pass, and
+  //      work items = contiguous tile ranges of one instance balanced by elements
+  std::vector<int32_t> tiles;
+  std::vector<int64_t> tile_work;
+  auto add_group = [&](int kd, int kn) {
+    std::vector<int32_t> cs;
+    for (int j = 0; j < ng; ++j)
+      if (s->cone_kind[j] == kd && s->cone_knot[j] == kn) cs.push_back(j);
+    for (size_t a = 0; a < cs.size(); a += 8) {
+      const int nc = (int)std::min<size_t>(8, cs.size() - a);
+      tiles.push_back(kd); tiles.push_back(kn); tiles.push_back(nc);
+      tiles.push_back(kd == 0 ? 0 : kn);
+      for (int c = 0; c < 8; ++c) tiles.push_back(c < nc ? cs[a + c] : 0);
+      tile_work.push_back((int64_t)nc * ((kd == 0 ? kn + 1 : 1) * nx + (kd == 0 ? kn : 1) * nu));
+    }
+  };
+  for (int kn = 1; kn <= T; ++kn) add_group(0, kn);
+  const int nstate_tiles = (int)tile_work.size();
+  for (int kn = 0; kn < T; ++kn) add_group(1, kn);
+  int nctrl = 0;
+  for (int j = 0; j < ng; ++j) nctrl += (s->cone_kind[j] == 1);
+  // path: TMA-pipelined state pass + exact control kernel when the geometry allows
+  const bool use_tma = tma_supported(d);
+  const int ntiles = use_tma ? nstate_tiles : (int)tile_work.size();
+  int nsm = 148;
+  { int dev = 0; if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); cudaGetLastError(); }
+  int64_t work_tot = 0;
+  for (int t = 0; t < ntiles; ++t) work_tot += tile_work[t];
+  const int64_t zbytes = 16LL * T * nu * nx;
+  const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, work_tot / std::max<int64_t>(zbytes, 1)));
+  int nsplit = (int)std::min<int64_t>(smax, std::max<int64_t>(1, (6LL * 2 * nsm + d.B - 1) / d.B));
+  if (ntiles == 0) nsplit = 1;
+  std::vector<int32_t> witems;
+  for (int b = 0; b < d.B && ntiles > 0; ++b) {
+    int t = 0;
+    int64_t acc = 0;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const int64_t goal = work_tot * (sp + 1) / nsplit;
+      const int t0 = t;
+      while (t < ntiles && (acc + tile_work[t] <= goal || t == t0)) acc += tile_work[t++];
+      if (sp == nsplit - 1) { while (t < ntiles) acc += tile_work[t++]; }
+      witems.push_back(b); witems.push_back(t0); witems.push_back(t); witems.push_back(sp);
+    }
+  }
+  v.fused = use_tma ? 2 : ((fused_supported(d) && ntiles > 0) ? 1 : 0);
+  v.nctrl = nctrl;
+  v.ntiles = ntiles; v.nsplit = nsplit; v.nwitems = (int)(witems.size() / 4);
 
   const int64_t B = d.B;
   int32_t *dknot, *dkind, *dkptr, *dkcone, *dsptr, *dsrow, *dcptr, *dcrow;
@@ -184,6 +233,12 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   AL(v.ru, B * T * nu); AL(v.kff, B * T * nu); AL(v.dxt, B * (T + 1) * nx); AL(v.dut, B * T * nu);
   AL(v.Kt, B * d.NK); AL(v.pit, B * ng); AL(v.tt, B * ng); AL(v.rdr_part, B * ng); AL(v.rdr, B);
   AL(v.dr_active, B); AL(v.status, B); AL(v.iters, B); AL(v.active, B); AL(v.r_p, B); AL(v.r_d, B);
+  int32_t *dtiles, *dwitems;
+  AL(dtiles, tiles.size()); AL(dwitems, witems.size());
+  v.tiles = dtiles; v.witems = dwitems;
+  AL(v.Zpart, (v.fused ? B * nsplit : 1) * T * nu * nx); AL(v.Zc, B * T * nu * nx);
+  AL(v.Zctrl, B * T * nu * nx);
+  AL(v.clist, B * ng); AL(v.cw, B * ng); AL(v.ncorr, B);
 
   // shape arrays (pageable host vectors: synchronous copies)
   cudaError_t ce = cudaSuccess;
@@ -195,6 +250,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   hup(dkptr, kptr.data(), (T + 1) * 4); hup(dkcone, kcone.data(), kcone.size() * 4);
   hup(dsptr, sptr.data(), (T + 2) * 4); hup(dsrow, srow.data(), srow.size() * 4);
   hup(dcptr, cptr.data(), (T + 1) * 4); hup(dcrow, crow.data(), crow.size() * 4);
+  hup(dtiles, tiles.data(), tiles.size() * 4); hup(dwitems, witems.data(), witems.size() * 4);
   if (ce != cudaSuccess) { free_all(h); delete h; return cuda_fail(ce, "nrto_setup shape upload"); }
   nrto_err re = nrto_refresh(h, data, stream);
   if (re != NRTO_OK) { free_all(h); delete h; return re; }
@@ -313,9 +369,21 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
   if (engine == NRTO_FULLADMM) {
     CK(launch_fa_reset(h, st));
     for (int l = 1; l <= prm.max_iter; ++l) {
-      CK(timed(NRTO_K_PASS, launch_fa_pass));
-      CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
-        return launch_adjoint(hh, hh->dev.Y, hh->dev.s, hh->dev.active, s2); }));
+      if (v.fused == 2) {
+        CK(timed(NRTO_K_PASS, launch_fa_tma));
+        CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
+          Dev& w = hh->dev;
+          return launch_zlist(hh, w.Y, w.clist, w.cw, nullptr, w.ncorr, 0, w.active, w.Zc, s2); }));
+      } else if (v.fused == 1) {
+        CK(timed(NRTO_K_PASS, launch_fa_fused));
+        CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
+          Dev& w = hh->dev;
+          return launch_zlist(hh, w.Y, w.clist, w.cw, nullptr, w.ncorr, 0, w.active, w.Zc, s2); }));
+      } else {
+        CK(timed(NRTO_K_PASS, launch_fa_pass));
+        CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
+          return launch_adjoint(hh, hh->dev.Y, hh->dev.s, hh->dev.active, s2); }));
+      }
       CK(timed(NRTO_K_GAIN, launch_fa_gain));
       CK(timed_qp(NRTO_FULLADMM, l));
       if (!prm.fixed_iters && l % prm.check_every == 0 && l < prm.max_iter) {

@@ -11,7 +11,8 @@ namespace nrto {
 struct Dims {
   int nx, nu, T, ng, B;
   int64_t E;    // ragged cone-row length (sum_j L_j)
-  int64_t EB;   // ragged B-data length (state: k_j n_u, control: n_u)
+  int64_t EB;   // ragged B-data length (state: k_j nup, control: nup)
+  int nup;      // B-data row stride: n_u rounded up to even (16-byte rows for TMA)
   int NK;       // T n_u n_x
 };
 
@@ -66,6 +67,19 @@ struct Dev {
   // per-instance control
   int32_t *status, *iters, *active;
   double *r_p, *r_d;
+  // fused FullADMM pass (fused.cu)
+  int fused;               // 0: generic k_fa_pass + adjoint; 1: k_fa_fused_r (all tiles) +
+                           // correction; 2: k_fa_tma (state tiles) + k_fa_ctrl + correction
+  int nctrl;               // number of control cones
+  double* Zctrl;           // [B][T][nu][nx] exact adjoint of the control cones (fused == 2)
+  int ntiles, nsplit, nwitems;
+  const int32_t* tiles;    // [ntiles][12] kind, knot, nc, klo, cone[8]
+  const int32_t* witems;   // [nwitems][4] b, t0, t1, split index
+  double* Zpart;           // [B][nsplit][T][nu][nx] per-work-item adjoint partials
+  double* Zc;              // [B][T][nu][nx] correction adjoint
+  int32_t* clist;          // [B][ng] mispredicted cones of the last pass
+  double* cw;              // [B][ng] their weights s^l - shat
+  int32_t* ncorr;          // [B]
 };
 
 }  // namespace nrto
@@ -136,5 +150,12 @@ cudaError_t launch_soc_project(const double* t, const double* y, const int64_t* 
                                int64_t n, double* to, double* yo, cudaStream_t st);
 cudaError_t launch_count_active(nrto_handle_s* h, int32_t* d_count, int dr, cudaStream_t st);
 int read_setup_error(cudaStream_t st);
+cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
+                         const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,
+                         double* Zout, cudaStream_t st);
+bool fused_supported(const Dims& d);
+bool tma_supported(const Dims& d);
+cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st);
 
 }  // namespace nrto

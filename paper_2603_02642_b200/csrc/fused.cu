@@ -1,0 +1,540 @@
+// Fused FullADMM cone pass (S3 forward map + S4 SOC projection + S5 state
+// update + S7 adjoint) in ONE streaming pass over the ragged cone data, with
+// both small contractions on the FP64 tensor cores (DMMA m8n8k4).
+//
+// Work decomposition.  Cones with the same (kind, knot) are grouped into tiles
+// of <= 8 (host side, nrto_setup).  A CTA (8 warps) walks a range of tiles of
+// one instance; warp w owns the time blocks k == w (mod 8) of every tile, so
+// the per-step adjoint accumulator Z_k lives in a warp-private slice of shared
+// memory and is never contended.
+//
+// Per (tile, block k) a warp computes, for the <= 8 cones c of the tile,
+//   y_new[c][k][:] = D_k b_{c,k} + b_hat_{c,k} + (1 - s^{l-1}_c) y_old[c][k][:]
+// (see k_fa_pass in iter.cu for the derivation) as one DMMA chain
+// [8 cones x 4 m] x [4 m x 8 i] (rows = cones, cols = state index i), writes
+// y_new, accumulates ||y_new||^2 per cone, and adds the PREDICTED adjoint
+//   Z_k += sum_c shat_c b_{c,k} y_new[c][k]^T,   shat_c = [s^{l-1}_c == 1]
+// as a second DMMA chain [8 m x 4 cones] x [4 cones x 8 i].  The exact adjoint
+// needs s^l_c, known only after the whole cone; cones whose s^l differs from
+// shat (case-3 cones and case switches; all cones at l = 1) are appended to a
+// correction list and added by k_zcorr with weight s^l - shat.  For cones in
+// case 1 at consecutive iterations (the large majority near convergence) the
+// prediction is exact, so the pass streams every cone element exactly once:
+// algorithmic bytes 8 (2E + E_s + E_B) per instance-iteration.
+#include "common.cuh"
+
+namespace nrto {
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+constexpr int kRing = 4;      // tile slots in flight per CTA (norm partials)
+constexpr int kTileInts = 12; // kind, knot, nc, klo, cone[8]
+
+// NTI: 8-wide tiles over the state index i (n_x <= 8 NTI);
+// NKS: 4-deep k-steps over the control index m (n_u <= 4 NKS).
+template <int NTI, int NKS>
+__global__ void __launch_bounds__(256, 2)
+k_fa_fused(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems) {
+  extern __shared__ double sm[];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, T = d.T;
+  constexpr int ZW = 8 * NTI;                        // padded Z row width
+  double* Zs = sm;                                   // [T][8][ZW]
+  double* ring = Zs + (size_t)T * 8 * ZW;            // [kRing][8 warps][8 cones]
+  int* cnt = (int*)(ring + kRing * 64);              // [kRing]
+  int* tag = cnt + kRing;                            // [kRing]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int b = witems[4 * blockIdx.x], t0 = witems[4 * blockIdx.x + 1];
+  const int t1 = witems[4 * blockIdx.x + 2], sidx = witems[4 * blockIdx.x + 3];
+  if (!v.active[b]) return;                          // uniform over the CTA
+  for (int r = threadIdx.x; r < T * 8 * ZW; r += blockDim.x) Zs[r] = 0.0;
+  if (threadIdx.x < kRing) { cnt[threadIdx.x] = 0; tag[threadIdx.x] = threadIdx.x; }
+  __syncthreads();
+
+  const double* __restrict__ bhat = v.bhat + (int64_t)b * d.E;
+  const double* __restrict__ Bd = v.Bd + (int64_t)b * d.EB;
+  const double* __restrict__ Dm = v.D + (int64_t)b * T * nx * nu;
+  double* __restrict__ Y = v.Y + (int64_t)b * d.E;
+  const int64_t bg = (int64_t)b * d.ng;
+  const bool vec2 = (nx & 1) == 0;
+
+  for (int t = t0; t < t1; ++t) {
+    const int* tl = tiles + (int64_t)t * kTileInts;
+    const int kind = tl[0], K = tl[1], nc = tl[2], klo = tl[3];
+    const int nblk = K - klo + 1;                    // blocks in each cone row
+    const int first = klo + ((warp - klo) % 8 + 8) % 8;
+    if (first > K) continue;                         // this warp owns no block of the tile
+    const int lt = t - t0, slot = lt % kRing;
+    // per-lane cone meta: C/A layout cone = g ; A2/B2 layout cones q, q+4
+    const bool gv = g < nc;
+    const int cg = gv ? tl[4 + g] : 0;
+    const int64_t offg = gv ? v.off[cg] : 0, offBg = gv ? v.offB[cg] : 0;
+    const double omsp = gv ? 1.0 - v.s[bg + cg] : 0.0;
+    int64_t offB2[2];     // the adjoint DMMA contracts over the tile's 8 cones: 2 steps of 4
+    double sh2[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int c2 = q + 4 * ks;
+      const bool c2v = c2 < nc;
+      const int cc = c2v ? tl[4 + c2] : 0;
+      offB2[ks] = c2v ? v.offB[cc] : 0;
+      sh2[ks] = (c2v && v.s[bg + cc] == 1.0) ? 1.0 : 0.0;   // shat = [s^{l-1} == 1]
+    }
+    double nrm = 0.0;
+    for (int k = first; k <= K; k += 8) {
+      const int kb = k - klo;
+      const bool hasB = (kind == 0) ? (k < K) : true;
+      double c[NTI][2];
+      // ---- C init: b_hat + (1 - s) y_old
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) {
+        const int i0 = 2 * q + 8 * nt;
+        c[nt][0] = 0.0; c[nt][1] = 0.0;
+        if (gv && i0 < nx) {
+          const int64_t e = offg + (int64_t)kb * nx + i0;
+          if (vec2) {
+            const double2 yo = *reinterpret_cast<const double2*>(Y + e);
+            c[nt][0] = omsp * yo.x; c[nt][1] = omsp * yo.y;
+            if (kind == 0) {
+              const double2 bh = __ldg(reinterpret_cast<const double2*>(bhat + e));
+              c[nt][0] += bh.x; c[nt][1] += bh.y;
+            }
+          } else {
+            c[nt][0] = omsp * Y[e] + (kind == 0 ? __ldg(bhat + e) : 0.0);
+            if (i0 + 1 < nx) c[nt][1] = omsp * Y[e + 1] + (kind == 0 ? __ldg(bhat + e + 1) : 0.0);
+          }
+        }
+      }
+      if (hasB) {
+        // ---- forward map: y += [b_{c,k}]_(c,m) [D_k^T]_(m,i)
+        const int kbB = (kind == 0) ? kb : 0;
+        double a[NKS];
+#pragma unroll
+        for (int ks = 0; ks < NKS; ++ks) {
+          const int m = q + 4 * ks;
+          a[ks] = (gv && m < nu) ? __ldg(Bd + offBg + (int64_t)kbB * d.nup + m) : 0.0;
+        }
+        const double* Dk = Dm + (int64_t)k * nx * nu;
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) {
+#pragma unroll
+          for (int ks = 0; ks < NKS; ++ks) {
+            const int m = q + 4 * ks, i = g + 8 * nt;
+            const double bb = (m < nu && i < nx) ? __ldg(Dk + i * nu + m) : 0.0;
+            dmma(c[nt], a[ks], bb);
+          }
+        }
+      }
+      // ---- store y_new, norm partial
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) {
+        const int i0 = 2 * q + 8 * nt;
+        if (gv && i0 < nx) {
+          const int64_t e = offg + (int64_t)kb * nx + i0;
+          if (vec2) {
+            *reinterpret_cast<double2*>(Y + e) = make_double2(c[nt][0], c[nt][1]);
+          } else {
+            Y[e] = c[nt][0];
+            if (i0 + 1 < nx) Y[e + 1] = c[nt][1];
+          }
+        }
+        nrm += c[nt][0] * c[nt][0] + c[nt][1] * c[nt][1];
+      }
+      if (hasB) {
+        // ---- predicted adjoint: Z_k += [shat_c b_{c,k,m}]_(m,c) [y_{c,k,i}]_(c,i)
+        const int kbB = (kind == 0) ? kb : 0;
+        double a2[2];
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+          a2[ks] = (g < nu && sh2[ks] != 0.0) ? __ldg(Bd + offB2[ks] + (int64_t)kbB * d.nup + g) : 0.0;
+        double* Zk = Zs + (size_t)k * 8 * ZW;
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) {
+          double z[2] = {Zk[g * ZW + 2 * q + 8 * nt], Zk[g * ZW + 2 * q + 8 * nt + 1]};
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            // B2[row = cone q+4ks][col = i = g + 8nt] lives in lane (q+4ks)*4 + g/2, slot g&1
+            const int src = (q + 4 * ks) * 4 + (g >> 1);
+            const double v0 = __shfl_sync(0xffffffffu, c[nt][0], src);
+            const double v1 = __shfl_sync(0xffffffffu, c[nt][1], src);
+            dmma(z, a2[ks], (g & 1) ? v1 : v0);
+          }
+          Zk[g * ZW + 2 * q + 8 * nt] = z[0];
+          Zk[g * ZW + 2 * q + 8 * nt + 1] = z[1];
+        }
+      }
+    }
+    // ---- per-cone norm partial of this warp -> ring slot; last warp projects
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+    if (lane == 0) {
+      while (atomicAdd(&tag[slot], 0) != lt) { __nanosleep(20); }
+    }
+    __syncwarp();
+    if (q == 0) ring[(slot * 8 + warp) * 8 + g] = nrm;
+    __threadfence_block();
+    __syncwarp();
+    int last = 0;
+    const int npart = nblk >= 8 ? 8 : nblk;
+    if (lane == 0) last = (atomicAdd(&cnt[slot], 1) == npart - 1);
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
+      if (lane < nc) {
+        double n2 = 0.0;
+        for (int w = 0; w < 8; ++w)
+          if (((w - klo) % 8 + 8) % 8 <= K - klo) n2 += ring[(slot * 8 + w) * 8 + lane];
+        const int cj = tl[4 + lane];
+        const int64_t ij = bg + cj;
+        const double shat = (v.s[ij] == 1.0) ? 1.0 : 0.0;
+        double s;
+        const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
+        v.s[ij] = s;
+        v.pt[ij] = tp;
+        if (s != shat) {
+          const int pos = atomicAdd(&v.ncorr[b], 1);
+          v.clist[bg + pos] = cj;
+          v.cw[bg + pos] = s - shat;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        cnt[slot] = 0;
+        __threadfence_block();
+        atomicExch(&tag[slot], lt + kRing);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- flush the warp-private Z slices: Zpart[b][sidx][k][m][i]
+  double* Zp = v.Zpart + ((int64_t)b * v.nsplit + sidx) * T * nu * nx;
+  for (int r = threadIdx.x; r < T * nu * nx; r += blockDim.x) {
+    const int k = r / (nu * nx), rem = r % (nu * nx), m = rem / nx, i = rem % nx;
+    Zp[r] = Zs[((size_t)k * 8 + m) * ZW + i];
+  }
+}
+
+// Register-resident variant (T <= 16 KK): 16 warps, warp w owns the blocks
+// k == w (mod 16) of every tile, its Z_k slices (KK of them) live in
+// registers, the k-loop is fully unrolled so the loads of later blocks are
+// hoisted over the DMMA chains of earlier ones.  Shared memory holds only the
+// norm ring, leaving L1 to cache the per-step D_k fragments and b rows.
+template <int NTI, int NKS, int KK>
+__global__ void __launch_bounds__(512, 1)
+k_fa_fused_r(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems) {
+  constexpr int NW = 16;
+  __shared__ double ring[kRing * NW * 8];
+  __shared__ int cnt[kRing], tag[kRing];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, T = d.T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int b = witems[4 * blockIdx.x], t0 = witems[4 * blockIdx.x + 1];
+  const int t1 = witems[4 * blockIdx.x + 2], sidx = witems[4 * blockIdx.x + 3];
+  if (!v.active[b]) return;
+  if (threadIdx.x < kRing) { cnt[threadIdx.x] = 0; tag[threadIdx.x] = threadIdx.x; }
+  __syncthreads();
+  const double* __restrict__ bhat = v.bhat + (int64_t)b * d.E;
+  const double* __restrict__ Bd = v.Bd + (int64_t)b * d.EB;
+  const double* __restrict__ Dm = v.D + (int64_t)b * T * nx * nu;
+  double* __restrict__ Y = v.Y + (int64_t)b * d.E;
+  const int64_t bg = (int64_t)b * d.ng;
+  const bool vec2 = (nx & 1) == 0;
+  double z[KK][NTI][2];
+#pragma unroll
+  for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+    for (int nt = 0; nt < NTI; ++nt) { z[kk][nt][0] = 0.0; z[kk][nt][1] = 0.0; }
+
+  for (int t = t0; t < t1; ++t) {
+    const int* tl = tiles + (int64_t)t * kTileInts;
+    const int kind = tl[0], K = tl[1], nc = tl[2], klo = tl[3];
+    const int nblk = K - klo + 1;
+    const int first = klo + ((warp - klo) % NW + NW) % NW;
+    if (first > K) continue;
+    const int lt = t - t0, slot = lt % kRing;
+    const bool gv = g < nc;
+    const int cg = gv ? tl[4 + g] : 0;
+    const int64_t offg = gv ? v.off[cg] : 0, offBg = gv ? v.offB[cg] : 0;
+    const double omsp = gv ? 1.0 - v.s[bg + cg] : 0.0;
+    int64_t offB2[2];
+    double sh2[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int c2 = q + 4 * ks;
+      const bool c2v = c2 < nc;
+      const int cc = c2v ? tl[4 + c2] : 0;
+      offB2[ks] = c2v ? v.offB[cc] : 0;
+      sh2[ks] = (c2v && v.s[bg + cc] == 1.0) ? 1.0 : 0.0;
+    }
+    double nrm = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk) {     // absolute slot: k = warp + NW kk (Z slice z[kk])
+      const int k = warp + NW * kk;
+      if (k > K) break;
+      if (k < klo) continue;
+      const int kb = k - klo;
+      const bool hasB = (kind == 0) ? (k < K) : true;
+      const int kbB = (kind == 0) ? kb : 0;
+      double c[NTI][2];
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) {
+        const int i0 = 2 * q + 8 * nt;
+        c[nt][0] = 0.0; c[nt][1] = 0.0;
+        if (gv && i0 < nx) {
+          const int64_t e = offg + (int64_t)kb * nx + i0;
+          if (vec2) {
+            const double2 yo = __ldcs(reinterpret_cast<const double2*>(Y + e));
+            c[nt][0] = omsp * yo.x; c[nt][1] = omsp * yo.y;
+            if (kind == 0) {
+              const double2 bh = __ldcs(reinterpret_cast<const double2*>(bhat + e));
+              c[nt][0] += bh.x; c[nt][1] += bh.y;
+            }
+          } else {
+            c[nt][0] = omsp * Y[e] + (kind == 0 ? __ldg(bhat + e) : 0.0);
+            if (i0 + 1 < nx) c[nt][1] = omsp * Y[e + 1] + (kind == 0 ? __ldg(bhat + e + 1) : 0.0);
+          }
+        }
+      }
+      double a[NKS], a2[2];
+      if (hasB) {
+#pragma unroll
+        for (int ks = 0; ks < NKS; ++ks) {
+          const int m = q + 4 * ks;
+          a[ks] = (gv && m < nu) ? __ldg(Bd + offBg + (int64_t)kbB * d.nup + m) : 0.0;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+          a2[ks] = (g < nu && sh2[ks] != 0.0) ? __ldg(Bd + offB2[ks] + (int64_t)kbB * d.nup + g) : 0.0;
+        const double* Dk = Dm + (int64_t)k * nx * nu;
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) {
+#pragma unroll
+          for (int ks = 0; ks < NKS; ++ks) {
+            const int m = q + 4 * ks, i = g + 8 * nt;
+            const double bb = (m < nu && i < nx) ? __ldg(Dk + i * nu + m) : 0.0;
+            dmma(c[nt], a[ks], bb);
+          }
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) {
+        const int i0 = 2 * q + 8 * nt;
+        if (gv && i0 < nx) {
+          const int64_t e = offg + (int64_t)kb * nx + i0;
+          if (vec2) {
+            __stcs(reinterpret_cast<double2*>(Y + e), make_double2(c[nt][0], c[nt][1]));
+          } else {
+            Y[e] = c[nt][0];
+            if (i0 + 1 < nx) Y[e + 1] = c[nt][1];
+          }
+        }
+        nrm += c[nt][0] * c[nt][0] + c[nt][1] * c[nt][1];
+      }
+      if (hasB) {
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const int src = (q + 4 * ks) * 4 + (g >> 1);
+            const double v0 = __shfl_sync(0xffffffffu, c[nt][0], src);
+            const double v1 = __shfl_sync(0xffffffffu, c[nt][1], src);
+            dmma(z[kk][nt], a2[ks], (g & 1) ? v1 : v0);
+          }
+        }
+      }
+    }
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+    if (lane == 0) {
+      while (atomicAdd(&tag[slot], 0) != lt) { __nanosleep(20); }
+    }
+    __syncwarp();
+    if (q == 0) ring[(slot * NW + warp) * 8 + g] = nrm;
+    __threadfence_block();
+    __syncwarp();
+    int last = 0;
+    const int npart = nblk >= NW ? NW : nblk;
+    if (lane == 0) last = (atomicAdd(&cnt[slot], 1) == npart - 1);
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
+      if (lane < nc) {
+        double n2 = 0.0;
+        for (int w = 0; w < NW; ++w)
+          if (((w - klo) % NW + NW) % NW <= K - klo) n2 += ring[(slot * NW + w) * 8 + lane];
+        const int cj = tl[4 + lane];
+        const int64_t ij = bg + cj;
+        const double shat = (v.s[ij] == 1.0) ? 1.0 : 0.0;
+        double s;
+        const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
+        v.s[ij] = s;
+        v.pt[ij] = tp;
+        if (s != shat) {
+          const int pos = atomicAdd(&v.ncorr[b], 1);
+          v.clist[bg + pos] = cj;
+          v.cw[bg + pos] = s - shat;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        cnt[slot] = 0;
+        __threadfence_block();
+        atomicExch(&tag[slot], lt + kRing);
+      }
+    }
+  }
+  // ---- flush this warp's Z slices: Zpart[b][sidx][k][m][i]  (row m = g, col i)
+  double* Zp = v.Zpart + ((int64_t)b * v.nsplit + sidx) * T * nu * nx;
+#pragma unroll
+  for (int kk = 0; kk < KK; ++kk) {
+    const int k = warp + NW * kk;
+    if (k < T && g < nu) {
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int i = 2 * q + r + 8 * nt;
+          if (i < nx) Zp[((int64_t)k * nu + g) * nx + i] = z[kk][nt][r];
+        }
+    }
+  }
+}
+
+// Adjoint over a cone list, S7 / S7': Z_k = sum_{j in list} w_j b_{j,k} y_{j,k}^T.
+// Correction of the fused pass (list = mispredicted cones, w = s^l - shat), or
+// the dense adjoint (list = all cones, w = scale_j or 1) for the DR engine,
+// nrto_gain_update and the generic path.  One CTA per (instance, step k);
+// listed cones are staged in chunks of 64 through shared memory (b rows and
+// y rows), then each thread owns outputs (m, i).  Requires n_u <= 8.
+__global__ void __launch_bounds__(128)
+k_zlist(Dev v, const double* __restrict__ y, const int32_t* __restrict__ clist,
+        const double* __restrict__ cw, const double* __restrict__ scale,
+        const int32_t* __restrict__ ncnt, int nfixed, const int32_t* __restrict__ act,
+        double* __restrict__ Zout) {
+  __shared__ double sb[64 * 8];
+  __shared__ double sy[64 * 32];
+  __shared__ double swt[64];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu;
+  const int b = blockIdx.x / d.T, k = blockIdx.x % d.T;
+  double* Zo = Zout + ((int64_t)b * d.T + k) * nu * nx;
+  if (act && !act[b]) return;
+  const int n = ncnt ? ncnt[b] : nfixed;
+  const int64_t bg = (int64_t)b * d.ng;
+  const double* yb = y + (int64_t)b * d.E;
+  const double* Bd = v.Bd + (int64_t)b * d.EB;
+  const int tid = threadIdx.x;
+  const int o0 = tid, o1 = tid + 128;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int base = 0; base < n; base += 64) {
+    const int cnt = min(64, n - base);
+    __syncthreads();
+    for (int r = tid; r < cnt; r += blockDim.x) {
+      const int j = clist ? clist[bg + base + r] : base + r;
+      const int kind = v.kind[j], knot = v.knot[j];
+      const bool has = (kind == 0) ? (knot > k) : (knot == k);
+      const double w = cw ? cw[bg + base + r] : (scale ? scale[bg + j] : 1.0);
+      swt[r] = has ? w : 0.0;
+    }
+    for (int r = tid; r < cnt * 8; r += blockDim.x) {
+      const int c = r >> 3, mm = r & 7;
+      const int j = clist ? clist[bg + base + c] : base + c;
+      const int kind = v.kind[j], knot = v.knot[j];
+      const bool has = (kind == 0) ? (knot > k) : (knot == k);
+      const int kb = (kind == 0) ? k : 0;
+      sb[r] = (has && mm < nu) ? Bd[v.offB[j] + (int64_t)kb * d.nup + mm] : 0.0;
+    }
+    for (int r = tid; r < cnt * 32; r += blockDim.x) {
+      const int c = r >> 5, ii = r & 31;
+      const int j = clist ? clist[bg + base + c] : base + c;
+      const int kind = v.kind[j], knot = v.knot[j];
+      const bool has = (kind == 0) ? (knot > k) : (knot == k);
+      const int kb = (kind == 0) ? k : 0;
+      sy[r] = (has && ii < nx) ? yb[v.off[j] + (int64_t)kb * nx + ii] : 0.0;
+    }
+    __syncthreads();
+    if (o0 < nu * nx) {
+      const int m = o0 / nx, i = o0 % nx;
+      for (int c = 0; c < cnt; ++c) acc0 += swt[c] * sb[c * 8 + m] * sy[c * 32 + i];
+    }
+    if (o1 < nu * nx) {
+      const int m = o1 / nx, i = o1 % nx;
+      for (int c = 0; c < cnt; ++c) acc1 += swt[c] * sb[c * 8 + m] * sy[c * 32 + i];
+    }
+  }
+  if (o0 < nu * nx) Zo[o0] = acc0;
+  if (o1 < nu * nx) Zo[o1] = acc1;
+}
+
+static int fused_variant(const Dims& d, int* nti, int* nks) {
+  *nti = (d.nx + 7) / 8;
+  *nks = (d.nu + 3) / 4;
+  return (*nti <= 2 && *nks <= 2);
+}
+
+size_t fused_smem_bytes(const Dims& d) {
+  const int nti = (d.nx + 7) / 8;
+  return ((size_t)d.T * 8 * 8 * nti + kRing * 64) * sizeof(double) + 2 * kRing * sizeof(int);
+}
+
+bool fused_supported(const Dims& d) {
+  int a, c;
+  return fused_variant(d, &a, &c) && fused_smem_bytes(d) <= 200 * 1024;
+}
+
+template <int NTI, int NKS>
+static cudaError_t launch_fused_t(nrto_handle_s* h, cudaStream_t st) {
+  const size_t smem = fused_smem_bytes(h->dev.d);
+  auto kfn = k_fa_fused<NTI, NKS>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kfn<<<h->dev.nwitems, 256, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+template <int NTI, int NKS, int KK>
+static cudaError_t launch_fused_r(nrto_handle_s* h, cudaStream_t st) {
+  k_fa_fused_r<NTI, NKS, KK><<<h->dev.nwitems, 512, 0, st>>>(h->dev, h->dev.tiles, h->dev.witems);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+template <int KK>
+static cudaError_t launch_fused_rk(nrto_handle_s* h, int nti, int nks, cudaStream_t st) {
+  if (nti == 1 && nks == 1) return launch_fused_r<1, 1, KK>(h, st);
+  if (nti == 1 && nks == 2) return launch_fused_r<1, 2, KK>(h, st);
+  if (nti == 2 && nks == 1) return launch_fused_r<2, 1, KK>(h, st);
+  return launch_fused_r<2, 2, KK>(h, st);
+}
+
+cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st) {
+  int nti, nks;
+  fused_variant(h->dev.d, &nti, &nks);
+  if (h->dev.nwitems == 0) return cudaSuccess;
+  const int T = h->dev.d.T;
+  if (T <= 32) return launch_fused_rk<2>(h, nti, nks, st);
+  if (T <= 64) return launch_fused_rk<4>(h, nti, nks, st);
+  if (T <= 112) return launch_fused_rk<7>(h, nti, nks, st);
+  if (nti == 1 && nks == 1) return launch_fused_t<1, 1>(h, st);
+  if (nti == 1 && nks == 2) return launch_fused_t<1, 2>(h, st);
+  if (nti == 2 && nks == 1) return launch_fused_t<2, 1>(h, st);
+  return launch_fused_t<2, 2>(h, st);
+}
+
+cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
+                         const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,
+                         double* Zout, cudaStream_t st) {
+  Dev& v = h->dev;
+  k_zlist<<<v.d.B * v.d.T, 128, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+}  // namespace nrto

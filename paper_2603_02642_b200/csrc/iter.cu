@@ -49,7 +49,7 @@ __global__ void k_fa_pass(Dev v) {
     double acc = (g.kind == 0) ? bh[e] : 0.0;
     if (kb < g.nbB) {
       const double* Dr = Dm + ((int64_t)(g.klo + kb) * nx + i) * nu;
-      const double* br = Bd + kb * nu;
+      const double* br = Bd + kb * d.nup;
       for (int m = 0; m < nu; ++m) acc += Dr[m] * br[m];
     }
     const double y = acc + omsp * Y[e];
@@ -82,7 +82,7 @@ __global__ void k_adjoint(Dev v, const double* __restrict__ y, const double* __r
     for (int c = v.kptr[k]; c < v.kptr[k + 1]; ++c) {
       const int j = v.kcone[c];
       const int kb = (v.kind[j] == 0) ? k : 0;
-      double t = Bd[v.offB[j] + kb * nu + m] * yb[v.off[j] + kb * nx + i];
+      double t = Bd[v.offB[j] + kb * d.nup + m] * yb[v.off[j] + kb * nx + i];
       if (scale) t *= scale[(int64_t)b * d.ng + j];
       acc += t;
     }
@@ -144,11 +144,22 @@ __global__ void k_fa_gain(Dev v, int mode, const double* kin, double* kout) {
   const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + k) * nx * nx;
   const double* Wk = v.W + bk * nu * nu;
   const double* Kp = (mode == 0 ? v.K : kin) + (int64_t)b * d.NK + (int64_t)k * nu * nx;
+  const bool fz = (mode == 0) && v.fused;
   for (int r = tid; r < nu * nx; r += nt) {   // G = Z - Zb into sX ; K_prev into sK
-    sX[r] = v.Z[bk * nu * nx + r] - v.Zb[bk * nu * nx + r];
+    double z;
+    if (fz) {                                  // fused pass partials + correction (+ control)
+      z = v.Zc[bk * nu * nx + r];
+      if (v.fused == 2) z += v.Zctrl[bk * nu * nx + r];
+      const double* zp = v.Zpart + ((int64_t)b * v.nsplit * d.T + k) * nu * nx + r;
+      for (int sp = 0; sp < v.nsplit; ++sp) z += zp[(int64_t)sp * d.T * nu * nx];
+    } else {
+      z = v.Z[bk * nu * nx + r];
+    }
+    sX[r] = z - v.Zb[bk * nu * nx + r];
     const int m = r / nx, i = r % nx;
     sK[r] = Kp[i * nu + m];
   }
+  if (fz && k == 0 && tid == 0) v.ncorr[b] = 0;   // correction list consumed
   __syncthreads();
   const double rho = v.prm.rho;
   for (int r = tid; r < nu * nx; r += nt) {
@@ -251,7 +262,7 @@ __global__ void k_dr_pass(Dev v) {
     double a = (g.kind == 0) ? bh[e] : 0.0;
     if (kb < g.nbB) {
       const double* Cr = Cm + ((int64_t)(g.klo + kb) * nx + i) * nu;
-      const double* br = Bd + kb * nu;
+      const double* br = Bd + kb * d.nup;
       for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
     }
     const double er = 2.0 * a - Y[e];
@@ -266,7 +277,7 @@ __global__ void k_dr_pass(Dev v) {
     double a = (g.kind == 0) ? bh[e] : 0.0;
     if (kb < g.nbB) {
       const double* Cr = Cm + ((int64_t)(g.klo + kb) * nx + i) * nu;
-      const double* br = Bd + kb * nu;
+      const double* br = Bd + kb * d.nup;
       for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
     }
     const double et = Y[e];
@@ -328,7 +339,7 @@ __global__ void k_finish_cones(Dev v, int engine, double* nu_out, double* lam_ou
     double a = (g.kind == 0) ? bh[e] : 0.0, dlt = 0.0;
     if (kb < g.nbB) {
       const int64_t r = ((int64_t)(g.klo + kb) * nx + i) * nu;
-      const double* br = Bd + kb * nu;
+      const double* br = Bd + kb * d.nup;
       for (int m = 0; m < nu; ++m) { a += Cc[r + m] * br[m]; dlt += (Cc[r + m] - Cp[r + m]) * br[m]; }
     }
     n2 += a * a;
@@ -431,6 +442,8 @@ static inline unsigned warp_grid(int64_t warps, int wpb) {
 cudaError_t launch_adjoint(nrto_handle_s* h, const double* y, const double* scale,
                            const int32_t* act, cudaStream_t st) {
   Dev& v = h->dev;
+  if (v.d.nu <= 8 && v.d.nx <= 32)
+    return launch_zlist(h, y, nullptr, nullptr, scale, nullptr, v.d.ng, act, v.Z, st);
   k_adjoint<<<v.d.B * v.d.T, 128, 0, st>>>(v, y, scale, act);
   h->launches++;
   return cudaGetLastError();
@@ -496,8 +509,8 @@ cudaError_t launch_gain_update(nrto_handle_s* h, const double* nu, const double*
                                double* kv_next, cudaStream_t st) {
   Dev& v = h->dev;
   const Dims& d = v.d;
-  k_adjoint<<<d.B * d.T, 128, 0, st>>>(v, nu, nullptr, nullptr);
-  h->launches++;
+  cudaError_t e = launch_adjoint(h, nu, nullptr, nullptr, st);
+  if (e != cudaSuccess) return e;
   k_fa_gain<<<d.B * d.T, 128, 3 * d.nu * d.nx * sizeof(double), st>>>(v, 1, kv_prev, kv_next);
   h->launches++;
   return cudaGetLastError();

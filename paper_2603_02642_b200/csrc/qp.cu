@@ -190,8 +190,251 @@ __global__ void __launch_bounds__(128) k_qp(Dev v, int engine, int l) {
   }
 }
 
+// Staged variant: the per-step closed-loop matrices Acl_k of the instance are
+// copied to shared memory once per call, the k-independent parts of the
+// Riccati solve are computed in parallel phases, and only the two linear
+// recurrences  s_k = a_k + Acl_k^T s_{k+1}  (backward) and
+// dx_{k+1} = Acl_k dx_k + e_k  (forward) run sequentially, on one warp with
+// the vector held in registers and exchanged by shuffles:
+//   a_k  = r_x,k - Kf_k^T r_u,k          kff_k = H^-1 r_u,k + H^-1 B_k^T s_{k+1}
+//   e_k  = B_k kff_k                      du~_k = kff_k - Kf_k dx_k
+__global__ void __launch_bounds__(1024) k_qp_staged(Dev v, int engine, int l, int stageA) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, T = d.T, ng = d.ng;
+  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  if (!v.active[b]) return;
+  const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
+  const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
+  const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp, aq = v.prm.alpha_qp;
+  const double den = rho + sq + rq, beta = rq / den;
+  const int64_t bg = (int64_t)b * ng;
+  const double* grad = v.grad + bg * nx;
+  const double* g0 = v.g0 + bg;
+  double* p = v.p + bg; double* zl = v.zl + bg; double* yl = v.yl + bg;
+  double* rp = v.rp + bg; double* wq = v.wq + bg;
+  const double* pt = v.pt + bg; double* lam = v.lamp + bg;
+  double* zb = v.zb + (int64_t)b * (T + 1) * nx; double* yb = v.yb + (int64_t)b * (T + 1) * nx;
+  double* du = v.du + (int64_t)b * T * nu;
+  const double* Ru = v.Ru + (int64_t)b * T * nu * nu;
+  const double* uh = v.uhat + (int64_t)b * T * nu;
+  const double* Bm = v.Bm + (int64_t)b * T * nx * nu;
+  const double* Kf = F.Kf + (int64_t)b * T * nu * nx;
+  const double* AclG = F.Acl + (int64_t)b * T * nx * nx;
+  const double* Hi = F.Hinv + (int64_t)b * T * nu * nu;
+  const double* HB = F.HB + (int64_t)b * T * nu * nx;
+  const double rtr = v.rtrust[b];
+  const double rinv = (engine == NRTO_FULLADMM) ? 1.0 : 1.0 / rho;
+  // shared memory
+  double* sS = sm;                          // [(T+1) nx]  s_k, then dx_k, then z^_ball
+  double* sA = sS + (T + 1) * nx;           // [T nx]      a_k, then e_k
+  double* sK = sA + T * nx;                 // [T nu]      kff_k
+  double* sR = sK + T * nu;                 // [T nu]      r_u,k, then du~_k
+  double* sAcl = sR + T * nu;               // [T nx nx]   (stageA)
+  const double* Acl = stageA ? sAcl : AclG;
+  if (stageA)
+    for (int r = tid; r < T * nx * nx; r += nt) sAcl[r] = AclG[r];
+
+  for (int it = 0; it < v.prm.qp_iters; ++it) {
+    for (int j = tid; j < ng; j += nt) {
+      const double vj = pt[j] - lam[j] * rinv;   // FullADMM: p~ - lam_p ; DR: p~ - lambda/rho
+      const double r = sq * p[j] + rho * vj + rq * zl[j] - yl[j];
+      rp[j] = r;
+      wq[j] = rq * zl[j] - yl[j] - beta * r;
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nu; r += nt) {      // r_u
+      const int k = r / nu, m = r % nu;
+      double acc = sq * du[r];
+#pragma unroll 4
+      for (int q = 0; q < nu; ++q) acc -= 2.0 * __ldg(Ru + (k * nu + m) * nu + q) * __ldg(uh + k * nu + q);
+#pragma unroll 4
+      for (int q = __ldg(v.cptr + k); q < __ldg(v.cptr + k + 1); ++q) {
+        const int j = __ldg(v.crow + q);
+        acc += __ldg(grad + j * nx + m) * wq[j];
+      }
+      sR[r] = acc;
+    }
+    __syncthreads();
+    for (int r = tid; r < (T + 1) * nx; r += nt) { // r_x and a_k
+      const int k = r / nx, i = r % nx;
+      double acc = 0.0;
+      if (k > 0) {
+        acc = rq * zb[r] - yb[r];
+#pragma unroll 8
+        for (int q = __ldg(v.sptr + k); q < __ldg(v.sptr + k + 1); ++q) {
+          const int j = __ldg(v.srow + q);
+          acc += __ldg(grad + j * nx + i) * wq[j];
+        }
+      }
+      if (k < T) {
+        const double* Kk = Kf + (int64_t)k * nu * nx;
+#pragma unroll 4
+        for (int m = 0; m < nu; ++m) acc -= __ldg(Kk + m * nx + i) * sR[k * nu + m];
+        sA[r] = acc;
+      } else {
+        sS[r] = acc;
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {                               // backward recurrence (one warp)
+      double s = (tid < nx) ? sS[T * nx + tid] : 0.0;
+      const int ic = tid < nx ? tid : 0;
+      for (int k = T - 1; k >= 0; --k) {
+        const double* Ak = Acl + (size_t)k * nx * nx + ic;
+        double a0 = sA[k * nx + ic], a1 = 0.0, a2 = 0.0, a3 = 0.0;   // 4 chains (ILP)
+        int r = 0;
+        for (; r + 4 <= nx; r += 4) {
+          a0 += Ak[(r + 0) * nx] * __shfl_sync(0xffffffffu, s, r + 0);
+          a1 += Ak[(r + 1) * nx] * __shfl_sync(0xffffffffu, s, r + 1);
+          a2 += Ak[(r + 2) * nx] * __shfl_sync(0xffffffffu, s, r + 2);
+          a3 += Ak[(r + 3) * nx] * __shfl_sync(0xffffffffu, s, r + 3);
+        }
+        for (; r < nx; ++r) a0 += Ak[r * nx] * __shfl_sync(0xffffffffu, s, r);
+        s = (a0 + a1) + (a2 + a3);
+        if (tid < nx) sS[k * nx + tid] = s;
+      }
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nu; r += nt) {      // kff_k
+      const int k = r / nu, m = r % nu;
+      const double* H = Hi + (int64_t)k * nu * nu;
+      const double* hb = HB + (int64_t)k * nu * nx;
+      double acc = 0.0;
+#pragma unroll 4
+      for (int q = 0; q < nu; ++q) acc += __ldg(H + m * nu + q) * sR[k * nu + q];
+#pragma unroll 4
+      for (int i = 0; i < nx; ++i) acc += __ldg(hb + m * nx + i) * sS[(k + 1) * nx + i];
+      sK[r] = acc;
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nx; r += nt) {      // e_k = B_k kff_k
+      const int k = r / nx, i = r % nx;
+      const double* Bk = Bm + (int64_t)k * nx * nu;
+      double acc = 0.0;
+#pragma unroll 4
+      for (int m = 0; m < nu; ++m) acc += __ldg(Bk + i * nu + m) * sK[k * nu + m];
+      sA[r] = acc;
+    }
+    __syncthreads();
+    if (tid < 32) {                               // forward recurrence (one warp)
+      double x = 0.0;
+      const int ic = tid < nx ? tid : 0;
+      if (tid < nx) sS[tid] = 0.0;
+      for (int k = 0; k < T; ++k) {
+        const double* Ak = Acl + (size_t)k * nx * nx + ic * nx;
+        double a0 = sA[k * nx + ic], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int r = 0;
+        for (; r + 4 <= nx; r += 4) {
+          a0 += Ak[r + 0] * __shfl_sync(0xffffffffu, x, r + 0);
+          a1 += Ak[r + 1] * __shfl_sync(0xffffffffu, x, r + 1);
+          a2 += Ak[r + 2] * __shfl_sync(0xffffffffu, x, r + 2);
+          a3 += Ak[r + 3] * __shfl_sync(0xffffffffu, x, r + 3);
+        }
+        for (; r < nx; ++r) a0 += Ak[r] * __shfl_sync(0xffffffffu, x, r);
+        x = (a0 + a1) + (a2 + a3);
+        if (tid < nx) sS[(k + 1) * nx + tid] = x;
+      }
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nu; r += nt) {      // du~_k
+      const int k = r / nu, m = r % nu;
+      const double* Kk = Kf + (int64_t)k * nu * nx;
+      double acc = sK[r];
+#pragma unroll 4
+      for (int q = 0; q < nx; ++q) acc -= __ldg(Kk + m * nx + q) * sS[k * nx + q];
+      sR[r] = acc;
+    }
+    __syncthreads();
+    for (int j = tid; j < ng; j += nt) {          // linear rows
+      const int k = v.knot[j];
+      double bd = 0.0;
+      if (v.kind[j] == 0) {
+#pragma unroll 4
+        for (int q = 0; q < nx; ++q) bd += __ldg(grad + j * nx + q) * sS[k * nx + q];
+      } else {
+#pragma unroll 4
+        for (int q = 0; q < nu; ++q) bd += __ldg(grad + j * nx + q) * sR[k * nu + q];
+      }
+      const double ptl = (rp[j] - rq * bd) / den;
+      const double ztl = bd + ptl;
+      p[j] = aq * ptl + (1.0 - aq) * p[j];
+      const double zh = aq * ztl + (1.0 - aq) * zl[j];
+      const double zn = fmin(zh + yl[j] / rq, -g0[j]);
+      yl[j] += rq * (zh - zn);
+      zl[j] = zn;
+    }
+    for (int r = tid; r < T * nu; r += nt) du[r] = aq * sR[r] + (1.0 - aq) * du[r];
+    __syncthreads();
+    double nb = 0.0;                              // trust-region ball on F_u du
+    for (int r = tid; r < (T + 1) * nx; r += nt) {
+      const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
+      sS[r] = zh;
+      const double w = zh + yb[r] / rq;
+      nb += w * w;
+    }
+    nb = sqrt(block_sum(nb, red));
+    const double scl = (nb > rtr) ? rtr / nb : 1.0;
+    for (int r = tid; r < (T + 1) * nx; r += nt) {
+      const double zh = sS[r];
+      const double zn = scl * (zh + yb[r] / rq);
+      yb[r] += rq * (zh - zn);
+      zb[r] = zn;
+    }
+    __syncthreads();
+  }
+  // ---- dual update + residuals of the outer iteration
+  double ap = 0.0, ad = 0.0;
+  double* tin = v.tin + bg;
+  double* ptp = v.ptprev + bg;
+  for (int j = tid; j < ng; j += nt) {
+    const double dp = p[j] - pt[j];
+    if (engine == NRTO_FULLADMM) {       // (16): lam_p += p - p~ ; next t = p + lam_p
+      lam[j] += dp;
+      tin[j] = p[j] + lam[j];
+    } else {                              // (5c): lambda += rho (p - p~)   (R4)
+      lam[j] += rho * dp;
+    }
+    ap += dp * dp;
+    const double dd = pt[j] - ptp[j];
+    ad += dd * dd;
+    ptp[j] = pt[j];
+  }
+  ap = block_sum(ap, red);
+  ad = block_sum(ad, red);
+  if (tid == 0) {
+    const double rpv = sqrt(ap), rdv = rho * sqrt(ad);
+    v.r_p[b] = rpv;
+    v.r_d[b] = rdv;
+    v.iters[b] = l;
+    if (!isfinite(rpv) || !isfinite(rdv)) {
+      v.status[b] = NRTO_DIVERGED;
+      v.active[b] = 0;
+    } else if (!v.prm.fixed_iters && (l % v.prm.check_every) == 0 && rpv <= v.prm.eps_p &&
+               rdv <= v.prm.eps_d) {
+      v.status[b] = NRTO_CONVERGED;
+      v.active[b] = 0;
+    }
+  }
+}
+
+static size_t qp_smem(const Dims& d, int stageA) {
+  return ((size_t)(d.T + 1) * d.nx + (size_t)d.T * d.nx + 2 * (size_t)d.T * d.nu +
+          (stageA ? (size_t)d.T * d.nx * d.nx : 0)) * sizeof(double);
+}
+
 cudaError_t launch_qp(nrto_handle_s* h, int engine, int l, cudaStream_t st) {
-  k_qp<<<h->dev.d.B, 128, 0, st>>>(h->dev, engine, l);
+  const Dims& d = h->dev.d;
+  const size_t lim = 200 * 1024;
+  int stageA = qp_smem(d, 1) <= lim;
+  if (stageA || qp_smem(d, 0) <= lim) {
+    const size_t smem = qp_smem(d, stageA);
+    cudaFuncSetAttribute(k_qp_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_qp_staged<<<d.B, 1024, smem, st>>>(h->dev, engine, l, stageA);
+  } else {
+    k_qp<<<d.B, 128, 0, st>>>(h->dev, engine, l);
+  }
   h->launches++;
   return cudaGetLastError();
 }
@@ -229,6 +472,7 @@ cudaError_t launch_fa_reset(nrto_handle_s* h, cudaStream_t st) {
   zero(h, v.D, B * d.T * d.nx * d.nu, st);
   zero(h, v.du, B * d.T * d.nu, st); zero(h, v.zl, B * d.ng, st); zero(h, v.yl, B * d.ng, st);
   zero(h, v.zb, B * (d.T + 1) * d.nx, st); zero(h, v.yb, B * (d.T + 1) * d.nx, st);
+  cudaMemsetAsync(v.ncorr, 0, B * sizeof(int32_t), st);
   k_reset_inst<<<(d.B + 127) / 128, 128, 0, st>>>(v, NRTO_FULLADMM);
   h->launches++;
   h->dr_fresh = 1;   // Y / Z now hold FullADMM state

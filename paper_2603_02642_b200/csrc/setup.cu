@@ -23,7 +23,7 @@ __global__ void k_costate(Dev v) {
   double* bh = v.bhat + (int64_t)b * d.E + v.off[j];
   double* Bd = v.Bd + (int64_t)b * d.EB + v.offB[j];
   if (v.kind[j] != 0) {
-    if (lane < nu) Bd[lane] = grad[lane];
+    if (lane < d.nup) Bd[lane] = (lane < nu) ? grad[lane] : 0.0;
     if (lane < nx) bh[lane] = 0.0;
     return;
   }
@@ -43,7 +43,7 @@ __global__ void k_costate(Dev v) {
         if (lane < nu) bm += Bk[r * nu + lane] * cr;   // (B_k^T c)_m
         if (lane < nx) cn += Ak[r * nx + lane] * cr;   // (A_k^T c)_i
       }
-      if (lane < nu) Bd[k * nu + lane] = bm;
+      if (lane < d.nup) Bd[k * d.nup + lane] = (lane < nu) ? bm : 0.0;
       c = cn;
     }
     const double* Pk = Psi + (int64_t)k * nx * nx;
@@ -74,8 +74,8 @@ __global__ void k_lam_zb(Dev v) {
       const int j = v.kcone[c];
       const bool st = v.kind[j] == 0;
       const int kb = st ? k : 0;
-      const double bm = Bd[v.offB[j] + kb * nu + m];
-      if (isLam) acc += bm * Bd[v.offB[j] + kb * nu + q];
+      const double bm = Bd[v.offB[j] + kb * d.nup + m];
+      if (isLam) acc += bm * Bd[v.offB[j] + kb * d.nup + q];
       else if (st) acc += bm * bhat[v.off[j] + kb * nx + q];
     }
     if (isLam) v.Lam[((int64_t)b * d.T + k) * nu * nu + o] = acc;

@@ -1,0 +1,396 @@
+// TMA-pipelined fused FullADMM pass for STATE cones (n_x even) and the exact
+// single-block pass for CONTROL cones.  Same arithmetic as k_fa_fused_r
+// (fused.cu); the difference is how bytes reach the SM:
+//
+//  * a producer warp streams each chunk (one tile of <= 8 same-knot cones x 16
+//    consecutive time blocks) of y_old, b_hat and b from HBM into a 3-stage
+//    shared-memory ring with cp.async.bulk (TMA, SASS UBLKCP) completing on an
+//    mbarrier with a transaction count;
+//  * 16 consumer warps (warp w <-> block k = kc + w, so the adjoint slice Z_k
+//    stays in warp w's registers) run the DMMA forward map / predicted adjoint
+//    from shared memory and store y_new straight to HBM;
+//  * D_k for the whole horizon is copied to shared memory once per work item.
+//
+// Control cones have a single time block, so their norm, projection and exact
+// adjoint contribution s b y^T are completed inside one warp (k_fa_ctrl).
+#include "common.cuh"
+
+namespace nrto {
+
+__device__ __forceinline__ void dmma2(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(saddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+
+constexpr int kStages = 3;
+constexpr int kRingT = 4;
+constexpr int kTI = 12;   // ints per tile
+
+struct TmaGeom {          // shared-memory geometry of one stage (doubles)
+  int SY;                 // per-cone stride of y / b_hat rows (16 n_x + pad)
+  int SB;                 // per-cone stride of b rows (16 nup + pad)
+  int stage;              // doubles per stage: 8 SY (y) + 8 SY (b_hat) + 8 SB (b)
+};
+__host__ __device__ inline TmaGeom tma_geom(int nx, int nup) {
+  TmaGeom g;
+  g.SY = 16 * nx + 8;     // == 8 (mod 16) doubles: conflict-free LDS.128 across the 8 cones
+  g.SB = 16 * nup + 4;    // == 4 (mod 16) doubles
+  g.stage = 16 * g.SY + 8 * g.SB;
+  return g;
+}
+
+template <int NTI, int NKS, int KK>
+__global__ void __launch_bounds__(544, 1)
+k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems) {
+  extern __shared__ __align__(128) double sm[];
+  constexpr int NW = 16;
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, nup = d.nup, T = d.T;
+  const TmaGeom G = tma_geom(nx, nup);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + kStages;
+  int* cnt = reinterpret_cast<int*>(empty + kStages);
+  int* tag = cnt + kRingT;
+  double* ring = sm + 16;                                  // [kRingT][NW][8]
+  double* Ds = ring + kRingT * NW * 8;                     // [T][nx][nu]
+  double* stg = Ds + ((T * nx * nu + 1) & ~1);             // stages
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int b = witems[4 * blockIdx.x], t0 = witems[4 * blockIdx.x + 1];
+  const int t1 = witems[4 * blockIdx.x + 2], sidx = witems[4 * blockIdx.x + 3];
+  if (!v.active[b]) return;
+  const double* __restrict__ bhat = v.bhat + (int64_t)b * d.E;
+  const double* __restrict__ Bd = v.Bd + (int64_t)b * d.EB;
+  double* __restrict__ Y = v.Y + (int64_t)b * d.E;
+  const int64_t bg = (int64_t)b * d.ng;
+  {
+    const double* Dg = v.D + (int64_t)b * T * nx * nu;
+    for (int r = threadIdx.x; r < T * nx * nu; r += blockDim.x) Ds[r] = Dg[r];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < kRingT) { cnt[threadIdx.x] = 0; tag[threadIdx.x] = threadIdx.x; }
+  __syncthreads();
+
+  if (warp == NW) {
+    // ---------------------------------------------------------------- producer
+    // lane c < nc owns cone c of the tile: its offsets are loaded once per tile
+    // and it issues that cone's bulk copies; lane 0 arms the stage barrier.
+    int n = 0;
+    int tnext = t0;
+    int64_t offn = 0, offBn = 0;
+    if (tnext < t1 && lane < tiles[(int64_t)tnext * kTI + 2]) {
+      const int j = tiles[(int64_t)tnext * kTI + 4 + lane];
+      offn = v.off[j]; offBn = v.offB[j];
+    }
+    for (int t = t0; t < t1; ++t) {
+      const int* tl = tiles + (int64_t)t * kTI;
+      const int K = tl[1], nc = tl[2];
+      const int64_t offc = offn, offBc = offBn;
+      if (t + 1 < t1 && lane < tiles[(int64_t)(t + 1) * kTI + 2]) {   // prefetch next tile
+        const int j = tiles[(int64_t)(t + 1) * kTI + 4 + lane];
+        offn = v.off[j]; offBn = v.offB[j];
+      }
+      for (int kc = 0; kc <= K; kc += 16, ++n) {
+        const int st = n % kStages;
+        const int nb = min(16, K + 1 - kc), nbB = max(0, min(16, K - kc));
+        if (lane == 0) {
+          mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
+          const uint32_t bytes = (uint32_t)nc * (2u * nb * nx + (uint32_t)nbB * nup) * 8u;
+          mbar_expect_tx(&full[st], bytes);
+        }
+        __syncwarp();
+        if (lane < nc) {
+          double* sY = stg + (size_t)st * G.stage;
+          double* sH = sY + 8 * G.SY;
+          double* sB = sH + 8 * G.SY;
+          const int64_t o = offc + (int64_t)kc * nx;
+          bulk_g2s(sY + lane * G.SY, Y + o, nb * nx * 8, &full[st]);
+          bulk_g2s(sH + lane * G.SY, bhat + o, nb * nx * 8, &full[st]);
+          if (nbB > 0)
+            bulk_g2s(sB + lane * G.SB, Bd + offBc + (int64_t)kc * nup, nbB * nup * 8, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ consumers
+  double z[KK][NTI][2];
+#pragma unroll
+  for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+    for (int nt = 0; nt < NTI; ++nt) { z[kk][nt][0] = 0.0; z[kk][nt][1] = 0.0; }
+  int n = 0;
+  for (int t = t0; t < t1; ++t) {
+    const int* tl = tiles + (int64_t)t * kTI;
+    const int K = tl[1], nc = tl[2];
+    const int lt = t - t0, slot = lt % kRingT;
+    const bool gv = g < nc;
+    const int cg = gv ? tl[4 + g] : 0;
+    const int64_t offg = gv ? v.off[cg] : 0;
+    const double omsp = gv ? 1.0 - v.s[bg + cg] : 0.0;
+    double sh2[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int c2 = q + 4 * ks;
+      sh2[ks] = (c2 < nc && v.s[bg + tl[4 + c2]] == 1.0) ? 1.0 : 0.0;   // shat = [s^{l-1} == 1]
+    }
+    double nrm = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk) {
+      const int kc = NW * kk;
+      if (kc > K) break;
+      const int st = n % kStages;
+      mbar_wait(&full[st], (n / kStages) & 1);
+      ++n;
+      const double* sY = stg + (size_t)st * G.stage;
+      const double* sH = sY + 8 * G.SY;
+      const double* sB = sH + 8 * G.SY;
+      const int k = kc + warp;
+      if (k <= K) {
+        const bool hasB = k < K;
+        double c[NTI][2];
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) {
+          const int i0 = 2 * q + 8 * nt;
+          c[nt][0] = 0.0; c[nt][1] = 0.0;
+          if (gv && i0 < nx) {
+            const int e = g * G.SY + warp * nx + i0;
+            const double2 yo = *reinterpret_cast<const double2*>(sY + e);
+            const double2 bh = *reinterpret_cast<const double2*>(sH + e);
+            c[nt][0] = bh.x + omsp * yo.x;
+            c[nt][1] = bh.y + omsp * yo.y;
+          }
+        }
+        double a2[2];
+        if (hasB) {
+#pragma unroll
+          for (int ks = 0; ks < NKS; ++ks) {
+            const int m = q + 4 * ks;
+            const double a = (gv && m < nu) ? sB[g * G.SB + warp * nup + m] : 0.0;
+#pragma unroll
+            for (int nt = 0; nt < NTI; ++nt) {
+              const int i = g + 8 * nt;
+              const double bb = (m < nu && i < nx) ? Ds[((size_t)k * nx + i) * nu + m] : 0.0;
+              dmma2(c[nt], a, bb);
+            }
+          }
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks)
+            a2[ks] = (g < nu && sh2[ks] != 0.0) ? sB[(q + 4 * ks) * G.SB + warp * nup + g] : 0.0;
+        }
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) {
+          const int i0 = 2 * q + 8 * nt;
+          if (gv && i0 < nx)
+            __stcs(reinterpret_cast<double2*>(Y + offg + (int64_t)k * nx + i0),
+                   make_double2(c[nt][0], c[nt][1]));
+          nrm += c[nt][0] * c[nt][0] + c[nt][1] * c[nt][1];
+        }
+        if (hasB) {
+#pragma unroll
+          for (int nt = 0; nt < NTI; ++nt) {
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const int src = (q + 4 * ks) * 4 + (g >> 1);
+              const double v0 = __shfl_sync(0xffffffffu, c[nt][0], src);
+              const double v1 = __shfl_sync(0xffffffffu, c[nt][1], src);
+              dmma2(z[kk][nt], a2[ks], (g & 1) ? v1 : v0);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    // ---- norm partials -> ring slot; last consumer warp projects the tile's cones
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+    if (lane == 0) {
+      while (atomicAdd(&tag[slot], 0) != lt) { __nanosleep(32); }
+    }
+    __syncwarp();
+    if (q == 0) ring[(slot * NW + warp) * 8 + g] = nrm;
+    __threadfence_block();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = (atomicAdd(&cnt[slot], 1) == NW - 1);
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
+      if (lane < nc) {
+        double n2 = 0.0;
+        for (int w = 0; w < NW; ++w) n2 += ring[(slot * NW + w) * 8 + lane];
+        const int cj = tl[4 + lane];
+        const int64_t ij = bg + cj;
+        const double shat = (v.s[ij] == 1.0) ? 1.0 : 0.0;
+        double s;
+        const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
+        v.s[ij] = s;
+        v.pt[ij] = tp;
+        if (s != shat) {
+          const int pos = atomicAdd(&v.ncorr[b], 1);
+          v.clist[bg + pos] = cj;
+          v.cw[bg + pos] = s - shat;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        cnt[slot] = 0;
+        __threadfence_block();
+        atomicExch(&tag[slot], lt + kRingT);
+      }
+    }
+  }
+  // ---- flush this warp's Z slices: Zpart[b][sidx][k][m][i]
+  double* Zp = v.Zpart + ((int64_t)b * v.nsplit + sidx) * T * nu * nx;
+#pragma unroll
+  for (int kk = 0; kk < KK; ++kk) {
+    const int k = warp + NW * kk;
+    if (k < T && g < nu) {
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int i = 2 * q + r + 8 * nt;
+          if (i < nx) Zp[((int64_t)k * nu + g) * nx + i] = z[kk][nt][r];
+        }
+    }
+  }
+}
+
+// Control cones (single block at step k): y = D_k h' + (1 - s) y_old, exact
+// projection, and the exact adjoint Zctrl_k = sum_{ctrl j@k} s_j h'_j y_j^T.
+// One warp per step; lane i < n_x holds y_i; Z_k[:, i] accumulates in lane i.
+__global__ void __launch_bounds__(512)
+k_fa_ctrl(Dev v) {
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, nup = d.nup;
+  const int b = blockIdx.x;
+  if (!v.active[b]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.y * (blockDim.x >> 5) + warp;
+  if (k >= d.T) return;
+  const int64_t bg = (int64_t)b * d.ng;
+  const double* Dk = v.D + ((int64_t)b * d.T + k) * nx * nu;
+  double* Y = v.Y + (int64_t)b * d.E;
+  const double* Bd = v.Bd + (int64_t)b * d.EB;
+  double zc[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) zc[m] = 0.0;
+  double drow[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) drow[m] = (lane < nx && m < nu) ? Dk[lane * nu + m] : 0.0;
+  for (int q = v.cptr[k]; q < v.cptr[k + 1]; ++q) {
+    const int j = v.crow[q];
+    const int64_t ij = bg + j;
+    const double* bj = Bd + v.offB[j];
+    double bm[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) bm[m] = (m < nu) ? bj[m] : 0.0;
+    double y = 0.0;
+    if (lane < nx) {
+      y = (1.0 - v.s[ij]) * Y[v.off[j] + lane];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) y += drow[m] * bm[m];
+      Y[v.off[j] + lane] = y;
+    }
+    const double n2 = warp_sum(y * y);
+    double s;
+    const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
+    __syncwarp();
+    if (lane == 0) { v.s[ij] = s; v.pt[ij] = tp; }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) zc[m] += s * bm[m] * y;
+  }
+  if (lane < nx) {
+    double* Zo = v.Zctrl + ((int64_t)b * d.T + k) * nu * nx;
+    for (int m = 0; m < nu; ++m) Zo[m * nx + lane] = zc[m];
+  }
+  (void)nup;
+}
+
+size_t tma_smem_bytes(const Dims& d) {
+  const TmaGeom G = tma_geom(d.nx, d.nup);
+  const size_t dbl = 16 + kRingT * 16 * 8 + ((size_t)(d.T * d.nx * d.nu + 1) & ~(size_t)1) +
+                     (size_t)kStages * G.stage;
+  return dbl * sizeof(double);
+}
+
+bool tma_supported(const Dims& d) {
+  return (d.nx % 2 == 0) && d.nx <= 16 && d.nu <= 8 && d.T <= 111 &&
+         tma_smem_bytes(d) <= 220 * 1024;
+}
+
+template <int NTI, int NKS, int KK>
+static cudaError_t launch_tma_t(nrto_handle_s* h, cudaStream_t st) {
+  const size_t smem = tma_smem_bytes(h->dev.d);
+  auto kfn = k_fa_tma<NTI, NKS, KK>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kfn<<<h->dev.nwitems, 544, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+template <int KK>
+static cudaError_t launch_tma_k(nrto_handle_s* h, int nti, int nks, cudaStream_t st) {
+  if (nti == 1 && nks == 1) return launch_tma_t<1, 1, KK>(h, st);
+  if (nti == 1 && nks == 2) return launch_tma_t<1, 2, KK>(h, st);
+  if (nti == 2 && nks == 1) return launch_tma_t<2, 1, KK>(h, st);
+  return launch_tma_t<2, 2, KK>(h, st);
+}
+
+cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st) {
+  const Dims& d = h->dev.d;
+  const int nti = (d.nx + 7) / 8, nks = (d.nu + 3) / 4;
+  cudaError_t e = cudaSuccess;
+  if (h->dev.nwitems > 0) {
+    if (d.T < 32) e = launch_tma_k<2>(h, nti, nks, st);
+    else if (d.T < 64) e = launch_tma_k<4>(h, nti, nks, st);
+    else e = launch_tma_k<7>(h, nti, nks, st);
+    if (e != cudaSuccess) return e;
+  }
+  if (h->dev.nctrl > 0) {
+    dim3 grid(d.B, (d.T + 15) / 16);
+    k_fa_ctrl<<<grid, 512, 0, st>>>(h->dev);
+    h->launches++;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace nrto

@@ -223,8 +223,8 @@ def test_host_memory_path_matches_device():
     b = single(shape, data)
     gd = gpu_solve(shape, b, nrto.NRTO_FULLADMM, max_iter=7, fixed_iters=1)
     gh = gpu_solve(shape, b, nrto.NRTO_FULLADMM, memory=nrto.NRTO_MEM_HOST, max_iter=7, fixed_iters=1)
-    for k in gd:
-        np.testing.assert_array_equal(gd[k], gh[k])
+    for k in gd:   # same kernels; only the (atomic) order of the adjoint correction differs
+        assert close(gh[k], gd[k], tol=1e-12), k
 
 
 def test_setup_rejects_non_spd_weights():
