@@ -44,6 +44,8 @@ struct Dev {
   double* Zb;     // [B][T][nu][nx]  sum_j b_{j,k} b_hat_{j,k}^T
   double* Lam;    // [B][T][nu][nu]  sum_j b_{j,k} b_{j,k}^T
   double* U;      // [B][T][nx][nx]  eigenvectors of Sigma_k = Psi_k^T Psi_k
+  double* Ulam;   // [B][T][nx]      their eigenvalues (valid at representative steps)
+  int32_t* Urep;  // [B][T]          representative step of each Psi_k run
   EngineFactors fa, dr;
   // iterate state
   double* Y;      // [B][E] FullADMM: projection input y^l; DR: eta~
@@ -71,6 +73,7 @@ struct Dev {
   int fused;               // 0: generic k_fa_pass + adjoint; 1: k_fa_fused_r (all tiles) +
                            // correction; 2: k_fa_tma (state tiles) + k_fa_ctrl + correction
   int nctrl;               // number of control cones
+  int iter;                // outer iteration l of the launch (set by the host loop)
   double* Zctrl;           // [B][T][nu][nx] exact adjoint of the control cones (fused == 2)
   int ntiles, nsplit, nwitems;
   const int32_t* tiles;    // [ntiles][12] kind, knot, nc, klo, cone[8]
@@ -128,6 +131,15 @@ __device__ __forceinline__ double soc_case(double t, double a, double* s) {
   const double h = 0.5 * (t + a);
   *s = h / a;
   return h;
+}
+
+// Predicted projection scale shat of the fused pass (fused.cu, tma.cu).
+// l = 1 (cold start, t = p^0 + lam_p^0 = 0): a state cone with a > 0 is in
+// case 3 with s = (0 + a)/(2a) = 1/2 exactly, so shat = 1/2.  l > 1: shat =
+// [s^{l-1} == 1] (case 1 persists).  Mispredictions are corrected exactly.
+__device__ __forceinline__ double shat_of(const Dev& v, double sprev) {
+  if (v.iter == 1) return 0.5;
+  return (sprev == 1.0) ? 1.0 : 0.0;
 }
 
 // Launchers (defined in the .cu files; return cudaGetLastError()).

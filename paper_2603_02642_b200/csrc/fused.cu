@@ -84,7 +84,7 @@ k_fa_fused(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__
       const bool c2v = c2 < nc;
       const int cc = c2v ? tl[4 + c2] : 0;
       offB2[ks] = c2v ? v.offB[cc] : 0;
-      sh2[ks] = (c2v && v.s[bg + cc] == 1.0) ? 1.0 : 0.0;   // shat = [s^{l-1} == 1]
+      sh2[ks] = c2v ? shat_of(v, v.s[bg + cc]) : 0.0;
     }
     double nrm = 0.0;
     for (int k = first; k <= K; k += 8) {
@@ -152,7 +152,7 @@ k_fa_fused(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__
         double a2[2];
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks)
-          a2[ks] = (g < nu && sh2[ks] != 0.0) ? __ldg(Bd + offB2[ks] + (int64_t)kbB * d.nup + g) : 0.0;
+          a2[ks] = (g < nu && sh2[ks] != 0.0) ? sh2[ks] * __ldg(Bd + offB2[ks] + (int64_t)kbB * d.nup + g) : 0.0;
         double* Zk = Zs + (size_t)k * 8 * ZW;
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
@@ -192,7 +192,7 @@ k_fa_fused(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__
           if (((w - klo) % 8 + 8) % 8 <= K - klo) n2 += ring[(slot * 8 + w) * 8 + lane];
         const int cj = tl[4 + lane];
         const int64_t ij = bg + cj;
-        const double shat = (v.s[ij] == 1.0) ? 1.0 : 0.0;
+        const double shat = shat_of(v, v.s[ij]);
         double s;
         const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
         v.s[ij] = s;
@@ -271,7 +271,7 @@ k_fa_fused_r(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict
       const bool c2v = c2 < nc;
       const int cc = c2v ? tl[4 + c2] : 0;
       offB2[ks] = c2v ? v.offB[cc] : 0;
-      sh2[ks] = (c2v && v.s[bg + cc] == 1.0) ? 1.0 : 0.0;
+      sh2[ks] = c2v ? shat_of(v, v.s[bg + cc]) : 0.0;
     }
     double nrm = 0.0;
 #pragma unroll
@@ -311,7 +311,7 @@ k_fa_fused_r(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict
         }
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks)
-          a2[ks] = (g < nu && sh2[ks] != 0.0) ? __ldg(Bd + offB2[ks] + (int64_t)kbB * d.nup + g) : 0.0;
+          a2[ks] = (g < nu && sh2[ks] != 0.0) ? sh2[ks] * __ldg(Bd + offB2[ks] + (int64_t)kbB * d.nup + g) : 0.0;
         const double* Dk = Dm + (int64_t)k * nx * nu;
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
@@ -371,7 +371,7 @@ k_fa_fused_r(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict
           if (((w - klo) % NW + NW) % NW <= K - klo) n2 += ring[(slot * NW + w) * 8 + lane];
         const int cj = tl[4 + lane];
         const int64_t ij = bg + cj;
-        const double shat = (v.s[ij] == 1.0) ? 1.0 : 0.0;
+        const double shat = shat_of(v, v.s[ij]);
         double s;
         const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
         v.s[ij] = s;
@@ -473,6 +473,94 @@ k_zlist(Dev v, const double* __restrict__ y, const int32_t* __restrict__ clist,
   if (o1 < nu * nx) Zo[o1] = acc1;
 }
 
+// DMMA list adjoint: grid (B, ceil(T/16)), 16 warps, warp w owns step
+// k = 16 blockIdx.y + w.  The warp walks the cone list 32 entries at a time,
+// keeps (ballot) the cones that have a b-block at k, and folds them into
+// Z_k with DMMA 8 cones at a time:
+//   Z_k[m][i] += sum_c (w_c b_{c,k,m}) y_{c,k,i}   ([8 m x 4 c] x [4 c x 8 i]).
+template <int NTI>
+__global__ void __launch_bounds__(512)
+k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ clist,
+            const double* __restrict__ cw, const double* __restrict__ scale,
+            const int32_t* __restrict__ ncnt, int nfixed, const int32_t* __restrict__ act,
+            double* __restrict__ Zout) {
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, nup = d.nup;
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int k = blockIdx.y * 16 + warp;
+  if (k >= d.T) return;
+  double* Zo = Zout + ((int64_t)b * d.T + k) * nu * nx;
+  if (act && !act[b]) return;
+  const int n = ncnt ? ncnt[b] : nfixed;
+  const int64_t bg = (int64_t)b * d.ng;
+  const double* yb = y + (int64_t)b * d.E;
+  const double* Bd = v.Bd + (int64_t)b * d.EB;
+  double z[NTI][2];
+#pragma unroll
+  for (int nt = 0; nt < NTI; ++nt) { z[nt][0] = 0.0; z[nt][1] = 0.0; }
+  for (int base = 0; base < n; base += 32) {
+    // lane l inspects entry base + l
+    int j = 0;
+    double w = 0.0;
+    bool has = false;
+    if (base + lane < n) {
+      j = clist ? clist[bg + base + lane] : base + lane;
+      const int kind = v.kind[j], knot = v.knot[j];
+      has = (kind == 0) ? (knot > k) : (knot == k);
+      w = cw ? cw[bg + base + lane] : (scale ? scale[bg + j] : 1.0);
+      has = has && (w != 0.0);
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, has);
+    const int nv = __popc(mask);
+    // per-lane row pointers of valid entries (computed by their owner lanes)
+    int64_t yoff = 0, boff = 0;
+    if (has) {
+      const int kb = (v.kind[j] == 0) ? k : 0;
+      yoff = v.off[j] + (int64_t)kb * nx;
+      boff = v.offB[j] + (int64_t)kb * nup;
+    }
+    for (int g8 = 0; g8 < nv; g8 += 8) {
+      // the (g8 + c)-th set bit of mask is cone c of this group
+      double a2[2], bv[2][NTI];
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int c = g8 + q + 4 * ks;                       // A2 / B2 column index
+        int src = 0;
+        if (c < nv) {                                         // lane of the c-th set bit
+          unsigned mm = mask;
+          for (int t = 0; t < c; ++t) mm &= mm - 1;
+          src = __ffs(mm) - 1;
+        }
+        const int64_t yo = __shfl_sync(0xffffffffu, yoff, src);
+        const int64_t bo = __shfl_sync(0xffffffffu, boff, src);
+        const double ww = __shfl_sync(0xffffffffu, w, src);
+        const bool cv = c < nv;
+        a2[ks] = (cv && g < nu) ? ww * Bd[bo + g] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) {
+          const int i = g + 8 * nt;
+          bv[ks][nt] = (cv && i < nx) ? yb[yo + i] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) dmma(z[nt], a2[ks], bv[ks][nt]);
+    }
+  }
+  if (g < nu) {
+#pragma unroll
+    for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int i = 2 * q + r + 8 * nt;
+        if (i < nx) Zo[g * nx + i] = z[nt][r];
+      }
+  }
+}
+
 static int fused_variant(const Dims& d, int* nti, int* nks) {
   *nti = (d.nx + 7) / 8;
   *nks = (d.nu + 3) / 4;
@@ -532,6 +620,15 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,
                          double* Zout, cudaStream_t st) {
   Dev& v = h->dev;
+  if (v.d.nu <= 8 && v.d.nx <= 16) {
+    dim3 grid(v.d.B, (v.d.T + 15) / 16);
+    if (v.d.nx <= 8)
+      k_zlist_mma<1><<<grid, 512, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout);
+    else
+      k_zlist_mma<2><<<grid, 512, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout);
+    h->launches++;
+    return cudaGetLastError();
+  }
   k_zlist<<<v.d.B * v.d.T, 128, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout);
   h->launches++;
   return cudaGetLastError();

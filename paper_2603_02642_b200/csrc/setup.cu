@@ -154,16 +154,56 @@ __global__ void k_chain(Dev v) {
   const int b = (int)(gw / d.T), k = (int)(gw % d.T);
   const int64_t bk = (int64_t)b * d.T + k;
   const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + k) * nx * nx;
-  for (int r = lane; r < nx * nx; r += 32) {   // Sigma = Psi^T Psi
-    const int i = r / nx, c = r % nx;
-    double acc = 0.0;
-    for (int q = 0; q < nx; ++q) acc += Pk[q * nx + i] * Pk[q * nx + c];
-    S[r] = acc;
+  // Sigma_k depends on Psi_k only: the warp for the first step of a run of
+  // bit-identical Psi blocks (S = blkdiag(S_0, S_d, ..., S_d)) does the
+  // eigen-decomposition; the others wait for it in k_chain_copy.
+  int k0 = k;
+  while (k0 > 0) {
+    const double* Pp = v.Psi + ((int64_t)b * (d.T + 1) + k0 - 1) * nx * nx;
+    int same = 1;
+    for (int r = lane; r < nx * nx; r += 32) same &= (Pp[r] == Pk[r]);
+    if (!__all_sync(0xffffffffu, same)) break;
+    --k0;
+  }
+  v.Urep[bk] = k0;
+  if (k0 == k) {
+    for (int r = lane; r < nx * nx; r += 32) {   // Sigma = Psi^T Psi
+      const int i = r / nx, c = r % nx;
+      double acc = 0.0;
+      for (int q = 0; q < nx; ++q) acc += Pk[q * nx + i] * Pk[q * nx + c];
+      S[r] = acc;
+    }
+    __syncwarp();
+    warp_jacobi(S, Uq, nx);
+    for (int r = lane; r < nx; r += 32) v.Ulam[bk * nx + r] = S[r * nx + r];
+    for (int r = lane; r < nx * nx; r += 32) v.U[bk * nx * nx + r] = Uq[r];
   }
   __syncwarp();
-  warp_jacobi(S, Uq, nx);
-  for (int r = lane; r < nx; r += 32) lam[r] = S[r * nx + r];
-  for (int r = lane; r < nx * nx; r += 32) v.U[bk * nx * nx + r] = Uq[r];
+}
+
+// S1b: generalized eigen-chain of (Lambda_k, W'_k) per engine, with the
+// Sigma_k eigenpairs of step Urep[k] (identical Psi blocks share them).
+__global__ void k_chain2(Dev v) {
+  extern __shared__ double sm[];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu;
+  const int wpb = blockDim.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int per = 4 * nu * nu + nx + nu;
+  double* M = sm + (threadIdx.x >> 5) * per;
+  double* Q = M + nu * nu;
+  double* L = Q + nu * nu;
+  double* Li = L + nu * nu;
+  double* lam = Li + nu * nu;
+  double* sig = lam + nx;
+  if (gw >= (int64_t)d.B * d.T) return;
+  const int b = (int)(gw / d.T), k = (int)(gw % d.T);
+  const int64_t bk = (int64_t)b * d.T + k;
+  const int64_t bk0 = (int64_t)b * d.T + v.Urep[bk];
+  if (bk0 != bk)
+    for (int r = lane; r < nx * nx; r += 32) v.U[bk * nx * nx + r] = v.U[bk0 * nx * nx + r];
+  for (int r = lane; r < nx; r += 32) lam[r] = v.Ulam[bk0 * nx + r];
   __syncwarp();
   const double tau = v.tau[b];
   for (int eng = 0; eng < 2; ++eng) {
@@ -391,6 +431,9 @@ cudaError_t launch_setup(nrto_handle_s* h, cudaStream_t st) {
   const int wpb = 4;
   const int64_t nw = (int64_t)d.B * d.T;
   k_chain<<<(unsigned)((nw + wpb - 1) / wpb), 32 * wpb, wpb * per * sizeof(double), st>>>(v);
+  h->launches++;
+  k_chain2<<<(unsigned)((nw + wpb - 1) / wpb), 32 * wpb,
+             wpb * (4 * d.nu * d.nu + d.nx + d.nu) * sizeof(double), st>>>(v);
   h->launches++;
   const int rs = 3 * d.nx * d.nx + 2 * d.nx * d.nu + 3 * d.nu * d.nu + 2 * d.nu * d.nx;
   k_riccati<<<2 * d.B, 128, rs * sizeof(double), st>>>(v);

@@ -168,7 +168,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       const int c2 = q + 4 * ks;
-      sh2[ks] = (c2 < nc && v.s[bg + tl[4 + c2]] == 1.0) ? 1.0 : 0.0;   // shat = [s^{l-1} == 1]
+      sh2[ks] = (c2 < nc) ? shat_of(v, v.s[bg + tl[4 + c2]]) : 0.0;
     }
     double nrm = 0.0;
 #pragma unroll
@@ -212,7 +212,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
           }
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks)
-            a2[ks] = (g < nu && sh2[ks] != 0.0) ? sB[(q + 4 * ks) * G.SB + warp * nup + g] : 0.0;
+            a2[ks] = (g < nu && sh2[ks] != 0.0) ? sh2[ks] * sB[(q + 4 * ks) * G.SB + warp * nup + g] : 0.0;
         }
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
@@ -258,7 +258,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
         for (int w = 0; w < NW; ++w) n2 += ring[(slot * NW + w) * 8 + lane];
         const int cj = tl[4 + lane];
         const int64_t ij = bg + cj;
-        const double shat = (v.s[ij] == 1.0) ? 1.0 : 0.0;
+        const double shat = shat_of(v, v.s[ij]);
         double s;
         const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
         v.s[ij] = s;
