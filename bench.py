@@ -163,12 +163,14 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
     from paper_2603_02642_b200 import nrto
+    from paper_2603_02642_b200.dist import instance_range, max_over_ranks, batch_stats
     from gen import make_batch
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     B, L = args.batch_per_gpu, args.iters
-    shape, batch = make_batch(args.workload, B, start=rank * B)
+    first, count = instance_range(rank, world, B)
+    shape, batch = make_batch(args.workload, count, start=first)
     E, E_s, E_B = workload_shape_stats(shape)
     data_dev = nrto.to_tensors(batch, device=dev)
     solver = nrto.InnerSolver(shape, data_dev, max_iter=L, fixed_iters=1)
@@ -204,10 +206,7 @@ def run_ours(args, rank, world, local_rank):
     prof = solver.profile_read()
     solver.profile(False)
     ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms, device=dev)
     value = world * B * L / (ms_max / 1000.0)
 
     # ---- end to end through the C ABI with HOST buffers (H2D + D2H inside)
@@ -233,19 +232,12 @@ def run_ours(args, rank, world, local_rank):
         ev3.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ems = ev2.elapsed_time(ev3) / args.steps
-        te = torch.tensor([ems], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        ems = float(te.item())
+        ems = max_over_ranks(ev2.elapsed_time(ev3) / args.steps, device=dev)
         e2e = {"value": world * B * L / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "sl_iteration_wall_clock_ms": ems}
 
     # batch-wide residual statistics over NVLink (the only collective)
-    stats = torch.tensor([out["r_p"].max().item(), float(out["status"].ne(2).all().item())],
-                         dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    max_rp, n_unconv, any_div = batch_stats(out["r_p"], out["status"], device=dev)
 
     if rank != 0:
         return
@@ -294,7 +286,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
-        "residuals": {"max_r_p": float(stats[0].item()), "all_finite": bool(stats[1].item())},
+        "residuals": {"max_r_p": max_rp, "unconverged_instances": n_unconv,
+                      "any_diverged": any_div},
     }
     print(json.dumps(line), flush=True)
 

@@ -1,0 +1,76 @@
+"""World-size-2 gloo test of the instance-sharded multi-rank path (CPU).
+
+Each rank takes its instance range, solves its shard with the CPU oracle
+(standing in for the per-rank GPU handle), and the ranks meet only in the
+max-over-ranks time and the batch residual statistics -- the same calls
+bench.py makes over NCCL.  The sharded result must equal the unsharded one.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, per_rank, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_02642_b200.dist import instance_range, max_over_ranks, batch_stats
+    from gen.problems import make_unicycle
+    from oracle import structured as st
+    from oracle.params import make_params
+    first, count = instance_range(rank, world, per_rank)
+    r_p, status = [], []
+    for i in range(first, first + count):
+        shape, data = make_unicycle(1, i, T=6)
+        r = st.fulladmm(st.StructuredProblem(shape, data), make_params(max_iter=15, fixed_iters=1))
+        r_p.append(r["r_p"]); status.append(r["status"])
+    t = max_over_ranks(float(rank + 1))
+    stats = batch_stats(np.array(r_p), np.array(status))
+    out[rank] = (first, count, r_p, t, stats)
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_sharding():
+    world, per_rank = 2, 3
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, port, per_rank, out), nprocs=world, join=True)
+    firsts = sorted(out[r][0] for r in range(world))
+    assert firsts == [0, per_rank]                            # disjoint, covering ranges
+    assert all(out[r][3] == 2.0 for r in range(world))        # max over ranks
+    all_rp = out[0][2] + out[1][2]
+    for r in range(world):
+        mx, nun, div = out[r][4]
+        assert mx == pytest.approx(max(all_rp))
+        assert nun == world * per_rank and not div
+    # sharded results equal the unsharded computation instance by instance
+    from gen.problems import make_unicycle
+    from oracle import structured as st
+    from oracle.params import make_params
+    for i in range(world * per_rank):
+        shape, data = make_unicycle(1, i, T=6)
+        r = st.fulladmm(st.StructuredProblem(shape, data), make_params(max_iter=15, fixed_iters=1))
+        assert all_rp[i] == r["r_p"]
+
+
+def test_ranges():
+    from paper_2603_02642_b200.dist import instance_range, strong_range
+    assert instance_range(3, 8, 512) == (1536, 512)
+    cover = [strong_range(r, 3, 10) for r in range(3)]
+    assert cover == [(0, 4), (4, 3), (7, 3)]
+    with pytest.raises(ValueError):
+        instance_range(2, 2, 4)
