@@ -237,7 +237,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   AL(dtiles, tiles.size()); AL(dwitems, witems.size());
   v.tiles = dtiles; v.witems = dwitems;
   AL(v.Zpart, (v.fused ? B * nsplit : 1) * T * nu * nx); AL(v.Zc, B * T * nu * nx);
-  AL(v.Zctrl, B * T * nu * nx);
+  AL(v.Zctrl, B * T * nu * nx); AL(v.nrm2, B * ng);
   AL(v.clist, B * ng); AL(v.cw, B * ng); AL(v.ncorr, B);
 
   // shape arrays (pageable host vectors: synchronous copies)
@@ -368,31 +368,53 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
   };
   if (engine == NRTO_FULLADMM) {
     CK(launch_fa_reset(h, st));
+    // QP(l) only gates project(l+1): in fixed-iteration mode it runs on the aux
+    // stream concurrently with gain(l) and pass(l+1).
+    const bool overlap = v.fused >= 1 && prm.fixed_iters;
+    if (overlap && !h->aux) {
+      CK(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h->ev_proj, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_qp, cudaEventDisableTiming));
+    }
+    cudaStream_t st2 = h->aux;
+    auto timed2 = [&](cudaStream_t s2, int cls, auto&& fn) -> cudaError_t {
+      cudaEvent_t a = nullptr, b = nullptr;
+      if (h->prof) { a = prof_event(h); b = prof_event(h); cudaEventRecord(a, s2); }
+      cudaError_t e = fn(s2);
+      if (h->prof) { cudaEventRecord(b, s2); h->recs.push_back({cls, a, b}); }
+      return e;
+    };
     for (int l = 1; l <= prm.max_iter; ++l) {
       v.iter = l;
-      if (v.fused == 2) {
-        CK(timed(NRTO_K_PASS, launch_fa_tma));
-        CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
-          Dev& w = hh->dev;
-          return launch_zlist(hh, w.Y, w.clist, w.cw, nullptr, w.ncorr, 0, w.active, w.Zc, s2); }));
-      } else if (v.fused == 1) {
-        CK(timed(NRTO_K_PASS, launch_fa_fused));
-        CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
-          Dev& w = hh->dev;
-          return launch_zlist(hh, w.Y, w.clist, w.cw, nullptr, w.ncorr, 0, w.active, w.Zc, s2); }));
-      } else {
+      if (v.fused == 0) {
         CK(timed(NRTO_K_PASS, launch_fa_pass));
         CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
           return launch_adjoint(hh, hh->dev.Y, hh->dev.s, hh->dev.active, s2); }));
+        CK(timed(NRTO_K_GAIN, launch_fa_gain));
+        CK(timed_qp(NRTO_FULLADMM, l));
+      } else {
+        CK(timed(NRTO_K_PASS, v.fused == 2 ? launch_fa_tma : launch_fa_fused));
+        if (overlap && l > 1) CK(cudaStreamWaitEvent(st, h->ev_qp, 0));
+        CK(timed(NRTO_K_OTHER, launch_project));
+        if (overlap) {
+          CK(cudaEventRecord(h->ev_proj, st));
+          CK(cudaStreamWaitEvent(st2, h->ev_proj, 0));
+          CK(timed2(st2, NRTO_K_QP, [&](cudaStream_t s2) { return launch_qp_lite(h, NRTO_FULLADMM, l, s2); }));
+          CK(cudaEventRecord(h->ev_qp, st2));
+        }
+        CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
+          Dev& w = hh->dev;
+          return launch_zlist(hh, w.Y, w.clist, w.cw, nullptr, w.ncorr, 0, w.active, w.Zc, s2); }));
+        CK(timed(NRTO_K_GAIN, launch_fa_gain));
+        if (!overlap) CK(timed_qp(NRTO_FULLADMM, l));
       }
-      CK(timed(NRTO_K_GAIN, launch_fa_gain));
-      CK(timed_qp(NRTO_FULLADMM, l));
       if (!prm.fixed_iters && l % prm.check_every == 0 && l < prm.max_iter) {
         const int c = poll_active(h, dcount, 0, st, &ce);
         if (ce != cudaSuccess) return cuda_fail(ce, "poll");
         if (c == 0) break;
       }
     }
+    if (overlap) CK(cudaStreamWaitEvent(st, h->ev_qp, 0));
   } else {
     CK(launch_dr_reset(h, h->dr_fresh, st));
     h->dr_fresh = 0;
@@ -465,6 +487,9 @@ extern "C" nrto_err nrto_destroy(nrto_handle h) {
   cudaDeviceSynchronize();
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
+  if (h->ev_proj) cudaEventDestroy(h->ev_proj);
+  if (h->ev_qp) cudaEventDestroy(h->ev_qp);
+  if (h->aux) cudaStreamDestroy(h->aux);
   free_all(h);
   delete h;
   return NRTO_OK;

@@ -74,6 +74,7 @@ struct Dev {
                            // correction; 2: k_fa_tma (state tiles) + k_fa_ctrl + correction
   int nctrl;               // number of control cones
   int iter;                // outer iteration l of the launch (set by the host loop)
+  double* nrm2;            // [B][ng] ||y^l||^2 written by the fused pass
   double* Zctrl;           // [B][T][nu][nx] exact adjoint of the control cones (fused == 2)
   int ntiles, nsplit, nwitems;
   const int32_t* tiles;    // [ntiles][12] kind, knot, nc, klo, cone[8]
@@ -100,6 +101,9 @@ struct nrto_handle_s {
   int prof = 0;
   std::vector<nrto_prof_rec> recs;
   std::vector<cudaEvent_t> pool;
+  // second stream for the QP(l) || pass(l+1) overlap (fixed-iteration mode)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_proj = nullptr, ev_qp = nullptr;
 };
 
 namespace nrto {
@@ -169,5 +173,7 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
 bool fused_supported(const Dims& d);
 bool tma_supported(const Dims& d);
 cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_project(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st);
 
 }  // namespace nrto

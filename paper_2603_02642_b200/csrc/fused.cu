@@ -190,18 +190,7 @@ k_fa_fused(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__
         double n2 = 0.0;
         for (int w = 0; w < 8; ++w)
           if (((w - klo) % 8 + 8) % 8 <= K - klo) n2 += ring[(slot * 8 + w) * 8 + lane];
-        const int cj = tl[4 + lane];
-        const int64_t ij = bg + cj;
-        const double shat = shat_of(v, v.s[ij]);
-        double s;
-        const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
-        v.s[ij] = s;
-        v.pt[ij] = tp;
-        if (s != shat) {
-          const int pos = atomicAdd(&v.ncorr[b], 1);
-          v.clist[bg + pos] = cj;
-          v.cw[bg + pos] = s - shat;
-        }
+        v.nrm2[bg + tl[4 + lane]] = n2;     // projection decided by k_project
       }
       __syncwarp();
       if (lane == 0) {
@@ -369,18 +358,7 @@ k_fa_fused_r(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict
         double n2 = 0.0;
         for (int w = 0; w < NW; ++w)
           if (((w - klo) % NW + NW) % NW <= K - klo) n2 += ring[(slot * NW + w) * 8 + lane];
-        const int cj = tl[4 + lane];
-        const int64_t ij = bg + cj;
-        const double shat = shat_of(v, v.s[ij]);
-        double s;
-        const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
-        v.s[ij] = s;
-        v.pt[ij] = tp;
-        if (s != shat) {
-          const int pos = atomicAdd(&v.ncorr[b], 1);
-          v.clist[bg + pos] = cj;
-          v.cw[bg + pos] = s - shat;
-        }
+        v.nrm2[bg + tl[4 + lane]] = n2;     // projection decided by k_project
       }
       __syncwarp();
       if (lane == 0) {

@@ -191,6 +191,97 @@ __global__ void k_fa_gain(Dev v, int mode, const double* kin, double* kout) {
   }
 }
 
+// Warp-level versions: one warp per (instance, step), 8 per CTA (the 7x14
+// chain has 98 outputs, so a CTA per step mostly idles and the tiny CTAs
+// crowd the SMs the concurrently running QP needs).
+__device__ void chain_solve_w(const double* V, const double* U, const double* den,
+                              double* sR, double* sX, int nu, int nx, int lane) {
+  for (int r = lane; r < nu * nx; r += 32) {
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+    for (int q = 0; q < nu; ++q) acc += V[q * nu + a] * sR[q * nx + c];
+    sX[r] = acc;
+  }
+  __syncwarp();
+  for (int r = lane; r < nu * nx; r += 32) {
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[q * nx + c];
+    sR[r] = acc * den[r];
+  }
+  __syncwarp();
+  for (int r = lane; r < nu * nx; r += 32) {
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+    for (int q = 0; q < nu; ++q) acc += V[a * nu + q] * sR[q * nx + c];
+    sX[r] = acc;
+  }
+  __syncwarp();
+  for (int r = lane; r < nu * nx; r += 32) {
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[c * nx + q];
+    sR[r] = acc;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
+  extern __shared__ double sm[];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + warp;
+  if (gw >= (int64_t)d.B * d.T) return;
+  const int b = (int)(gw / d.T), k = (int)(gw % d.T);
+  if (!v.active[b]) return;
+  const int64_t bk = (int64_t)b * d.T + k;
+  double* sR = sm + (size_t)warp * 3 * nu * nx;
+  double* sX = sR + nu * nx;
+  double* sK = sX + nu * nx;
+  const double st = sqrt(v.tau[b]);
+  const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + k) * nx * nx;
+  const double* Wk = v.W + bk * nu * nu;
+  double* Kb = v.K + (int64_t)b * d.NK + (int64_t)k * nu * nx;
+  for (int r = lane; r < nu * nx; r += 32) {
+    double z = v.Zc[bk * nu * nx + r];
+    if (v.fused == 2) z += v.Zctrl[bk * nu * nx + r];
+    const double* zp = v.Zpart + ((int64_t)b * v.nsplit * d.T + k) * nu * nx + r;
+    for (int sp = 0; sp < v.nsplit; ++sp) z += zp[(int64_t)sp * d.T * nu * nx];
+    sX[r] = z - v.Zb[bk * nu * nx + r];
+    const int m = r / nx, i = r % nx;
+    sK[r] = Kb[i * nu + m];
+  }
+  if (k == 0 && lane == 0) v.ncorr[b] = 0;      // correction list consumed
+  __syncwarp();
+  const double rho = v.prm.rho;
+  for (int r = lane; r < nu * nx; r += 32) {
+    const int m = r / nx, i = r % nx;
+    double gp = 0.0, wk = 0.0;
+    for (int q = 0; q < nx; ++q) gp += sX[m * nx + q] * Pk[q * nx + i];
+    for (int q = 0; q < nu; ++q) wk += Wk[m * nu + q] * sK[q * nx + i];
+    sR[r] = 2.0 * wk + rho * st * gp;
+  }
+  __syncwarp();
+  chain_solve_w(v.fa.V + bk * nu * nu, v.U + bk * nx * nx, v.fa.den + bk * nu * nx, sR, sX,
+                nu, nx, lane);
+  for (int r = lane; r < nu * nx; r += 32) {
+    const int m = r / nx, i = r % nx;
+    Kb[i * nu + m] = sR[r];
+  }
+  for (int r = lane; r < nx * nu; r += 32) {    // C = sqrt(tau) Psi K^T ; D = 2C - Cold
+    const int i = r / nu, m = r % nu;
+    double acc = 0.0;
+    for (int q = 0; q < nx; ++q) acc += Pk[i * nx + q] * sR[m * nx + q];
+    const double c = st * acc;
+    const int64_t idx = bk * nx * nu + r;
+    const double cold = v.Ccur[idx];
+    v.Cprev[idx] = cold;
+    v.Ccur[idx] = c;
+    v.D[idx] = 2.0 * c - cold;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // DR engine.  Affine prox (11a) via the Schur form of K_KKT (F3):
 //   (Q_v + sigma I + r_s sum A^T A) k = sigma k~ + r_s sum A^T (eta~ - b_hat)
@@ -462,6 +553,12 @@ cudaError_t launch_fa_pass(nrto_handle_s* h, cudaStream_t st) {
 cudaError_t launch_fa_gain(nrto_handle_s* h, cudaStream_t st) {
   Dev& v = h->dev;
   const Dims& d = v.d;
+  if (v.fused) {
+    const int64_t nw = (int64_t)d.B * d.T;
+    k_fa_gain_w<<<(unsigned)((nw + 7) / 8), 256, 8 * 3 * d.nu * d.nx * sizeof(double), st>>>(v);
+    h->launches++;
+    return cudaGetLastError();
+  }
   k_fa_gain<<<d.B * d.T, 128, 3 * d.nu * d.nx * sizeof(double), st>>>(v, 0, nullptr, nullptr);
   h->launches++;
   return cudaGetLastError();

@@ -256,18 +256,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       if (lane < nc) {
         double n2 = 0.0;
         for (int w = 0; w < NW; ++w) n2 += ring[(slot * NW + w) * 8 + lane];
-        const int cj = tl[4 + lane];
-        const int64_t ij = bg + cj;
-        const double shat = shat_of(v, v.s[ij]);
-        double s;
-        const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
-        v.s[ij] = s;
-        v.pt[ij] = tp;
-        if (s != shat) {
-          const int pos = atomicAdd(&v.ncorr[b], 1);
-          v.clist[bg + pos] = cj;
-          v.cw[bg + pos] = s - shat;
-        }
+        v.nrm2[bg + tl[4 + lane]] = n2;     // projection decided by k_project
       }
       __syncwarp();
       if (lane == 0) {
@@ -294,8 +283,9 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
   }
 }
 
-// Control cones (single block at step k): y = D_k h' + (1 - s) y_old, exact
-// projection, and the exact adjoint Zctrl_k = sum_{ctrl j@k} s_j h'_j y_j^T.
+// Control cones (single block at step k): y = D_k h' + (1 - s) y_old, ||y||^2,
+// and the predicted adjoint Zctrl_k = sum_{ctrl j@k} shat_j h'_j y_j^T
+// (k_project appends mispredicted cones to the correction list).
 // One warp per step; lane i < n_x holds y_i; Z_k[:, i] accumulates in lane i.
 __global__ void __launch_bounds__(512)
 k_fa_ctrl(Dev v) {
@@ -331,18 +321,48 @@ k_fa_ctrl(Dev v) {
       Y[v.off[j] + lane] = y;
     }
     const double n2 = warp_sum(y * y);
-    double s;
-    const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
+    const double sh = shat_of(v, v.s[ij]);          // predicted scale (k_project corrects)
     __syncwarp();
-    if (lane == 0) { v.s[ij] = s; v.pt[ij] = tp; }
+    if (lane == 0) v.nrm2[ij] = n2;
 #pragma unroll
-    for (int m = 0; m < 8; ++m) zc[m] += s * bm[m] * y;
+    for (int m = 0; m < 8; ++m) zc[m] += sh * bm[m] * y;
   }
   if (lane < nx) {
     double* Zo = v.Zctrl + ((int64_t)b * d.T + k) * nu * nx;
     for (int m = 0; m < nu; ++m) Zo[m * nx + lane] = zc[m];
   }
   (void)nup;
+}
+
+// Projection of every cone of the batch from its ||y^l||^2 (SM Eq.(18)):
+// s^l, p~^l; cones whose s^l differs from the prediction shat used by the
+// pass (shat_of(s^{l-1})) go to the correction list with weight s^l - shat.
+// Runs after QP(l-1) (it needs t = p^{l-1} + lam_p^{l-1}).
+__global__ void k_project(Dev v) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)v.d.B * v.d.ng;
+  if (id >= n) return;
+  const int b = (int)(id / v.d.ng), j = (int)(id % v.d.ng);
+  if (!v.active[b]) return;
+  const double shat = shat_of(v, v.s[id]);
+  double s;
+  const double tp = soc_case(v.tin[id], sqrt(v.nrm2[id]), &s);
+  v.s[id] = s;
+  v.pt[id] = tp;
+  if (s != shat) {
+    const int pos = atomicAdd(&v.ncorr[b], 1);
+    v.clist[(int64_t)b * v.d.ng + pos] = j;
+    v.cw[(int64_t)b * v.d.ng + pos] = s - shat;
+  }
+}
+
+cudaError_t launch_project(nrto_handle_s* h, cudaStream_t st) {
+  const int64_t n = (int64_t)h->dev.d.B * h->dev.d.ng;
+  if (n > 0) {
+    k_project<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->dev);
+    h->launches++;
+  }
+  return cudaGetLastError();
 }
 
 size_t tma_smem_bytes(const Dims& d) {
