@@ -204,6 +204,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   v.fused = use_tma ? 2 : ((fused_supported(d) && ntiles > 0) ? 1 : 0);
   v.nctrl = nctrl;
   v.ntiles = ntiles; v.nsplit = nsplit; v.nwitems = (int)(witems.size() / 4);
+  v.nstate_tiles = nstate_tiles;
 
   const int64_t B = d.B;
   int32_t *dknot, *dkind, *dkptr, *dkcone, *dsptr, *dsrow, *dcptr, *dcrow;
@@ -328,28 +329,24 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
   const bool host = o->memory == NRTO_MEM_HOST;
   const int64_t B = d.B;
   const size_t D8 = sizeof(double);
-  // staging for kernel-written optional outputs when the caller wants host memory
+  // handle-owned staging for kernel-written optional outputs in host mode
   double *nu_d = o->nu, *lam_d = o->lam_nu, *obj_d = o->objective, *mc_d = o->margin_cone,
          *ml_d = o->margin_lin;
-  std::vector<void*> tmp;
-  auto stage = [&](double** p, int64_t n) -> nrto_err {
-    if (!*p || !host) return NRTO_OK;
-    void* q = nullptr;
-    cudaError_t e = cudaMallocAsync(&q, (size_t)std::max<int64_t>(n, 1) * D8, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(staging)");
-    tmp.push_back(q);
-    *p = (double*)q;
-    return NRTO_OK;
-  };
-  nrto_err ee;
-  if ((ee = stage(&nu_d, B * d.E)) != NRTO_OK) return ee;
-  if ((ee = stage(&lam_d, B * d.E)) != NRTO_OK) return ee;
-  if ((ee = stage(&obj_d, B)) != NRTO_OK) return ee;
-  if ((ee = stage(&mc_d, B * d.ng)) != NRTO_OK) return ee;
-  if ((ee = stage(&ml_d, B * d.ng)) != NRTO_OK) return ee;
-  int32_t* dcount = nullptr;
-  CK(cudaMallocAsync((void**)&dcount, 4, st));
-  tmp.push_back(dcount);
+  if (!h->dcount) {
+    CK(cudaMalloc((void**)&h->dcount, 4));
+    CK(cudaMalloc((void**)&h->stage_ng2, (size_t)std::max<int64_t>(2 * B * d.ng, 1) * D8));
+    CK(cudaMalloc((void**)&h->stage_b, (size_t)B * D8));
+  }
+  if (host) {
+    if ((o->nu || o->lam_nu) && !h->stage_e2)
+      CK(cudaMalloc((void**)&h->stage_e2, (size_t)std::max<int64_t>(2 * B * d.E, 1) * D8));
+    if (o->nu) nu_d = h->stage_e2;
+    if (o->lam_nu) lam_d = h->stage_e2 + B * d.E;
+    if (o->objective) obj_d = h->stage_b;
+    if (o->margin_cone) mc_d = h->stage_ng2;
+    if (o->margin_lin) ml_d = h->stage_ng2 + B * d.ng;
+  }
+  int32_t* dcount = h->dcount;
 
   cudaError_t ce = cudaSuccess;
   auto timed = [&](int cls, cudaError_t (*fn)(nrto_handle_s*, cudaStream_t)) -> cudaError_t {
@@ -459,7 +456,6 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     CK(copy_out(o->margin_cone, mc_d, B * d.ng * D8, true, st));
     CK(copy_out(o->margin_lin, ml_d, B * d.ng * D8, true, st));
   }
-  for (void* q : tmp) CK(cudaFreeAsync(q, st));
   if (host) CK(cudaStreamSynchronize(st));
   return NRTO_OK;
 }
@@ -490,6 +486,10 @@ extern "C" nrto_err nrto_destroy(nrto_handle h) {
   if (h->ev_proj) cudaEventDestroy(h->ev_proj);
   if (h->ev_qp) cudaEventDestroy(h->ev_qp);
   if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->dcount) cudaFree(h->dcount);
+  if (h->stage_ng2) cudaFree(h->stage_ng2);
+  if (h->stage_b) cudaFree(h->stage_b);
+  if (h->stage_e2) cudaFree(h->stage_e2);
   free_all(h);
   delete h;
   return NRTO_OK;

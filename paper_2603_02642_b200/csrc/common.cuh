@@ -77,6 +77,7 @@ struct Dev {
   double* nrm2;            // [B][ng] ||y^l||^2 written by the fused pass
   double* Zctrl;           // [B][T][nu][nx] exact adjoint of the control cones (fused == 2)
   int ntiles, nsplit, nwitems;
+  int nstate_tiles;        // state tiles come first in `tiles`
   const int32_t* tiles;    // [ntiles][12] kind, knot, nc, klo, cone[8]
   const int32_t* witems;   // [nwitems][4] b, t0, t1, split index
   double* Zpart;           // [B][nsplit][T][nu][nx] per-work-item adjoint partials
@@ -104,6 +105,11 @@ struct nrto_handle_s {
   // second stream for the QP(l) || pass(l+1) overlap (fixed-iteration mode)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_proj = nullptr, ev_qp = nullptr;
+  // persistent staging for host-memory outputs and the active-count poll
+  double* stage_ng2 = nullptr;   // [2][B][ng]  margins
+  double* stage_b = nullptr;     // [B]         objective
+  double* stage_e2 = nullptr;    // [2][B][E]   nu, lam_nu (allocated on first host request)
+  int32_t* dcount = nullptr;
 };
 
 namespace nrto {
@@ -172,6 +178,7 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
                          double* Zout, cudaStream_t st);
 bool fused_supported(const Dims& d);
 bool tma_supported(const Dims& d);
+cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_project(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st);

@@ -539,6 +539,192 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
   }
 }
 
+// ---------------------------------------------------------------------------
+// S0 on tensor cores: costate sweep for a tile of <= 8 state cones with the
+// same knot K (rows = cones), one warp per (instance, tile):
+//   C_K = [grad_j]; for k = K..0:  b_k = C_{k+1} B_k,  C_k = C_{k+1} A_k,
+//   b_hat_k = sqrt(tau) C_k Psi_k^T          (row form of P:846-866)
+// as DMMA chains [8 cones x 4 r] x [4 r x 8 cols], contraction over n_x <= 16.
+template <int NTI>
+__device__ __forceinline__ void c_as_a(const double (&C)[NTI][2], int g, int q, double (&a)[4]) {
+  // A operand [row g][col 4ks + q] of the accumulator-layout matrix C
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int col = 4 * ks + q;
+    const int nt = col >> 3, src = g * 4 + ((col & 7) >> 1);
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < NTI; ++t) {
+      const double x0 = __shfl_sync(0xffffffffu, C[t][0], src);
+      const double x1 = __shfl_sync(0xffffffffu, C[t][1], src);
+      if (t == nt) { v0 = x0; v1 = x1; }
+    }
+    a[ks] = (nt < NTI) ? ((col & 1) ? v1 : v0) : 0.0;
+  }
+}
+
+template <int NTI>
+__global__ void __launch_bounds__(256) k_costate_mma(Dev v, const int32_t* __restrict__ tiles,
+                                                     int ntiles) {
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, nup = d.nup;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + warp;
+  if (gw >= (int64_t)d.B * ntiles) return;
+  const int b = (int)(gw / ntiles), t = (int)(gw % ntiles);
+  const int* tl = tiles + (int64_t)t * 12;
+  const int K = tl[1], nc = tl[2];
+  const bool gv = g < nc;
+  const int cg = gv ? tl[4 + g] : 0;
+  const double st = sqrt(v.tau[b]);
+  const double* A = v.A + (int64_t)b * d.T * nx * nx;
+  const double* Bm = v.Bm + (int64_t)b * d.T * nx * nu;
+  const double* Psi = v.Psi + (int64_t)b * (d.T + 1) * nx * nx;
+  double* bh = v.bhat + (int64_t)b * d.E + (gv ? v.off[cg] : 0);
+  double* Bd = v.Bd + (int64_t)b * d.EB + (gv ? v.offB[cg] : 0);
+  const double* grad = v.grad + ((int64_t)b * d.ng + cg) * nx;
+  double C[NTI][2];
+#pragma unroll
+  for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int i = 2 * q + r + 8 * nt;
+      C[nt][r] = (gv && i < nx) ? grad[i] : 0.0;
+    }
+  for (int k = K; k >= 0; --k) {
+    double a[4];
+    if (k < K) {
+      c_as_a<NTI>(C, g, q, a);                        // C = c_{k+1} rows
+      const double* Bk = Bm + (int64_t)k * nx * nu;
+      const double* Ak = A + (int64_t)k * nx * nx;
+      double bb[2] = {0.0, 0.0};
+      double Cn[NTI][2];
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) { Cn[nt][0] = 0.0; Cn[nt][1] = 0.0; }
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int r = 4 * ks + q;
+        const double bop = (r < nx && g < nu) ? __ldg(Bk + r * nu + g) : 0.0;
+        dmma(bb, a[ks], bop);
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) {
+          const int i = g + 8 * nt;
+          const double aop = (r < nx && i < nx) ? __ldg(Ak + r * nx + i) : 0.0;
+          dmma(Cn[nt], a[ks], aop);
+        }
+      }
+      if (gv) {                                        // b_k row (padded to nup)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int m = 2 * q + rr;
+          if (m < nup) Bd[(int64_t)k * nup + m] = (m < nu) ? bb[rr] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) { C[nt][0] = Cn[nt][0]; C[nt][1] = Cn[nt][1]; }
+    }
+    c_as_a<NTI>(C, g, q, a);                          // C = c_k rows
+    const double* Pk = Psi + (int64_t)k * nx * nx;
+    double h[NTI][2];
+#pragma unroll
+    for (int nt = 0; nt < NTI; ++nt) { h[nt][0] = 0.0; h[nt][1] = 0.0; }
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int r = 4 * ks + q;
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) {
+        const int i = g + 8 * nt;
+        const double pop = (r < nx && i < nx) ? __ldg(Pk + i * nx + r) : 0.0;   // Psi_k^T
+        dmma(h[nt], a[ks], pop);
+      }
+    }
+    if (gv) {
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int i = 2 * q + rr + 8 * nt;
+          if (i < nx) bh[(int64_t)k * nx + i] = st * h[nt][rr];
+        }
+    }
+  }
+}
+
+// Control cones for the MMA setup path: b = h'_j (padded), b_hat row = 0.
+__global__ void k_costate_ctrl(Dev v) {
+  const Dims d = v.d;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)d.B * d.ng) return;
+  const int b = (int)(id / d.ng), j = (int)(id % d.ng);
+  if (v.kind[j] == 0) return;
+  const double* grad = v.grad + ((int64_t)b * d.ng + j) * d.nx;
+  double* Bd = v.Bd + (int64_t)b * d.EB + v.offB[j];
+  double* bh = v.bhat + (int64_t)b * d.E + v.off[j];
+  for (int m = 0; m < d.nup; ++m) Bd[m] = (m < d.nu) ? grad[m] : 0.0;
+  for (int i = 0; i < d.nx; ++i) bh[i] = 0.0;
+}
+
+// Lambda_k = sum_j b_{j,k} b_{j,k}^T over the cones with a b-block at k, DMMA
+// [8 m x 4 c] x [4 c x 8 m'] per 8 cones (same walk as k_zlist_mma).
+__global__ void __launch_bounds__(512) k_lam_mma(Dev v) {
+  const Dims d = v.d;
+  const int nu = d.nu, nup = d.nup;
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int k = blockIdx.y * 16 + warp;
+  if (k >= d.T) return;
+  const double* Bd = v.Bd + (int64_t)b * d.EB;
+  double z[2] = {0.0, 0.0};
+  for (int base = v.kptr[k]; base < v.kptr[k + 1]; base += 8) {
+    const int cnt = min(8, v.kptr[k + 1] - base);
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int c = q + 4 * ks;
+      double a2 = 0.0, bv = 0.0;
+      if (c < cnt) {
+        const int j = v.kcone[base + c];
+        const int kb = (v.kind[j] == 0) ? k : 0;
+        const double* row = Bd + v.offB[j] + (int64_t)kb * nup;
+        a2 = (g < nu) ? row[g] : 0.0;
+        bv = (g < nu) ? row[g] : 0.0;
+      }
+      dmma(z, a2, bv);
+    }
+  }
+  if (g < nu) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int m2 = 2 * q + r;
+      if (m2 < nu) v.Lam[((int64_t)b * d.T + k) * nu * nu + g * nu + m2] = z[r];
+    }
+  }
+}
+
+cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  const int nst = v.nstate_tiles;
+  if ((int64_t)d.B * d.ng > 0) {
+    k_costate_ctrl<<<(unsigned)(((int64_t)d.B * d.ng + 255) / 256), 256, 0, st>>>(v);
+    h->launches++;
+  }
+  if (nst > 0) {
+    const int64_t nw = (int64_t)d.B * nst;
+    if (d.nx <= 8)
+      k_costate_mma<1><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(v, v.tiles, nst);
+    else
+      k_costate_mma<2><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(v, v.tiles, nst);
+    h->launches++;
+  }
+  dim3 grid(d.B, (d.T + 15) / 16);
+  k_lam_mma<<<grid, 512, 0, st>>>(v);
+  h->launches++;
+  // Zb_k = sum_j b_{j,k} b_hat_{j,k}^T : the list adjoint with y = b_hat
+  return launch_zlist(h, v.bhat, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, v.Zb, st);
+}
+
 static int fused_variant(const Dims& d, int* nti, int* nks) {
   *nti = (d.nx + 7) / 8;
   *nks = (d.nu + 3) / 4;

@@ -420,13 +420,18 @@ cudaError_t launch_setup(nrto_handle_s* h, cudaStream_t st) {
   const Dims& d = v.d;
   int zero = 0;
   cudaMemcpyToSymbolAsync(g_setup_err, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st);
-  if ((int64_t)d.B * d.ng > 0) {
-    const int64_t warps = (int64_t)d.B * d.ng;
-    k_costate<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(v);
+  if (d.nx <= 16 && d.nu <= 8) {              // tensor-core S0 / S0b
+    cudaError_t e = launch_setup_mma(h, st);
+    if (e != cudaSuccess) return e;
+  } else {
+    if ((int64_t)d.B * d.ng > 0) {
+      const int64_t warps = (int64_t)d.B * d.ng;
+      k_costate<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(v);
+      h->launches++;
+    }
+    k_lam_zb<<<d.B * d.T, 128, 0, st>>>(v);
     h->launches++;
   }
-  k_lam_zb<<<d.B * d.T, 128, 0, st>>>(v);
-  h->launches++;
   const int per = 2 * d.nx * d.nx + 4 * d.nu * d.nu + d.nx + d.nu;
   const int wpb = 4;
   const int64_t nw = (int64_t)d.B * d.T;
