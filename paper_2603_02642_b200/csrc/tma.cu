@@ -46,12 +46,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Streaming (read-once) TMA load: L2 evict-first policy so the 30 GB/iteration
+// cone stream does not flush the concurrently running QP's working set.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
+                                         uint64_t* bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           saddr(dst)),
-      "l"(src), "r"(bytes), "r"(saddr(bar))
+      "l"(src), "r"(bytes), "r"(saddr(bar)), "l"(pol)
       : "memory");
 }
 
@@ -112,6 +119,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
     // lane c < nc owns cone c of the tile: its offsets are loaded once per tile
     // and it issues that cone's bulk copies; lane 0 arms the stage barrier.
     int n = 0;
+    const uint64_t pol = policy_evict_first();
     int tnext = t0;
     int64_t offn = 0, offBn = 0;
     if (tnext < t1 && lane < tiles[(int64_t)tnext * kTI + 2]) {
@@ -140,10 +148,10 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
           double* sH = sY + 8 * G.SY;
           double* sB = sH + 8 * G.SY;
           const int64_t o = offc + (int64_t)kc * nx;
-          bulk_g2s(sY + lane * G.SY, Y + o, nb * nx * 8, &full[st]);
-          bulk_g2s(sH + lane * G.SY, bhat + o, nb * nx * 8, &full[st]);
+          bulk_g2s(sY + lane * G.SY, Y + o, nb * nx * 8, &full[st], pol);
+          bulk_g2s(sH + lane * G.SY, bhat + o, nb * nx * 8, &full[st], pol);
           if (nbB > 0)
-            bulk_g2s(sB + lane * G.SB, Bd + offBc + (int64_t)kc * nup, nbB * nup * 8, &full[st]);
+            bulk_g2s(sB + lane * G.SB, Bd + offBc + (int64_t)kc * nup, nbB * nup * 8, &full[st], pol);
         }
       }
     }
