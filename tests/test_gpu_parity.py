@@ -248,3 +248,21 @@ def test_empty_cone_set():
     o = oracle_run(sh0, d0, nrto.NRTO_FULLADMM, max_iter=5, fixed_iters=1)
     assert np.all(g["kv"] == 0)
     assert close(g["du"][0], o["du"], tol=1e-9)
+
+
+# ------------------------------------------------ c4: long horizons (other kernel paths)
+@pytest.mark.parametrize("T,n_obs,L", [(150, 6, 3), (200, 4, 2), (400, 2, 1)])
+def test_fulladmm_long_horizon(T, n_obs, L):
+    """T=150: shared-memory-Z fused pass; T>=200: generic pass + dense adjoint."""
+    shape, data = make_quad(4, 7, T=T, n_obs=n_obs)
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_FULLADMM, max_iter=L, fixed_iters=1)
+    o = oracle_run(shape, data, nrto.NRTO_FULLADMM, max_iter=L, fixed_iters=1)
+    assert_parity(g, o)
+
+
+def test_dr_long_horizon():
+    shape, data = make_quad(4, 8, T=150, n_obs=4)
+    kw = dict(max_admm_iter=2, max_dr_iter=3, fixed_iters=1)
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_DR, **kw)
+    o = oracle_run(shape, data, nrto.NRTO_DR, **kw)
+    assert_parity(g, o, engine=1)
