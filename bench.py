@@ -276,8 +276,8 @@ def run_ours(args, rank, world, local_rank):
         "cone_elements_per_s": value * E,
         "sl_iteration_wall_clock_ms": (e2e or {}).get("sl_iteration_wall_clock_ms"),
         "kernel_ms_per_step": kernel_ms,
-        "roofline": {"bound": "hbm", "kernel": "k_fa_pass (S3 forward map + S4 SOC projection + "
-                                                "S5 state update)",
+        "roofline": {"bound": "hbm", "kernel": "k_fa_tma: fused cone pass (S3 forward map + S4 SOC "
+                                                "norms + S5 state update + S7 predicted adjoint)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_kind": peak_kind,

@@ -367,13 +367,31 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     CK(launch_fa_reset(h, st));
     // QP(l) only gates project(l+1): in fixed-iteration mode it runs on the aux
     // stream concurrently with gain(l) and pass(l+1).
-    const bool overlap = v.fused >= 1 && prm.fixed_iters;
+    // overlap needs enough instances to keep the SMs busy with the pass while the
+    // QP runs; for small batches the QP is on the critical path and the wide
+    // staged variant (Acl in shared memory, 1024 threads) is used in order.
+    int nsm = 148;
+    { int dev = 0; if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); }
+    const bool overlap = v.fused >= 1 && prm.fixed_iters && d.B >= nsm;
     if (overlap && !h->aux) {
-      CK(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+      // the cone-pass chain gets the highest stream priority so that SM slots freed
+      // by finishing pass CTAs go to pass CTAs; QP CTAs fill the leftover room
+      int lo = 0, hp = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hp));
+      CK(cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, lo));
+      CK(cudaStreamCreateWithPriority(&h->hi, cudaStreamNonBlocking, hp));
       CK(cudaEventCreateWithFlags(&h->ev_proj, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&h->ev_qp, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
     }
     cudaStream_t st2 = h->aux;
+    const cudaStream_t user_st = st;
+    if (overlap) {                 // run the loop on the internal streams, joined to `st`
+      CK(cudaEventRecord(h->ev_in, user_st));
+      CK(cudaStreamWaitEvent(h->hi, h->ev_in, 0));
+      st = h->hi;
+    }
     auto timed2 = [&](cudaStream_t s2, int cls, auto&& fn) -> cudaError_t {
       cudaEvent_t a = nullptr, b = nullptr;
       if (h->prof) { a = prof_event(h); b = prof_event(h); cudaEventRecord(a, s2); }
@@ -411,7 +429,12 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
         if (c == 0) break;
       }
     }
-    if (overlap) CK(cudaStreamWaitEvent(st, h->ev_qp, 0));
+    if (overlap) {
+      CK(cudaStreamWaitEvent(st, h->ev_qp, 0));
+      CK(cudaEventRecord(h->ev_out, st));
+      CK(cudaStreamWaitEvent(user_st, h->ev_out, 0));
+      st = user_st;
+    }
   } else {
     CK(launch_dr_reset(h, h->dr_fresh, st));
     h->dr_fresh = 0;
@@ -486,6 +509,9 @@ extern "C" nrto_err nrto_destroy(nrto_handle h) {
   if (h->ev_proj) cudaEventDestroy(h->ev_proj);
   if (h->ev_qp) cudaEventDestroy(h->ev_qp);
   if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->hi) cudaStreamDestroy(h->hi);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->dcount) cudaFree(h->dcount);
   if (h->stage_ng2) cudaFree(h->stage_ng2);
   if (h->stage_b) cudaFree(h->stage_b);

@@ -103,8 +103,9 @@ struct nrto_handle_s {
   std::vector<nrto_prof_rec> recs;
   std::vector<cudaEvent_t> pool;
   // second stream for the QP(l) || pass(l+1) overlap (fixed-iteration mode)
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev_proj = nullptr, ev_qp = nullptr;
+  cudaStream_t aux = nullptr;     // low priority: QP
+  cudaStream_t hi = nullptr;      // high priority: cone pass chain
+  cudaEvent_t ev_proj = nullptr, ev_qp = nullptr, ev_in = nullptr, ev_out = nullptr;
   // persistent staging for host-memory outputs and the active-count poll
   double* stage_ng2 = nullptr;   // [2][B][ng]  margins
   double* stage_b = nullptr;     // [B]         objective

@@ -472,18 +472,22 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
   double* Zo = Zout + ((int64_t)b * d.T + k) * nu * nx;
   if (act && !act[b]) return;
   const int n = ncnt ? ncnt[b] : nfixed;
+  // blockIdx.z splits the list (small batches); partial sums are added atomically
+  const int nsp = gridDim.z, sp = blockIdx.z;
+  const int per = (((n + nsp - 1) / nsp) + 31) & ~31;
+  const int lo = sp * per, hi = min(n, lo + per);
   const int64_t bg = (int64_t)b * d.ng;
   const double* yb = y + (int64_t)b * d.E;
   const double* Bd = v.Bd + (int64_t)b * d.EB;
   double z[NTI][2];
 #pragma unroll
   for (int nt = 0; nt < NTI; ++nt) { z[nt][0] = 0.0; z[nt][1] = 0.0; }
-  for (int base = 0; base < n; base += 32) {
+  for (int base = lo; base < hi; base += 32) {
     // lane l inspects entry base + l
     int j = 0;
     double w = 0.0;
     bool has = false;
-    if (base + lane < n) {
+    if (base + lane < hi) {
       j = clist ? clist[bg + base + lane] : base + lane;
       const int kind = v.kind[j], knot = v.knot[j];
       has = (kind == 0) ? (knot > k) : (knot == k);
@@ -534,7 +538,10 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int i = 2 * q + r + 8 * nt;
-        if (i < nx) Zo[g * nx + i] = z[nt][r];
+        if (i < nx) {
+          if (nsp == 1) Zo[g * nx + i] = z[nt][r];
+          else atomicAdd(&Zo[g * nx + i], z[nt][r]);
+        }
       }
   }
 }
@@ -780,12 +787,30 @@ cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st) {
   return launch_fused_t<2, 2>(h, st);
 }
 
+__global__ void k_zero_active(double* Z, int64_t per, int B, const int32_t* act) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)B * per) return;
+  if (act && !act[id / per]) return;
+  Z[id] = 0.0;
+}
+
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,
                          double* Zout, cudaStream_t st) {
   Dev& v = h->dev;
   if (v.d.nu <= 8 && v.d.nx <= 16) {
-    dim3 grid(v.d.B, (v.d.T + 15) / 16);
+    // split the list when the batch alone cannot fill the GPU (dense lists only)
+    int nsp = 1;
+    if (!ncnt && nfixed > 256) {
+      const int64_t ctas = (int64_t)v.d.B * ((v.d.T + 15) / 16);
+      while (nsp < 64 && ctas * nsp < 296 && (nfixed / (nsp * 2)) >= 64) nsp *= 2;
+    }
+    if (nsp > 1) {           // zero the slices of the instances that will be accumulated
+      const int64_t per = (int64_t)v.d.T * v.d.nu * v.d.nx;
+      k_zero_active<<<(unsigned)(((int64_t)v.d.B * per + 255) / 256), 256, 0, st>>>(Zout, per, v.d.B, act);
+      h->launches++;
+    }
+    dim3 grid(v.d.B, (v.d.T + 15) / 16, nsp);
     if (v.d.nx <= 8)
       k_zlist_mma<1><<<grid, 512, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout);
     else

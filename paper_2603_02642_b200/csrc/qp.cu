@@ -433,7 +433,7 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kQPRing = 4;
+constexpr int kQPRing = 8;
 
 __global__ void __launch_bounds__(256, 5) k_qp_lite(Dev v, int engine, int l) {
   extern __shared__ double sm[];
@@ -470,14 +470,17 @@ __global__ void __launch_bounds__(256, 5) k_qp_lite(Dev v, int engine, int l) {
   double* ring = sS + (T + 1) * nx;                   // [kQPRing][nx nx]
   const int nn = nx * nx;
 
-  for (int it = 0; it < v.prm.qp_iters; ++it) {
-    for (int j = tid; j < ng; j += nt) {
-      const double vj = pt[j] - lam[j] * rinv;
-      const double r = sq * p[j] + rho * vj + rq * zl[j] - yl[j];
-      rp[j] = r;
-      wq[j] = rq * zl[j] - yl[j] - beta * r;
+  const int nits = v.prm.qp_iters;
+  for (int it = 0; it < nits; ++it) {
+    if (it == 0) {           // later iterations get rhs_p / w from the fused row update below
+      for (int j = tid; j < ng; j += nt) {
+        const double vj = pt[j] - lam[j] * rinv;
+        const double r = sq * p[j] + rho * vj + rq * zl[j] - yl[j];
+        rp[j] = r;
+        wq[j] = rq * zl[j] - yl[j] - beta * r;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     for (int r = tid; r < T * nu; r += nt) {
       const int k = r / nu, m = r % nu;
       double acc = sq * du[r];
@@ -607,11 +610,18 @@ __global__ void __launch_bounds__(256, 5) k_qp_lite(Dev v, int engine, int l) {
       }
       const double ptl = (rp[j] - rq * bd) / den;
       const double ztl = bd + ptl;
-      p[j] = aq * ptl + (1.0 - aq) * p[j];
-      const double zh = aq * ztl + (1.0 - aq) * zl[j];
-      const double zn = fmin(zh + yl[j] / rq, -g0[j]);
-      yl[j] += rq * (zh - zn);
-      zl[j] = zn;
+      const double pn = aq * ptl + (1.0 - aq) * p[j];
+      const double zl0 = zl[j], yl0 = yl[j];
+      const double zh = aq * ztl + (1.0 - aq) * zl0;
+      const double zn = fmin(zh + yl0 / rq, -g0[j]);
+      const double yn = yl0 + rq * (zh - zn);
+      p[j] = pn; zl[j] = zn; yl[j] = yn;
+      if (it + 1 < nits) {   // rhs_p and w of the next QP iteration
+        const double vj = pt[j] - lam[j] * rinv;
+        const double r = sq * pn + rho * vj + rq * zn - yn;
+        rp[j] = r;
+        wq[j] = rq * zn - yn - beta * r;
+      }
     }
     for (int r = tid; r < T * nu; r += nt) du[r] = aq * gR[r] + (1.0 - aq) * du[r];
     __syncthreads();
