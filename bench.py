@@ -116,6 +116,16 @@ def cpu_oracle_sample(cfg, L, n_inst=1, seed0=0):
     return n_inst * L / dt, dt
 
 
+def workload_config(args, world, shape, E, E_B):
+    """The `config` of both arms (ours and --impl reference)."""
+    B, L = args.batch_per_gpu, args.iters
+    return {"workload": f"{args.workload}: batch of Franka-shaped SOCP subproblems "
+                        f"(n_x=14, n_u=7, T=100, n_g={shape.n_g}, E={E}), FullADMM, "
+                        f"L={L} fixed iterations, {B} instances/GPU",
+            "global_batch": world * B, "parallelism": f"instances sharded dp{world}",
+            "l2": "inputs larger than L2 (working set ~%.0f GB/GPU)" % (B * 8 * (2 * E + E_B) / 1e9)}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -139,13 +149,18 @@ def run_reference(args, rank, world):
         times.append(dt)
     ms = 1000.0 * float(np.mean(times))
     value = L / (ms / 1000.0)
-    sample = f"1 {cfg} instance x {L} FullADMM iterations (+ setup) per step, 1 host thread"
+    sample = (f"bounded sample: 1 {cfg} instance x {L} FullADMM iterations (+ setup) per step "
+              f"(of the {args.batch_per_gpu} instances/GPU of the workload), 1 host thread")
+    from gen import make_instance
+    shape, _ = make_instance(cfg, 0)
+    E, _, E_B = workload_shape_stats(shape)
+    config = workload_config(args, world, shape, E, E_B)
+    config["sample"] = sample
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen/, seeded PCG64)",
-            "config": {"workload": f"{cfg}: Franka n_x=14 n_u=7 T=100 FullADMM L={L}",
-                       "sample": sample},
+            "config": config,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -266,12 +281,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (gen/, seeded PCG64; no datasets or trained weights)",
-        "config": {"workload": f"{args.workload}: batch of Franka-shaped SOCP subproblems "
-                               f"(n_x=14, n_u=7, T=100, n_g={shape.n_g}, E={E}), FullADMM, "
-                               f"L={L} fixed iterations, {B} instances/GPU",
-                   "global_batch": world * B, "parallelism": f"instances sharded dp{world}",
-                   "l2": "inputs larger than L2 (working set ~%.0f GB/GPU)" % (
-                       B * 8 * (2 * E + E_B) / 1e9)},
+        "config": workload_config(args, world, shape, E, E_B),
         "soc_projections_per_s": value * shape.n_g,
         "cone_elements_per_s": value * E,
         "sl_iteration_wall_clock_ms": (e2e or {}).get("sl_iteration_wall_clock_ms"),
