@@ -436,6 +436,12 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
       st = user_st;
     }
   } else {
+    if (!h->dr_ready) {                  // DR factors on first use after setup/refresh
+      CK(launch_engine_factors(h, NRTO_DR, st));
+      const int se = read_setup_error(st);
+      if (se) return fail(NRTO_ENOTSPD, se == 1 ? "W_K + sigma_dr/2 is not SPD" : "Riccati H_uu is not SPD");
+      h->dr_ready = 1;
+    }
     CK(launch_dr_reset(h, h->dr_fresh, st));
     h->dr_fresh = 0;
     for (int l = 1; l <= prm.max_admm_iter; ++l) {

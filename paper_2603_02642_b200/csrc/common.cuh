@@ -95,6 +95,7 @@ struct nrto_handle_s {
   nrto::Dev dev;
   int64_t launches = 0;
   int dr_fresh = 1;
+  int dr_ready = 0;        // DR engine factors built for the current setup
   void* allocs[96];
   int nallocs = 0;
   cudaStream_t stream = 0;
@@ -173,6 +174,7 @@ cudaError_t launch_soc_project(const double* t, const double* y, const int64_t* 
                                int64_t n, double* to, double* yo, cudaStream_t st);
 cudaError_t launch_count_active(nrto_handle_s* h, int32_t* d_count, int dr, cudaStream_t st);
 int read_setup_error(cudaStream_t st);
+cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st);
 cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,

@@ -183,7 +183,7 @@ __global__ void k_chain(Dev v) {
 
 // S1b: generalized eigen-chain of (Lambda_k, W'_k) per engine, with the
 // Sigma_k eigenpairs of step Urep[k] (identical Psi blocks share them).
-__global__ void k_chain2(Dev v) {
+__global__ void k_chain2(Dev v, int engmask) {
   extern __shared__ double sm[];
   const Dims d = v.d;
   const int nx = d.nx, nu = d.nu;
@@ -207,6 +207,7 @@ __global__ void k_chain2(Dev v) {
   __syncwarp();
   const double tau = v.tau[b];
   for (int eng = 0; eng < 2; ++eng) {
+    if (!((engmask >> eng) & 1)) continue;
     const EngineFactors& F = eng == 0 ? v.fa : v.dr;
     const double shift = eng == 0 ? 0.0 : 0.5 * v.prm.sigma_dr;
     const double coef = eng == 0 ? v.prm.rho : v.prm.r_s;
@@ -279,11 +280,11 @@ __global__ void k_chain2(Dev v) {
 // with Qt_k = rho_q I + c sum_{state j@k} g g^T, Rt_k = 2 R_u + sigma_q I +
 // c sum_{ctrl j@k} h h^T, c = rho_q (rho+sigma_q)/(rho+sigma_q+rho_q).
 // One CTA per (instance, engine).
-__global__ void k_riccati(Dev v) {
+__global__ void k_riccati(Dev v, int eng) {
   extern __shared__ double sm[];
   const Dims d = v.d;
   const int nx = d.nx, nu = d.nu;
-  const int b = blockIdx.x >> 1, eng = blockIdx.x & 1;
+  const int b = blockIdx.x;
   const EngineFactors& F = eng == 0 ? v.fa : v.dr;
   const double rho = eng == 0 ? v.prm.rho : v.prm.rho_admm;
   const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp;
@@ -437,11 +438,25 @@ cudaError_t launch_setup(nrto_handle_s* h, cudaStream_t st) {
   const int64_t nw = (int64_t)d.B * d.T;
   k_chain<<<(unsigned)((nw + wpb - 1) / wpb), 32 * wpb, wpb * per * sizeof(double), st>>>(v);
   h->launches++;
+  h->dr_ready = 0;
+  return launch_engine_factors(h, NRTO_FULLADMM, st);
+}
+
+// Per-engine S1b/S2 factors: FullADMM at setup, DR lazily on its first solve.
+cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  if (engine != NRTO_FULLADMM) {       // fresh error flag for the lazily built DR factors
+    int zero = 0;
+    cudaMemcpyToSymbolAsync(g_setup_err, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st);
+  }
+  const int wpb = 4;
+  const int64_t nw = (int64_t)d.B * d.T;
   k_chain2<<<(unsigned)((nw + wpb - 1) / wpb), 32 * wpb,
-             wpb * (4 * d.nu * d.nu + d.nx + d.nu) * sizeof(double), st>>>(v);
+             wpb * (4 * d.nu * d.nu + d.nx + d.nu) * sizeof(double), st>>>(v, 1 << engine);
   h->launches++;
   const int rs = 3 * d.nx * d.nx + 2 * d.nx * d.nu + 3 * d.nu * d.nu + 2 * d.nu * d.nx;
-  k_riccati<<<2 * d.B, 128, rs * sizeof(double), st>>>(v);
+  k_riccati<<<d.B, 128, rs * sizeof(double), st>>>(v, engine);
   h->launches++;
   return cudaGetLastError();
 }
