@@ -239,6 +239,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   v.tiles = dtiles; v.witems = dwitems;
   AL(v.Zpart, (v.fused ? B * nsplit : 1) * T * nu * nx); AL(v.Zc, B * T * nu * nx);
   AL(v.Zctrl, B * T * nu * nx); AL(v.nrm2, B * ng);
+  AL(v.gnz, B * ng); AL(v.gidx, B * ng * 8); AL(v.gval, B * ng * 8);
   AL(v.clist, B * ng); AL(v.cw, B * ng); AL(v.ncorr, B);
 
   // shape arrays (pageable host vectors: synchronous copies)

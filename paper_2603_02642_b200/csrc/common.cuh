@@ -75,6 +75,9 @@ struct Dev {
   int nctrl;               // number of control cones
   int iter;                // outer iteration l of the launch (set by the host loop)
   double* nrm2;            // [B][ng] ||y^l||^2 written by the fused pass
+  uint8_t* gnz;            // [B][ng] nonzeros of each gradient row (255: dense)
+  int8_t* gidx;            // [B][ng][8] their indices
+  double* gval;            // [B][ng][8] their values
   double* Zctrl;           // [B][T][nu][nx] exact adjoint of the control cones (fused == 2)
   int ntiles, nsplit, nwitems;
   int nstate_tiles;        // state tiles come first in `tiles`
@@ -175,6 +178,7 @@ cudaError_t launch_soc_project(const double* t, const double* y, const int64_t* 
 cudaError_t launch_count_active(nrto_handle_s* h, int32_t* d_count, int dr, cudaStream_t st);
 int read_setup_error(cudaStream_t st);
 cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st);
+cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,

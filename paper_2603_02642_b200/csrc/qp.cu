@@ -676,10 +676,314 @@ __global__ void __launch_bounds__(256, 5) k_qp_lite(Dev v, int engine, int l) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Sparse-row variant of k_qp_lite.  The constraint gradients are kept in a
+// compressed row form built at setup (<= 8 nonzeros per row, else dense), and
+// the row phase of QP iteration m gathers (B du~)_j, updates (p, z, y)_j and
+// immediately scatters the NEXT iteration's w_j grad_j into the knot
+// accumulators S_k / U_k with FP64 RED.ADD -- each row is read once per QP
+// iteration (SURVEY F4 products with B and B^T).
+constexpr int kRowNZ = 8;
+
+__device__ __forceinline__ void scatter_row(const Dev& v, int64_t ij, int kind, int k, double w,
+                                            const double* grad_j, double* gS, double* gU) {
+  const int nx = v.d.nx, nu = v.d.nu;
+  const int nz = v.gnz[ij];
+  double* dst = (kind == 0) ? gS + (int64_t)k * nx : gU + (int64_t)k * nu;
+  if (nz <= kRowNZ) {
+    const int8_t* gi = v.gidx + ij * kRowNZ;
+    const double* gv = v.gval + ij * kRowNZ;
+    for (int s = 0; s < nz; ++s) atomicAdd(dst + gi[s], w * gv[s]);
+  } else {
+    const int n = (kind == 0) ? nx : nu;
+    for (int i = 0; i < n; ++i) atomicAdd(dst + i, w * grad_j[i]);
+  }
+}
+
+__device__ __forceinline__ double gather_row(const Dev& v, int64_t ij, int kind,
+                                             const double* x, const double* grad_j) {
+  const int nx = v.d.nx, nu = v.d.nu;
+  const int nz = v.gnz[ij];
+  double acc = 0.0;
+  if (nz <= kRowNZ) {
+    const int8_t* gi = v.gidx + ij * kRowNZ;
+    const double* gv = v.gval + ij * kRowNZ;
+    for (int s = 0; s < nz; ++s) acc += gv[s] * x[gi[s]];
+  } else {
+    const int n = (kind == 0) ? nx : nu;
+    for (int i = 0; i < n; ++i) acc += grad_j[i] * x[i];
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, T = d.T, ng = d.ng;
+  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  if (!v.active[b]) return;
+  const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
+  const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
+  const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp, aq = v.prm.alpha_qp;
+  const double den = rho + sq + rq, beta = rq / den;
+  const int64_t bg = (int64_t)b * ng;
+  const double* __restrict__ grad = v.grad + bg * nx;
+  const double* __restrict__ g0 = v.g0 + bg;
+  double* p = v.p + bg; double* zl = v.zl + bg; double* yl = v.yl + bg;
+  double* rp = v.rp + bg;
+  const double* pt = v.pt + bg; double* lam = v.lamp + bg;
+  double* zb = v.zb + (int64_t)b * (T + 1) * nx; double* yb = v.yb + (int64_t)b * (T + 1) * nx;
+  double* du = v.du + (int64_t)b * T * nu;
+  double* gA = v.dxt + (int64_t)b * (T + 1) * nx;    // a_k, then e_k
+  double* gK = v.kff + (int64_t)b * T * nu;           // kff_k
+  double* gR = v.ru + (int64_t)b * T * nu;            // r_u,k, then du~_k
+  double* gS = v.rx + (int64_t)b * (T + 1) * nx;      // S_k = sum_{state j@k} w_j grad_j (atomic)
+  double* gU = v.dut + (int64_t)b * T * nu;           // U_k = sum_{ctrl j@k} w_j h'_j   (atomic)
+  const double* __restrict__ Ru = v.Ru + (int64_t)b * T * nu * nu;
+  const double* __restrict__ uh = v.uhat + (int64_t)b * T * nu;
+  const double* __restrict__ Bm = v.Bm + (int64_t)b * T * nx * nu;
+  const double* __restrict__ Kf = F.Kf + (int64_t)b * T * nu * nx;
+  const double* __restrict__ AclG = F.Acl + (int64_t)b * T * nx * nx;
+  const double* __restrict__ Hi = F.Hinv + (int64_t)b * T * nu * nu;
+  const double* __restrict__ HB = F.HB + (int64_t)b * T * nu * nx;
+  const double rtr = v.rtrust[b];
+  const double rinv = (engine == NRTO_FULLADMM) ? 1.0 : 1.0 / rho;
+  double* sS = sm;                                    // [(T+1) nx]
+  double* ring = sS + (T + 1) * nx;                   // [kQPRing][nx nx]
+  const int nn = nx * nx;
+  const int nits = v.prm.qp_iters;
+
+  for (int r = tid; r < (T + 1) * nx; r += nt) gS[r] = 0.0;
+  for (int r = tid; r < T * nu; r += nt) gU[r] = 0.0;
+  __syncthreads();
+  if (nits > 0) {                                     // rhs / w / scatter of iteration 0
+    for (int j = tid; j < ng; j += nt) {
+      const double vj = pt[j] - lam[j] * rinv;
+      const double r = sq * p[j] + rho * vj + rq * zl[j] - yl[j];
+      rp[j] = r;
+      const double w = rq * zl[j] - yl[j] - beta * r;
+      scatter_row(v, bg + j, v.kind[j], v.knot[j], w, grad + (int64_t)j * nx, gS, gU);
+    }
+    __syncthreads();
+  }
+  for (int it = 0; it < nits; ++it) {
+    for (int r = tid; r < T * nu; r += nt) {          // r_u (consumes and clears U)
+      const int k = r / nu, m = r % nu;
+      double acc = sq * du[r] + gU[r];
+      gU[r] = 0.0;
+      for (int q = 0; q < nu; ++q) acc -= 2.0 * Ru[(k * nu + m) * nu + q] * uh[k * nu + q];
+      gR[r] = acc;
+    }
+    __syncthreads();
+    for (int r = tid; r < (T + 1) * nx; r += nt) {    // r_x and a_k (consumes and clears S)
+      const int k = r / nx, i = r % nx;
+      double acc = (k > 0) ? gS[r] + rq * zb[r] - yb[r] : 0.0;
+      gS[r] = 0.0;
+      if (k < T) {
+        const double* Kk = Kf + (int64_t)k * nu * nx;
+        for (int m = 0; m < nu; ++m) acc -= Kk[m * nx + i] * gR[k * nu + m];
+        gA[r] = acc;
+      } else {
+        sS[r] = acc;
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {                                   // backward recurrence, Acl ring
+      for (int pf = 0; pf < kQPRing; ++pf) {
+        const int k = T - 1 - pf;
+        if (k >= 0) for (int e = tid; e < nn; e += 32) cpa8(ring + pf * nn + e, AclG + (int64_t)k * nn + e);
+        cpa_commit();
+      }
+      double s = (tid < nx) ? sS[T * nx + tid] : 0.0;
+      const int ic = tid < nx ? tid : 0;
+      for (int k = T - 1, slot = 0; k >= 0; --k, slot = (slot + 1) % kQPRing) {
+        cpa_wait<kQPRing - 1>();
+        __syncwarp();
+        const double* Ak = ring + slot * nn + ic;
+        double a0 = gA[k * nx + ic], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int r = 0;
+        for (; r + 4 <= nx; r += 4) {
+          a0 += Ak[(r + 0) * nx] * __shfl_sync(0xffffffffu, s, r + 0);
+          a1 += Ak[(r + 1) * nx] * __shfl_sync(0xffffffffu, s, r + 1);
+          a2 += Ak[(r + 2) * nx] * __shfl_sync(0xffffffffu, s, r + 2);
+          a3 += Ak[(r + 3) * nx] * __shfl_sync(0xffffffffu, s, r + 3);
+        }
+        for (; r < nx; ++r) a0 += Ak[r * nx] * __shfl_sync(0xffffffffu, s, r);
+        s = (a0 + a1) + (a2 + a3);
+        if (tid < nx) sS[k * nx + tid] = s;
+        __syncwarp();
+        const int kn = k - kQPRing;
+        if (kn >= 0) for (int e = tid; e < nn; e += 32) cpa8(ring + slot * nn + e, AclG + (int64_t)kn * nn + e);
+        cpa_commit();
+      }
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nu; r += nt) {          // kff_k
+      const int k = r / nu, m = r % nu;
+      const double* H = Hi + (int64_t)k * nu * nu;
+      const double* hb = HB + (int64_t)k * nu * nx;
+      double acc = 0.0;
+      for (int q = 0; q < nu; ++q) acc += H[m * nu + q] * gR[k * nu + q];
+      for (int i = 0; i < nx; ++i) acc += hb[m * nx + i] * sS[(k + 1) * nx + i];
+      gK[r] = acc;
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nx; r += nt) {          // e_k = B_k kff_k
+      const int k = r / nx, i = r % nx;
+      const double* Bk = Bm + (int64_t)k * nx * nu;
+      double acc = 0.0;
+      for (int m = 0; m < nu; ++m) acc += Bk[i * nu + m] * gK[k * nu + m];
+      gA[r] = acc;
+    }
+    __syncthreads();
+    if (tid < 32) {                                   // forward recurrence, Acl ring
+      for (int pf = 0; pf < kQPRing; ++pf) {
+        if (pf < T) for (int e = tid; e < nn; e += 32) cpa8(ring + pf * nn + e, AclG + (int64_t)pf * nn + e);
+        cpa_commit();
+      }
+      double x = 0.0;
+      const int ic = tid < nx ? tid : 0;
+      if (tid < nx) sS[tid] = 0.0;
+      for (int k = 0, slot = 0; k < T; ++k, slot = (slot + 1) % kQPRing) {
+        cpa_wait<kQPRing - 1>();
+        __syncwarp();
+        const double* Ak = ring + slot * nn + ic * nx;
+        double a0 = gA[k * nx + ic], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int r = 0;
+        for (; r + 4 <= nx; r += 4) {
+          a0 += Ak[r + 0] * __shfl_sync(0xffffffffu, x, r + 0);
+          a1 += Ak[r + 1] * __shfl_sync(0xffffffffu, x, r + 1);
+          a2 += Ak[r + 2] * __shfl_sync(0xffffffffu, x, r + 2);
+          a3 += Ak[r + 3] * __shfl_sync(0xffffffffu, x, r + 3);
+        }
+        for (; r < nx; ++r) a0 += Ak[r] * __shfl_sync(0xffffffffu, x, r);
+        x = (a0 + a1) + (a2 + a3);
+        if (tid < nx) sS[(k + 1) * nx + tid] = x;
+        __syncwarp();
+        const int kn = k + kQPRing;
+        if (kn < T) for (int e = tid; e < nn; e += 32) cpa8(ring + slot * nn + e, AclG + (int64_t)kn * nn + e);
+        cpa_commit();
+      }
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nu; r += nt) {          // du~_k
+      const int k = r / nu, m = r % nu;
+      const double* Kk = Kf + (int64_t)k * nu * nx;
+      double acc = gK[r];
+      for (int q = 0; q < nx; ++q) acc -= Kk[m * nx + q] * sS[k * nx + q];
+      gR[r] = acc;
+    }
+    __syncthreads();
+    const bool more = it + 1 < nits;
+    for (int j = tid; j < ng; j += nt) {              // rows: gather, update, next rhs, scatter
+      const int k = v.knot[j], kind = v.kind[j];
+      const double* gj = grad + (int64_t)j * nx;
+      const double bd = gather_row(v, bg + j, kind, (kind == 0) ? sS + (int64_t)k * nx : gR + (int64_t)k * nu, gj);
+      const double ptl = (rp[j] - rq * bd) / den;
+      const double pn = aq * ptl + (1.0 - aq) * p[j];
+      const double zl0 = zl[j], yl0 = yl[j];
+      const double zh = aq * (bd + ptl) + (1.0 - aq) * zl0;
+      const double zn = fmin(zh + yl0 / rq, -g0[j]);
+      const double yn = yl0 + rq * (zh - zn);
+      p[j] = pn; zl[j] = zn; yl[j] = yn;
+      if (more) {
+        const double vj = pt[j] - lam[j] * rinv;
+        const double r = sq * pn + rho * vj + rq * zn - yn;
+        rp[j] = r;
+        scatter_row(v, bg + j, kind, k, rq * zn - yn - beta * r, gj, gS, gU);
+      }
+    }
+    for (int r = tid; r < T * nu; r += nt) du[r] = aq * gR[r] + (1.0 - aq) * du[r];
+    __syncthreads();
+    double nb = 0.0;                                  // trust-region ball
+    for (int r = tid; r < (T + 1) * nx; r += nt) {
+      const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
+      sS[r] = zh;
+      const double w = zh + yb[r] / rq;
+      nb += w * w;
+    }
+    nb = sqrt(block_sum(nb, red));
+    const double scl = (nb > rtr) ? rtr / nb : 1.0;
+    for (int r = tid; r < (T + 1) * nx; r += nt) {
+      const double zh = sS[r];
+      const double zn = scl * (zh + yb[r] / rq);
+      yb[r] += rq * (zh - zn);
+      zb[r] = zn;
+    }
+    __syncthreads();
+  }
+  double ap = 0.0, ad = 0.0;
+  double* tin = v.tin + bg;
+  double* ptp = v.ptprev + bg;
+  for (int j = tid; j < ng; j += nt) {
+    const double dp = p[j] - pt[j];
+    if (engine == NRTO_FULLADMM) {
+      lam[j] += dp;
+      tin[j] = p[j] + lam[j];
+    } else {
+      lam[j] += rho * dp;
+    }
+    ap += dp * dp;
+    const double dd = pt[j] - ptp[j];
+    ad += dd * dd;
+    ptp[j] = pt[j];
+  }
+  ap = block_sum(ap, red);
+  ad = block_sum(ad, red);
+  if (tid == 0) {
+    const double rpv = sqrt(ap), rdv = rho * sqrt(ad);
+    v.r_p[b] = rpv;
+    v.r_d[b] = rdv;
+    v.iters[b] = l;
+    if (!isfinite(rpv) || !isfinite(rdv)) {
+      v.status[b] = NRTO_DIVERGED;
+      v.active[b] = 0;
+    } else if (!v.prm.fixed_iters && (l % v.prm.check_every) == 0 && rpv <= v.prm.eps_p &&
+               rdv <= v.prm.eps_d) {
+      v.status[b] = NRTO_CONVERGED;
+      v.active[b] = 0;
+    }
+  }
+}
+
+// Setup: compressed rows of the constraint gradients (state rows: n_x entries,
+// control rows: the first n_u); nnz > kRowNZ keeps the dense row (gnz = 255).
+__global__ void k_sparse_rows(Dev v) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)v.d.B * v.d.ng) return;
+  const int j = (int)(id % v.d.ng);
+  const int n = (v.kind[j] == 0) ? v.d.nx : v.d.nu;
+  const double* g = v.grad + id * v.d.nx;
+  int nz = 0;
+  for (int i = 0; i < n; ++i) nz += (g[i] != 0.0);
+  if (nz > kRowNZ) { v.gnz[id] = (uint8_t)255; return; }
+  int s = 0;
+  for (int i = 0; i < n; ++i)
+    if (g[i] != 0.0) { v.gidx[id * kRowNZ + s] = (int8_t)i; v.gval[id * kRowNZ + s] = g[i]; ++s; }
+  v.gnz[id] = (uint8_t)nz;
+}
+
+cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
+  const int64_t n = (int64_t)h->dev.d.B * h->dev.d.ng;
+  if (n > 0) {
+    k_sparse_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->dev);
+    h->launches++;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st) {
   const Dims& d = h->dev.d;
   const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx) * sizeof(double);
   if (smem > 48 * 1024) return launch_qp(h, engine, l, st);
+  if (d.nx <= 127) {
+    k_qp_sparse<<<d.B, 256, smem, st>>>(h->dev, engine, l);
+    h->launches++;
+    return cudaGetLastError();
+  }
   k_qp_lite<<<d.B, 256, smem, st>>>(h->dev, engine, l);
   h->launches++;
   return cudaGetLastError();

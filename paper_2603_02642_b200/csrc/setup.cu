@@ -439,6 +439,8 @@ cudaError_t launch_setup(nrto_handle_s* h, cudaStream_t st) {
   k_chain<<<(unsigned)((nw + wpb - 1) / wpb), 32 * wpb, wpb * per * sizeof(double), st>>>(v);
   h->launches++;
   h->dr_ready = 0;
+  cudaError_t e = launch_sparse_rows(h, st);
+  if (e != cudaSuccess) return e;
   return launch_engine_factors(h, NRTO_FULLADMM, st);
 }
 

@@ -7,7 +7,7 @@ from gen import make_batch
 B = 512
 shape, batch = make_batch("c5", B)
 dd = nrto.to_tensors(batch, device="cuda")
-for qpi in (10, 0):
+for qpi in (10, 5, 2):
     s = nrto.InnerSolver(shape, dd, max_iter=50, fixed_iters=1, qp_iters=qpi)
     od = nrto.alloc_out(shape, B, s.E, device="cuda", full=False)
     s.solve(nrto.NRTO_FULLADMM, out=od); torch.cuda.synchronize()
