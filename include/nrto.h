@@ -205,6 +205,12 @@ typedef enum {
 nrto_err nrto_profile_enable(nrto_handle h, int32_t enable);
 nrto_err nrto_profile_read(nrto_handle h, int32_t kclass, double* total_ms, int64_t* launches);
 
+/* Algorithmic bytes moved by the fused state-cone pass (k_fa_tma) since the
+ * last call, then reset: b_hat and b of every cone block, y^{l-1} read for
+ * cones with s^{l-1} != 1 and y^l written where it is needed later (DESIGN §7,
+ * lazy y).  0 when the TMA pass is not in use.  Synchronises the device. */
+nrto_err nrto_pass_bytes(nrto_handle h, int64_t* bytes);
+
 nrto_err nrto_destroy(nrto_handle h);
 
 /* Thread-local message for the last non-OK return (never NULL). */

@@ -237,9 +237,16 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   int32_t *dtiles, *dwitems;
   AL(dtiles, tiles.size()); AL(dwitems, witems.size());
   v.tiles = dtiles; v.witems = dwitems;
-  AL(v.Zpart, (v.fused ? B * nsplit : 1) * T * nu * nx); AL(v.Zc, B * T * nu * nx);
+  AL(v.Zpart, (v.fused == 1 ? B * nsplit : 1) * T * nu * nx); AL(v.Zc, B * T * nu * nx);
+  if (v.fused == 2) {
+    AL(v.G, B * T * nu * nu); AL(v.G0, B * T * nu * nu); AL(v.dG, B * T * nu * nu);
+    AL(v.H, B * T * nu * nx); AL(v.H0, B * T * nu * nx); AL(v.dH, B * T * nu * nx);
+  }
   AL(v.Zctrl, B * T * nu * nx); AL(v.nrm2, B * ng);
   AL(v.gnz, B * ng); AL(v.gidx, B * ng * 8); AL(v.gval, B * ng * 8);
+  AL(v.pass_bytes, 1);
+  cudaMemset(v.pass_bytes, 0, sizeof(unsigned long long));
+  v.ylazy = 0;
   AL(v.clist, B * ng); AL(v.cw, B * ng); AL(v.ncorr, B);
 
   // shape arrays (pageable host vectors: synchronous copies)
@@ -402,6 +409,8 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     };
     for (int l = 1; l <= prm.max_iter; ++l) {
       v.iter = l;
+      // lazy y storage needs a known last iteration (it stores every y^L)
+      v.ylazy = (v.fused == 2 && prm.fixed_iters && l < prm.max_iter) ? 1 : 0;
       if (v.fused == 0) {
         CK(timed(NRTO_K_PASS, launch_fa_pass));
         CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
@@ -420,7 +429,8 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
         }
         CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
           Dev& w = hh->dev;
-          return launch_zlist(hh, w.Y, w.clist, w.cw, nullptr, w.ncorr, 0, w.active, w.Zc, s2); }));
+          return launch_zlist(hh, w.Y, w.clist, w.cw, nullptr, w.ncorr, 0, w.active, w.Zc, s2, w.ylazy,
+                              w.fused == 2 ? 1 : 0, w.dG, w.dH); }));
         CK(timed(NRTO_K_GAIN, launch_fa_gain));
         if (!overlap) CK(timed_qp(NRTO_FULLADMM, l));
       }
@@ -430,6 +440,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
         if (c == 0) break;
       }
     }
+    v.ylazy = 0;
     if (overlap) {
       CK(cudaStreamWaitEvent(st, h->ev_qp, 0));
       CK(cudaEventRecord(h->ev_out, st));
@@ -555,5 +566,17 @@ extern "C" nrto_err nrto_profile_read(nrto_handle h, int32_t cls, double* total_
   h->recs.swap(keep);
   if (total_ms) *total_ms = tot;
   if (launches) *launches = n;
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_pass_bytes(nrto_handle h, int64_t* bytes) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (!bytes) return fail(NRTO_EINVAL, "bytes is NULL");
+  unsigned long long v = 0;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(&v, h->dev.pass_bytes, sizeof(v), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(h->dev.pass_bytes, 0, sizeof(v));
+  if (e != cudaSuccess) return cuda_fail(e, "nrto_pass_bytes");
+  *bytes = (int64_t)v;
   return NRTO_OK;
 }

@@ -74,7 +74,17 @@ struct Dev {
                            // correction; 2: k_fa_tma (state tiles) + k_fa_ctrl + correction
   int nctrl;               // number of control cones
   int iter;                // outer iteration l of the launch (set by the host loop)
+  int ylazy;               // 1: lazy y storage in this iteration
+  unsigned long long* pass_bytes;  // algorithmic bytes moved by k_fa_tma (device counter)
   double* nrm2;            // [B][ng] ||y^l||^2 written by the fused pass
+  // TMA path predicted adjoint: Z_pred,k = c_l (G_k D_k^T + H_k) with
+  // G_k = sum b b^T, H_k = sum b b_hat^T over state cones with s^{l-1} = 1.
+  double* G;               // [B][T][nu][nu]
+  double* H;               // [B][T][nu][nx]
+  double* G0;              // [B][T][nu][nu] all state cones (setup)
+  double* H0;              // [B][T][nu][nx]
+  double* dG;              // [B][T][nu][nu] this iteration's leave/enter update
+  double* dH;              // [B][T][nu][nx]
   uint8_t* gnz;            // [B][ng] nonzeros of each gradient row (255: dense)
   int8_t* gidx;            // [B][ng][8] their indices
   double* gval;            // [B][ng][8] their values
@@ -99,7 +109,7 @@ struct nrto_handle_s {
   int64_t launches = 0;
   int dr_fresh = 1;
   int dr_ready = 0;        // DR engine factors built for the current setup
-  void* allocs[96];
+  void* allocs[128];
   int nallocs = 0;
   cudaStream_t stream = 0;
   // optional CUDA-event profiler (nrto_profile_enable)
@@ -148,6 +158,12 @@ __device__ __forceinline__ double soc_case(double t, double a, double* s) {
   return h;
 }
 
+// Correction-list entries: cone index | kRecompute (lazy y: rebuild y^l).
+constexpr int kListMask = (1 << 28) - 1;
+constexpr int kRecompute = 1 << 30;   // y^l not stored by the pass: rebuild it
+constexpr int kLeave = 1 << 29;       // state cone leaves {s = 1}: G -= b b^T, H -= b b_hat^T
+constexpr int kEnter = 1 << 28;       // state cone enters {s = 1}: G += b b^T, H += b b_hat^T
+
 // Predicted projection scale shat of the fused pass (fused.cu, tma.cu).
 // l = 1 (cold start, t = p^0 + lam_p^0 = 0): a state cone with a > 0 is in
 // case 3 with s = (0 + a)/(2a) = 1/2 exactly, so shat = 1/2.  l > 1: shat =
@@ -182,7 +198,8 @@ cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,
-                         double* Zout, cudaStream_t st);
+                         double* Zout, cudaStream_t st, int lazy = 0, int ghmode = 0,
+                         double* dG = nullptr, double* dH = nullptr);
 bool fused_supported(const Dims& d);
 bool tma_supported(const Dims& d);
 cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st);

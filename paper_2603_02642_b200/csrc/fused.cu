@@ -461,7 +461,8 @@ __global__ void __launch_bounds__(512)
 k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ clist,
             const double* __restrict__ cw, const double* __restrict__ scale,
             const int32_t* __restrict__ ncnt, int nfixed, const int32_t* __restrict__ act,
-            double* __restrict__ Zout) {
+            double* __restrict__ Zout, int lazy, int ghmode, double* __restrict__ dG,
+            double* __restrict__ dH) {
   const Dims d = v.d;
   const int nx = d.nx, nu = d.nu, nup = d.nup;
   const int b = blockIdx.x;
@@ -469,43 +470,68 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
   const int g = lane >> 2, q = lane & 3;
   const int k = blockIdx.y * 16 + warp;
   if (k >= d.T) return;
-  double* Zo = Zout + ((int64_t)b * d.T + k) * nu * nx;
   if (act && !act[b]) return;
+  // lazy y: entries flagged kRecompute were not stored by the pass
+  // (s^{l-1} = 1 predicted s^l = 1); their block y_{c,k} = D_k b_{c,k} + b_hat_{c,k}
+  // is rebuilt here from D_k (rows i = g + 8 nt in registers) and stored.
+  double dk[NTI][8];
+  if (lazy) {
+    const double* Dk = v.D + ((int64_t)b * d.T + k) * nx * nu;
+#pragma unroll
+    for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int i = g + 8 * nt;
+        dk[nt][m] = (i < nx && m < nu) ? Dk[i * nu + m] : 0.0;
+      }
+  }
   const int n = ncnt ? ncnt[b] : nfixed;
   // blockIdx.z splits the list (small batches); partial sums are added atomically
   const int nsp = gridDim.z, sp = blockIdx.z;
   const int per = (((n + nsp - 1) / nsp) + 31) & ~31;
   const int lo = sp * per, hi = min(n, lo + per);
   const int64_t bg = (int64_t)b * d.ng;
-  const double* yb = y + (int64_t)b * d.E;
+  const double* yb = y ? y + (int64_t)b * d.E : nullptr;
   const double* Bd = v.Bd + (int64_t)b * d.EB;
-  double z[NTI][2];
+  const double* bhb = v.bhat + (int64_t)b * d.E;
+  // Z_k += sum_c w_c b_c y_c^T ; with ghmode also (sign s_c = +1 enter, -1 leave)
+  // dG_k += sum_c s_c b_c b_c^T and dH_k += sum_c s_c b_c b_hat_c^T (state cones).
+  double z[NTI][2], hz[NTI][2], gz[2] = {0.0, 0.0};
 #pragma unroll
-  for (int nt = 0; nt < NTI; ++nt) { z[nt][0] = 0.0; z[nt][1] = 0.0; }
+  for (int nt = 0; nt < NTI; ++nt) { z[nt][0] = z[nt][1] = 0.0; hz[nt][0] = hz[nt][1] = 0.0; }
   for (int base = lo; base < hi; base += 32) {
     // lane l inspects entry base + l
-    int j = 0;
+    int j = 0, rec = 0, sgn = 0;
     double w = 0.0;
-    bool has = false;
+    bool has = false, hasg = false;
     if (base + lane < hi) {
-      j = clist ? clist[bg + base + lane] : base + lane;
+      const int raw = clist ? clist[bg + base + lane] : base + lane;
+      rec = (raw >> 30) & 1;
+      sgn = ((raw >> 28) & 1) - ((raw >> 29) & 1);
+      j = raw & kListMask;
       const int kind = v.kind[j], knot = v.knot[j];
-      has = (kind == 0) ? (knot > k) : (knot == k);
-      w = cw ? cw[bg + base + lane] : (scale ? scale[bg + j] : 1.0);
-      has = has && (w != 0.0);
+      const bool blk = (kind == 0) ? (knot > k) : (knot == k);
+      if (Zout) {
+        w = cw ? cw[bg + base + lane] : (scale ? scale[bg + j] : 1.0);
+        has = blk && (w != 0.0);
+      }
+      if (ghmode == 2) sgn = 1;
+      hasg = ghmode && kind == 0 && blk && sgn != 0;
+      if (!has) w = 0.0;
+      if (!hasg) sgn = 0;
     }
-    const unsigned mask = __ballot_sync(0xffffffffu, has);
+    const unsigned mask = __ballot_sync(0xffffffffu, has || hasg);
     const int nv = __popc(mask);
     // per-lane row pointers of valid entries (computed by their owner lanes)
     int64_t yoff = 0, boff = 0;
-    if (has) {
+    if (has || hasg) {
       const int kb = (v.kind[j] == 0) ? k : 0;
       yoff = v.off[j] + (int64_t)kb * nx;
       boff = v.offB[j] + (int64_t)kb * nup;
     }
     for (int g8 = 0; g8 < nv; g8 += 8) {
       // the (g8 + c)-th set bit of mask is cone c of this group
-      double a2[2], bv[2][NTI];
+      double a2[2], ag[2], bb[2], bv[2][NTI], bh[2][NTI];
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
         const int c = g8 + q + 4 * ks;                       // A2 / B2 column index
@@ -518,31 +544,90 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
         const int64_t yo = __shfl_sync(0xffffffffu, yoff, src);
         const int64_t bo = __shfl_sync(0xffffffffu, boff, src);
         const double ww = __shfl_sync(0xffffffffu, w, src);
+        const int rc = __shfl_sync(0xffffffffu, rec, src);
+        const int sg = __shfl_sync(0xffffffffu, sgn, src);
         const bool cv = c < nv;
-        a2[ks] = (cv && g < nu) ? ww * Bd[bo + g] : 0.0;
+        // b_{c,g}: A operand row m = g; also the G B-operand (row c, col m' = g)
+        const double bcg = (cv && g < nu) ? Bd[bo + g] : 0.0;
+        a2[ks] = ww * bcg;
+        ag[ks] = (double)sg * bcg;
+        bb[ks] = bcg;
+        const bool rb = lazy && cv && rc;
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
           const int i = g + 8 * nt;
-          bv[ks][nt] = (cv && i < nx) ? yb[yo + i] : 0.0;
+          bh[ks][nt] = (cv && (sg != 0 || rb) && i < nx) ? bhb[yo + i] : 0.0;
         }
+        if (rb) {
+          double bm[8];
+#pragma unroll
+          for (int m = 0; m < 8; ++m) bm[m] = (m < nu) ? Bd[bo + m] : 0.0;
+          double* yw = v.Y + (int64_t)b * d.E + yo;
+#pragma unroll
+          for (int nt = 0; nt < NTI; ++nt) {
+            const int i = g + 8 * nt;
+            double acc = 0.0;
+            if (i < nx) {
+#pragma unroll
+              for (int m = 0; m < 8; ++m) acc += dk[nt][m] * bm[m];
+              acc += bh[ks][nt];
+              yw[i] = acc;
+            }
+            bv[ks][nt] = acc;
+          }
+        } else {
+#pragma unroll
+          for (int nt = 0; nt < NTI; ++nt) {
+            const int i = g + 8 * nt;
+            bv[ks][nt] = (cv && ww != 0.0 && i < nx) ? yb[yo + i] : 0.0;
+          }
+        }
+      }
+      if (Zout) {
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) dmma(z[nt], a2[ks], bv[ks][nt]);
+      }
+      if (ghmode) {
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          dmma(gz, ag[ks], bb[ks]);
+#pragma unroll
+          for (int nt = 0; nt < NTI; ++nt) dmma(hz[nt], ag[ks], bh[ks][nt]);
+        }
+      }
+    }
+  }
+  if (g < nu) {
+    const int64_t bk = (int64_t)b * d.T + k;
+    if (Zout) {
+      double* Zo = Zout + bk * nu * nx;
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int i = 2 * q + r + 8 * nt;
+          if (i < nx) {
+            if (nsp == 1) Zo[g * nx + i] = z[nt][r];
+            else atomicAdd(&Zo[g * nx + i], z[nt][r]);
+          }
+        }
+    }
+    if (ghmode) {                       // launched unsplit (nsp == 1)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int m2 = 2 * q + r;
+        if (m2 < nu) dG[bk * nu * nu + g * nu + m2] = gz[r];
       }
 #pragma unroll
       for (int nt = 0; nt < NTI; ++nt)
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) dmma(z[nt], a2[ks], bv[ks][nt]);
-    }
-  }
-  if (g < nu) {
-#pragma unroll
-    for (int nt = 0; nt < NTI; ++nt)
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int i = 2 * q + r + 8 * nt;
-        if (i < nx) {
-          if (nsp == 1) Zo[g * nx + i] = z[nt][r];
-          else atomicAdd(&Zo[g * nx + i], z[nt][r]);
+        for (int r = 0; r < 2; ++r) {
+          const int i = 2 * q + r + 8 * nt;
+          if (i < nx) dH[bk * nu * nx + g * nx + i] = hz[nt][r];
         }
-      }
+    }
   }
 }
 
@@ -729,7 +814,11 @@ cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st) {
   k_lam_mma<<<grid, 512, 0, st>>>(v);
   h->launches++;
   // Zb_k = sum_j b_{j,k} b_hat_{j,k}^T : the list adjoint with y = b_hat
-  return launch_zlist(h, v.bhat, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, v.Zb, st);
+  cudaError_t e = launch_zlist(h, v.bhat, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, v.Zb, st);
+  if (e != cudaSuccess || v.fused != 2) return e;
+  // G0_k = sum_{state j} b b^T, H0_k = sum_{state j} b b_hat^T (TMA path predicted adjoint)
+  return launch_zlist(h, nullptr, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, nullptr, st,
+                      0, 2, v.G0, v.H0);
 }
 
 static int fused_variant(const Dims& d, int* nti, int* nks) {
@@ -796,12 +885,13 @@ __global__ void k_zero_active(double* Z, int64_t per, int B, const int32_t* act)
 
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,
-                         double* Zout, cudaStream_t st) {
+                         double* Zout, cudaStream_t st, int lazy, int ghmode, double* dG,
+                         double* dH) {
   Dev& v = h->dev;
   if (v.d.nu <= 8 && v.d.nx <= 16) {
     // split the list when the batch alone cannot fill the GPU (dense lists only)
     int nsp = 1;
-    if (!ncnt && nfixed > 256) {
+    if (!ncnt && nfixed > 256 && !ghmode) {
       const int64_t ctas = (int64_t)v.d.B * ((v.d.T + 15) / 16);
       while (nsp < 64 && ctas * nsp < 296 && (nfixed / (nsp * 2)) >= 64) nsp *= 2;
     }
@@ -812,12 +902,13 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
     }
     dim3 grid(v.d.B, (v.d.T + 15) / 16, nsp);
     if (v.d.nx <= 8)
-      k_zlist_mma<1><<<grid, 512, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout);
+      k_zlist_mma<1><<<grid, 512, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
     else
-      k_zlist_mma<2><<<grid, 512, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout);
+      k_zlist_mma<2><<<grid, 512, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
     h->launches++;
     return cudaGetLastError();
   }
+  if (ghmode || lazy) return cudaErrorInvalidValue;   // TMA path only (n_x <= 16, n_u <= 8)
   k_zlist<<<v.d.B * v.d.T, 128, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout);
   h->launches++;
   return cudaGetLastError();

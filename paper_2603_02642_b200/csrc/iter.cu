@@ -243,14 +243,32 @@ __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
   const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + k) * nx * nx;
   const double* Wk = v.W + bk * nu * nu;
   double* Kb = v.K + (int64_t)b * d.NK + (int64_t)k * nu * nx;
-  for (int r = lane; r < nu * nx; r += 32) {
-    double z = v.Zc[bk * nu * nx + r];
-    if (v.fused == 2) z += v.Zctrl[bk * nu * nx + r];
-    const double* zp = v.Zpart + ((int64_t)b * v.nsplit * d.T + k) * nu * nx + r;
-    for (int sp = 0; sp < v.nsplit; ++sp) z += zp[(int64_t)sp * d.T * nu * nx];
-    sX[r] = z - v.Zb[bk * nu * nx + r];
-    const int m = r / nx, i = r % nx;
-    sK[r] = Kb[i * nu + m];
+  if (v.fused == 2) {
+    // TMA path: Z_k = c_l (G_k D_k^T + H_k) [predicted, cones with s^{l-1} = 1;
+    // c_1 = 1/2] + Zc [list corrections] + Zctrl [control cones]; then the
+    // leave/enter updates of this iteration give G, H of the next one.
+    const double cl = (v.iter == 1) ? 0.5 : 1.0;
+    const double* Gk = v.G + bk * nu * nu;
+    const double* Dk = v.D + bk * nx * nu;
+    for (int r = lane; r < nu * nx; r += 32) {
+      const int m = r / nx, i = r % nx;
+      double pr = v.H[bk * nu * nx + r];
+      for (int q = 0; q < nu; ++q) pr += Gk[m * nu + q] * Dk[i * nu + q];
+      sX[r] = cl * pr + v.Zc[bk * nu * nx + r] + v.Zctrl[bk * nu * nx + r] - v.Zb[bk * nu * nx + r];
+      sK[r] = Kb[i * nu + m];
+    }
+    __syncwarp();
+    for (int r = lane; r < nu * nx; r += 32) v.H[bk * nu * nx + r] += v.dH[bk * nu * nx + r];
+    for (int r = lane; r < nu * nu; r += 32) v.G[bk * nu * nu + r] += v.dG[bk * nu * nu + r];
+  } else {
+    for (int r = lane; r < nu * nx; r += 32) {
+      double z = v.Zc[bk * nu * nx + r];
+      const double* zp = v.Zpart + ((int64_t)b * v.nsplit * d.T + k) * nu * nx + r;
+      for (int sp = 0; sp < v.nsplit; ++sp) z += zp[(int64_t)sp * d.T * nu * nx];
+      sX[r] = z - v.Zb[bk * nu * nx + r];
+      const int m = r / nx, i = r % nx;
+      sK[r] = Kb[i * nu + m];
+    }
   }
   if (k == 0 && lane == 0) v.ncorr[b] = 0;      // correction list consumed
   __syncwarp();

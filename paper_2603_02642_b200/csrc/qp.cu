@@ -1043,6 +1043,10 @@ cudaError_t launch_fa_reset(nrto_handle_s* h, cudaStream_t st) {
   zero(h, v.du, B * d.T * d.nu, st); zero(h, v.zl, B * d.ng, st); zero(h, v.yl, B * d.ng, st);
   zero(h, v.zb, B * (d.T + 1) * d.nx, st); zero(h, v.yb, B * (d.T + 1) * d.nx, st);
   cudaMemsetAsync(v.ncorr, 0, B * sizeof(int32_t), st);
+  if (v.fused == 2) {
+    cudaMemcpyAsync(v.G, v.G0, B * d.T * d.nu * d.nu * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(v.H, v.H0, B * d.T * d.nu * d.nx * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  }
   k_reset_inst<<<(d.B + 127) / 128, 128, 0, st>>>(v, NRTO_FULLADMM);
   h->launches++;
   h->dr_fresh = 1;   // Y / Z now hold FullADMM state

@@ -118,29 +118,43 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
     // ---------------------------------------------------------------- producer
     // lane c < nc owns cone c of the tile: its offsets are loaded once per tile
     // and it issues that cone's bulk copies; lane 0 arms the stage barrier.
+    // Lazy y: y_old is fetched only for cones with 1 - s^{l-1} != 0 (y^0 = 0).
     int n = 0;
+    unsigned long long moved = 0;
     const uint64_t pol = policy_evict_first();
     int tnext = t0;
     int64_t offn = 0, offBn = 0;
+    bool ynext = false, wnext = false;
+    auto cone_flags = [&](int j, bool& yr, bool& yw) {
+      const double sp = v.s[bg + j];
+      yr = v.iter > 1 && sp != 1.0;
+      yw = !v.ylazy || shat_of(v, sp) != 1.0;
+    };
     if (tnext < t1 && lane < tiles[(int64_t)tnext * kTI + 2]) {
       const int j = tiles[(int64_t)tnext * kTI + 4 + lane];
       offn = v.off[j]; offBn = v.offB[j];
+      cone_flags(j, ynext, wnext);
     }
     for (int t = t0; t < t1; ++t) {
       const int* tl = tiles + (int64_t)t * kTI;
       const int K = tl[1], nc = tl[2];
       const int64_t offc = offn, offBc = offBn;
+      const bool yrd = ynext, ywr = wnext;
       if (t + 1 < t1 && lane < tiles[(int64_t)(t + 1) * kTI + 2]) {   // prefetch next tile
         const int j = tiles[(int64_t)(t + 1) * kTI + 4 + lane];
         offn = v.off[j]; offBn = v.offB[j];
+        cone_flags(j, ynext, wnext);
       }
+      const uint32_t nyr = __popc(__ballot_sync(0xffffffffu, lane < nc && yrd));
+      const uint32_t nyw = __popc(__ballot_sync(0xffffffffu, lane < nc && ywr));
       for (int kc = 0; kc <= K; kc += 16, ++n) {
         const int st = n % kStages;
         const int nb = min(16, K + 1 - kc), nbB = max(0, min(16, K - kc));
         if (lane == 0) {
           mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
-          const uint32_t bytes = (uint32_t)nc * (2u * nb * nx + (uint32_t)nbB * nup) * 8u;
+          const uint32_t bytes = ((nyr + (uint32_t)nc) * nb * nx + (uint32_t)nc * nbB * nup) * 8u;
           mbar_expect_tx(&full[st], bytes);
+          moved += bytes + (unsigned long long)nyw * nb * nx * 8u;
         }
         __syncwarp();
         if (lane < nc) {
@@ -148,21 +162,17 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
           double* sH = sY + 8 * G.SY;
           double* sB = sH + 8 * G.SY;
           const int64_t o = offc + (int64_t)kc * nx;
-          bulk_g2s(sY + lane * G.SY, Y + o, nb * nx * 8, &full[st], pol);
+          if (yrd) bulk_g2s(sY + lane * G.SY, Y + o, nb * nx * 8, &full[st], pol);
           bulk_g2s(sH + lane * G.SY, bhat + o, nb * nx * 8, &full[st], pol);
           if (nbB > 0)
             bulk_g2s(sB + lane * G.SB, Bd + offBc + (int64_t)kc * nup, nbB * nup * 8, &full[st], pol);
         }
       }
     }
+    if (lane == 0 && v.pass_bytes) atomicAdd(v.pass_bytes, moved);
     return;
   }
   // ------------------------------------------------------------------ consumers
-  double z[KK][NTI][2];
-#pragma unroll
-  for (int kk = 0; kk < KK; ++kk)
-#pragma unroll
-    for (int nt = 0; nt < NTI; ++nt) { z[kk][nt][0] = 0.0; z[kk][nt][1] = 0.0; }
   int n = 0;
   for (int t = t0; t < t1; ++t) {
     const int* tl = tiles + (int64_t)t * kTI;
@@ -171,13 +181,9 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
     const bool gv = g < nc;
     const int cg = gv ? tl[4 + g] : 0;
     const int64_t offg = gv ? v.off[cg] : 0;
-    const double omsp = gv ? 1.0 - v.s[bg + cg] : 0.0;
-    double sh2[2];
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int c2 = q + 4 * ks;
-      sh2[ks] = (c2 < nc) ? shat_of(v, v.s[bg + tl[4 + c2]]) : 0.0;
-    }
+    const double sg = gv ? v.s[bg + cg] : 1.0;
+    const double omsp = (gv && v.iter > 1) ? 1.0 - sg : 0.0;   // != 0 <=> y_old was fetched
+    const bool wy = gv && (!v.ylazy || shat_of(v, sg) != 1.0);  // store y^l
     double nrm = 0.0;
 #pragma unroll
     for (int kk = 0; kk < KK; ++kk) {
@@ -191,7 +197,6 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       const double* sB = sH + 8 * G.SY;
       const int k = kc + warp;
       if (k <= K) {
-        const bool hasB = k < K;
         double c[NTI][2];
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
@@ -199,14 +204,18 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
           c[nt][0] = 0.0; c[nt][1] = 0.0;
           if (gv && i0 < nx) {
             const int e = g * G.SY + warp * nx + i0;
-            const double2 yo = *reinterpret_cast<const double2*>(sY + e);
             const double2 bh = *reinterpret_cast<const double2*>(sH + e);
-            c[nt][0] = bh.x + omsp * yo.x;
-            c[nt][1] = bh.y + omsp * yo.y;
+            if (omsp != 0.0) {
+              const double2 yo = *reinterpret_cast<const double2*>(sY + e);
+              c[nt][0] = bh.x + omsp * yo.x;
+              c[nt][1] = bh.y + omsp * yo.y;
+            } else {
+              c[nt][0] = bh.x;
+              c[nt][1] = bh.y;
+            }
           }
         }
-        double a2[2];
-        if (hasB) {
+        if (k < K) {
 #pragma unroll
           for (int ks = 0; ks < NKS; ++ks) {
             const int m = q + 4 * ks;
@@ -218,35 +227,20 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
               dmma2(c[nt], a, bb);
             }
           }
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks)
-            a2[ks] = (g < nu && sh2[ks] != 0.0) ? sh2[ks] * sB[(q + 4 * ks) * G.SB + warp * nup + g] : 0.0;
         }
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
           const int i0 = 2 * q + 8 * nt;
-          if (gv && i0 < nx)
+          if (wy && i0 < nx)
             __stcs(reinterpret_cast<double2*>(Y + offg + (int64_t)k * nx + i0),
                    make_double2(c[nt][0], c[nt][1]));
           nrm += c[nt][0] * c[nt][0] + c[nt][1] * c[nt][1];
-        }
-        if (hasB) {
-#pragma unroll
-          for (int nt = 0; nt < NTI; ++nt) {
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              const int src = (q + 4 * ks) * 4 + (g >> 1);
-              const double v0 = __shfl_sync(0xffffffffu, c[nt][0], src);
-              const double v1 = __shfl_sync(0xffffffffu, c[nt][1], src);
-              dmma2(z[kk][nt], a2[ks], (g & 1) ? v1 : v0);
-            }
-          }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
-    // ---- norm partials -> ring slot; last consumer warp projects the tile's cones
+    // ---- norm partials -> ring slot; last consumer warp publishes the tile's norms
     nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
     nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
     if (lane == 0) {
@@ -274,21 +268,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       }
     }
   }
-  // ---- flush this warp's Z slices: Zpart[b][sidx][k][m][i]
-  double* Zp = v.Zpart + ((int64_t)b * v.nsplit + sidx) * T * nu * nx;
-#pragma unroll
-  for (int kk = 0; kk < KK; ++kk) {
-    const int k = warp + NW * kk;
-    if (k < T && g < nu) {
-#pragma unroll
-      for (int nt = 0; nt < NTI; ++nt)
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int i = 2 * q + r + 8 * nt;
-          if (i < nx) Zp[((int64_t)k * nu + g) * nx + i] = z[kk][nt][r];
-        }
-    }
-  }
+  (void)sidx;
 }
 
 // Control cones (single block at step k): y = D_k h' + (1 - s) y_old, ||y||^2,
@@ -357,10 +337,26 @@ __global__ void k_project(Dev v) {
   const double tp = soc_case(v.tin[id], sqrt(v.nrm2[id]), &s);
   v.s[id] = s;
   v.pt[id] = tp;
-  if (s != shat) {
+  // TMA path: state cones leaving / entering the interior set {s = 1} update
+  // the Gram sums G, H of the predicted adjoint; at l = 1 every
+  // state cone counts as interior before the projection.
+  const bool gh = v.fused == 2 && v.kind[j] == 0;
+  const bool first = v.iter == 1;
+  const bool leave = gh && s != 1.0 && (first || shat == 1.0);
+  const bool enter = gh && !first && shat == 0.0 && s == 1.0;
+  if (s != shat || leave) {
+    // lazy y: a state cone predicted interior (shat = 1) was not stored by the
+    // pass; flag it so the correction rebuilds y^l (blocks k < K there, the
+    // b-free last block y_K = b_hat_K here).
+    const bool rec = v.ylazy && leave && !first;
     const int pos = atomicAdd(&v.ncorr[b], 1);
-    v.clist[(int64_t)b * v.d.ng + pos] = j;
+    v.clist[(int64_t)b * v.d.ng + pos] = j | (rec ? kRecompute : 0) | (leave ? kLeave : 0) |
+                                         (enter ? kEnter : 0);
     v.cw[(int64_t)b * v.d.ng + pos] = s - shat;
+    if (rec) {
+      const int64_t o = (int64_t)b * v.d.E + v.off[j] + (int64_t)v.knot[j] * v.d.nx;
+      for (int i = 0; i < v.d.nx; ++i) v.Y[o + i] = v.bhat[o + i];
+    }
   }
 }
 

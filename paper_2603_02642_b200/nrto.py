@@ -83,9 +83,10 @@ def lib():
         L.nrto_profile_enable.argtypes = [C.c_void_p, C.c_int32]
         L.nrto_profile_read.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_double),
                                         C.POINTER(C.c_int64)]
+        L.nrto_pass_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
         for f in ("nrto_layout", "nrto_setup", "nrto_inner_solve", "nrto_gain_update",
                   "nrto_soc_project", "nrto_destroy", "nrto_refresh", "nrto_profile_enable",
-                  "nrto_profile_read"):
+                  "nrto_profile_read", "nrto_pass_bytes"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -190,6 +191,13 @@ def nrto_profile_read(handle, kclass):
     return float(ms.value), int(n.value)
 
 
+def nrto_pass_bytes(handle) -> int:
+    """Algorithmic bytes moved by the fused state-cone pass since the last call."""
+    n = C.c_int64()
+    _check(lib().nrto_pass_bytes(C.c_void_p(handle), C.byref(n)))
+    return int(n.value)
+
+
 def nrto_inner_solve(handle, engine, out: dict, stream=None, memory=NRTO_MEM_DEVICE):
     o = nrto_out(memory, *[_ptr(out.get(k)) for k in OUT_FIELDS])
     _check(lib().nrto_inner_solve(C.c_void_p(handle), int(engine), C.byref(o), _stream_ptr(stream)))
@@ -265,6 +273,9 @@ class InnerSolver:
 
     def profile_read(self):
         return {n: nrto_profile_read(self.handle, i) for i, n in enumerate(KERNEL_CLASSES)}
+
+    def pass_bytes(self):
+        return nrto_pass_bytes(self.handle)
 
     def gain_update(self, nu, kv_prev, kv_next):
         nrto_gain_update(self.handle, nu, kv_prev, kv_next, self.stream)

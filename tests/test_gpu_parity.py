@@ -218,6 +218,37 @@ def test_bench_config_sampled():
         assert_parity(g, o, i=i)
 
 
+def test_overlapped_lazy_batch():
+    """B >= #SMs and fixed iterations: QP overlapped with the next pass and lazy
+    y storage.  Sampled instances against the oracle; the whole batch
+    against the eager in-order schedule (termination mode, eps = 0); the pass
+    byte counter between its bounds."""
+    _require_gpu()
+    B, L = 160, 20
+    items = [make_franka(5, i, T=12, jitter=True) for i in range(B)]
+    shape, batch = stack_instances(items)
+    data = nrto.to_tensors(batch, device="cuda")
+    s = nrto.InnerSolver(shape, data, max_iter=L, fixed_iters=1)
+    s.pass_bytes()
+    g = {k: v.cpu().numpy() for k, v in s.solve(nrto.NRTO_FULLADMM).items()}
+    moved = s.pass_bytes()
+    s.close()
+    for i in (0, 77, B - 1):
+        o = oracle_run(shape, items[i][1], nrto.NRTO_FULLADMM, max_iter=L, fixed_iters=1)
+        assert_parity(g, o, i=i)
+    e = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, max_iter=L, eps_p=0.0, eps_d=0.0)
+    assert np.all(e["iters"] == L)
+    for k in ("kv", "du", "p", "p_tilde", "lam_p", "nu", "lam_nu", "objective"):
+        assert close(g[k], e[k], tol=1e-11), k
+    kind = np.asarray(shape.cone_kind); knot = np.asarray(shape.cone_knot)
+    st_ = kind == 0
+    Es = int(((knot[st_] + 1) * shape.n_x).sum())
+    EBs = int((knot[st_] * (shape.n_u + shape.n_u % 2)).sum())
+    lo = 8 * B * L * (Es + EBs)                    # b_hat and b every iteration
+    hi = 8 * B * L * (3 * Es + EBs)                # + y read and written every iteration
+    assert lo < moved < hi
+
+
 def test_host_memory_path_matches_device():
     shape, data = CASES["c3s"]()
     b = single(shape, data)
