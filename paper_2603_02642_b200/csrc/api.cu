@@ -205,6 +205,17 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   v.nctrl = nctrl;
   v.ntiles = ntiles; v.nsplit = nsplit; v.nwitems = (int)(witems.size() / 4);
   v.nstate_tiles = nstate_tiles;
+  std::vector<int32_t> ttb;
+  int64_t est = 0, ebst = 0;
+  if (use_tma) {
+    for (int t = 0; t < nstate_tiles; ++t) {
+      const int kn = tiles[t * 12 + 1], nc = tiles[t * 12 + 2];
+      ttb.push_back((int32_t)est); ttb.push_back((int32_t)ebst);
+      est += (int64_t)(kn + 1) * nc * nx;
+      ebst += (int64_t)kn * nc * d.nup;
+    }
+  }
+  v.Est = est; v.EBst = ebst;
 
   const int64_t B = d.B;
   int32_t *dknot, *dkind, *dkptr, *dkcone, *dsptr, *dsrow, *dcptr, *dcrow;
@@ -239,6 +250,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   v.tiles = dtiles; v.witems = dwitems;
   AL(v.Zpart, (v.fused == 1 ? B * nsplit : 1) * T * nu * nx); AL(v.Zc, B * T * nu * nx);
   if (v.fused == 2) {
+    AL(v.ttb, ttb.size()); AL(v.bhat_t, B * est); AL(v.Bd_t, B * ebst);
     AL(v.G, B * T * nu * nu); AL(v.G0, B * T * nu * nu); AL(v.dG, B * T * nu * nu);
     AL(v.H, B * T * nu * nx); AL(v.H0, B * T * nu * nx); AL(v.dH, B * T * nu * nx);
   }
@@ -260,6 +272,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   hup(dsptr, sptr.data(), (T + 2) * 4); hup(dsrow, srow.data(), srow.size() * 4);
   hup(dcptr, cptr.data(), (T + 1) * 4); hup(dcrow, crow.data(), crow.size() * 4);
   hup(dtiles, tiles.data(), tiles.size() * 4); hup(dwitems, witems.data(), witems.size() * 4);
+  if (v.fused == 2) hup(v.ttb, ttb.data(), ttb.size() * 4);
   if (ce != cudaSuccess) { free_all(h); delete h; return cuda_fail(ce, "nrto_setup shape upload"); }
   nrto_err re = nrto_refresh(h, data, stream);
   if (re != NRTO_OK) { free_all(h); delete h; return re; }

@@ -91,6 +91,12 @@ struct Dev {
   double* Zctrl;           // [B][T][nu][nx] exact adjoint of the control cones (fused == 2)
   int ntiles, nsplit, nwitems;
   int nstate_tiles;        // state tiles come first in `tiles`
+  // TMA path: tile-interleaved copies of b_hat and b for the state tiles,
+  // block-major [k][cone of tile][i] so a chunk of a tile is one bulk copy.
+  int32_t* ttb;            // [nstate_tiles][2] tile base (b_hat_t, Bd_t) within an instance
+  int64_t Est, EBst;       // per-instance sizes of b_hat_t / Bd_t
+  double* bhat_t;          // [B][Est]
+  double* Bd_t;            // [B][EBst]
   const int32_t* tiles;    // [ntiles][12] kind, knot, nc, klo, cone[8]
   const int32_t* witems;   // [nwitems][4] b, t0, t1, split index
   double* Zpart;           // [B][nsplit][T][nu][nx] per-work-item adjoint partials
@@ -195,6 +201,7 @@ cudaError_t launch_count_active(nrto_handle_s* h, int32_t* d_count, int dr, cuda
 int read_setup_error(cudaStream_t st);
 cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st);
 cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_relayout(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,

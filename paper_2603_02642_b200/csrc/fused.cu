@@ -816,6 +816,8 @@ cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st) {
   // Zb_k = sum_j b_{j,k} b_hat_{j,k}^T : the list adjoint with y = b_hat
   cudaError_t e = launch_zlist(h, v.bhat, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, v.Zb, st);
   if (e != cudaSuccess || v.fused != 2) return e;
+  e = launch_relayout(h, st);
+  if (e != cudaSuccess) return e;
   // G0_k = sum_{state j} b b^T, H0_k = sum_{state j} b b_hat^T (TMA path predicted adjoint)
   return launch_zlist(h, nullptr, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, nullptr, st,
                       0, 2, v.G0, v.H0);

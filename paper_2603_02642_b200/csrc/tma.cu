@@ -14,6 +14,7 @@
 // Control cones have a single time block, so their norm, projection and exact
 // adjoint contribution s b y^T are completed inside one warp (k_fa_ctrl).
 #include "common.cuh"
+#include <algorithm>
 
 namespace nrto {
 
@@ -62,45 +63,54 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-constexpr int kStages = 3;
+constexpr int kMaxStages = 8;
 constexpr int kRingT = 4;
 constexpr int kTI = 12;   // ints per tile
+constexpr int kHdr = 32;  // header doubles: 2 kMaxStages barriers + cnt/tag
 
 struct TmaGeom {          // shared-memory geometry of one stage (doubles)
-  int SY;                 // per-cone stride of y / b_hat rows (16 n_x + pad)
-  int SB;                 // per-cone stride of b rows (16 nup + pad)
-  int stage;              // doubles per stage: 8 SY (y) + 8 SY (b_hat) + 8 SB (b)
+  int SY;                 // b_hat region: 16 blocks x 8 cones x n_x, block-major
+  int SB;                 // b region: 16 blocks x 8 cones x nup
+  int stage;              // doubles per stage (SY is a multiple of 16 doubles)
 };
 __host__ __device__ inline TmaGeom tma_geom(int nx, int nup) {
   TmaGeom g;
-  g.SY = 16 * nx + 8;     // == 8 (mod 16) doubles: conflict-free LDS.128 across the 8 cones
-  g.SB = 16 * nup + 4;    // == 4 (mod 16) doubles
-  g.stage = 16 * g.SY + 8 * g.SB;
+  g.SY = (16 * 8 * nx + 15) & ~15;
+  g.SB = 16 * 8 * nup;
+  g.stage = g.SY + g.SB;
   return g;
 }
+__host__ __device__ inline size_t tma_fixed_doubles(int T, int nx, int nu) {
+  return kHdr + kRingT * 16 * 8 + (((size_t)T * nx * nu + 1) & ~(size_t)1);
+}
 
+// Fused state-cone pass (norm-only form).  Per cone block k:
+//   y^l_k = D_k b_k + b_hat_k + (1 - s^{l-1}) y^{l-1}_k,  ||y^l||^2 accumulated,
+// y^l stored where a later step reads it (lazy y).  The adjoint is not formed
+// here: Z_pred = G D^T + H (k_fa_gain_w) plus the exact list correction.
+// b_hat and b reach shared memory by TMA bulk copies (producer warp, nst-stage
+// mbarrier ring); y^{l-1} of the few cones with s^{l-1} != 1 is loaded by the
+// consumers straight from global memory, issued before the stage wait.
 template <int NTI, int NKS, int KK>
 __global__ void __launch_bounds__(544, 1)
-k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems) {
+k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems, int nst) {
   extern __shared__ __align__(128) double sm[];
   constexpr int NW = 16;
   const Dims d = v.d;
   const int nx = d.nx, nu = d.nu, nup = d.nup, T = d.T;
   const TmaGeom G = tma_geom(nx, nup);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
-  uint64_t* empty = full + kStages;
-  int* cnt = reinterpret_cast<int*>(empty + kStages);
+  uint64_t* empty = full + kMaxStages;
+  int* cnt = reinterpret_cast<int*>(empty + kMaxStages);
   int* tag = cnt + kRingT;
-  double* ring = sm + 16;                                  // [kRingT][NW][8]
+  double* ring = sm + kHdr;                                // [kRingT][NW][8]
   double* Ds = ring + kRingT * NW * 8;                     // [T][nx][nu]
-  double* stg = Ds + ((T * nx * nu + 1) & ~1);             // stages
+  double* stg = sm + tma_fixed_doubles(T, nx, nu);         // stages
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int b = witems[4 * blockIdx.x], t0 = witems[4 * blockIdx.x + 1];
-  const int t1 = witems[4 * blockIdx.x + 2], sidx = witems[4 * blockIdx.x + 3];
+  const int t1 = witems[4 * blockIdx.x + 2];
   if (!v.active[b]) return;
-  const double* __restrict__ bhat = v.bhat + (int64_t)b * d.E;
-  const double* __restrict__ Bd = v.Bd + (int64_t)b * d.EB;
   double* __restrict__ Y = v.Y + (int64_t)b * d.E;
   const int64_t bg = (int64_t)b * d.ng;
   {
@@ -108,7 +118,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
     for (int r = threadIdx.x; r < T * nx * nu; r += blockDim.x) Ds[r] = Dg[r];
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
+    for (int s = 0; s < nst; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (threadIdx.x < kRingT) { cnt[threadIdx.x] = 0; tag[threadIdx.x] = threadIdx.x; }
@@ -117,63 +127,54 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
   if (warp == NW) {
     // ---------------------------------------------------------------- producer
     // lane c < nc owns cone c of the tile: its offsets are loaded once per tile
-    // and it issues that cone's bulk copies; lane 0 arms the stage barrier.
-    // Lazy y: y_old is fetched only for cones with 1 - s^{l-1} != 0 (y^0 = 0).
-    int n = 0;
+    // (one tile ahead) and it issues that cone's bulk copies; lane 0 arms the
+    // stage barrier and counts the algorithmic bytes of the launch.
+    int st = 0;
+    uint32_t ph = 0;
     unsigned long long moved = 0;
     const uint64_t pol = policy_evict_first();
-    int tnext = t0;
-    int64_t offn = 0, offBn = 0;
     bool ynext = false, wnext = false;
     auto cone_flags = [&](int j, bool& yr, bool& yw) {
       const double sp = v.s[bg + j];
       yr = v.iter > 1 && sp != 1.0;
       yw = !v.ylazy || shat_of(v, sp) != 1.0;
     };
-    if (tnext < t1 && lane < tiles[(int64_t)tnext * kTI + 2]) {
-      const int j = tiles[(int64_t)tnext * kTI + 4 + lane];
-      offn = v.off[j]; offBn = v.offB[j];
-      cone_flags(j, ynext, wnext);
-    }
+    if (t0 < t1 && lane < tiles[(int64_t)t0 * kTI + 2])
+      cone_flags(tiles[(int64_t)t0 * kTI + 4 + lane], ynext, wnext);
+    const double* __restrict__ bht = v.bhat_t + (int64_t)b * v.Est;
+    const double* __restrict__ bdt = v.Bd_t + (int64_t)b * v.EBst;
     for (int t = t0; t < t1; ++t) {
       const int* tl = tiles + (int64_t)t * kTI;
       const int K = tl[1], nc = tl[2];
-      const int64_t offc = offn, offBc = offBn;
+      const int64_t tb0 = v.ttb[2 * t], tb1 = v.ttb[2 * t + 1];
       const bool yrd = ynext, ywr = wnext;
-      if (t + 1 < t1 && lane < tiles[(int64_t)(t + 1) * kTI + 2]) {   // prefetch next tile
-        const int j = tiles[(int64_t)(t + 1) * kTI + 4 + lane];
-        offn = v.off[j]; offBn = v.offB[j];
-        cone_flags(j, ynext, wnext);
-      }
+      if (t + 1 < t1 && lane < tiles[(int64_t)(t + 1) * kTI + 2])   // flags of the next tile
+        cone_flags(tiles[(int64_t)(t + 1) * kTI + 4 + lane], ynext, wnext);
       const uint32_t nyr = __popc(__ballot_sync(0xffffffffu, lane < nc && yrd));
       const uint32_t nyw = __popc(__ballot_sync(0xffffffffu, lane < nc && ywr));
-      for (int kc = 0; kc <= K; kc += 16, ++n) {
-        const int st = n % kStages;
+      for (int kc = 0; kc <= K; kc += 16) {
         const int nb = min(16, K + 1 - kc), nbB = max(0, min(16, K - kc));
         if (lane == 0) {
-          mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
-          const uint32_t bytes = ((nyr + (uint32_t)nc) * nb * nx + (uint32_t)nc * nbB * nup) * 8u;
-          mbar_expect_tx(&full[st], bytes);
-          moved += bytes + (unsigned long long)nyw * nb * nx * 8u;
+          mbar_wait(&empty[st], ph ^ 1);
+          const uint32_t hb = (uint32_t)nc * nb * nx * 8u, bb = (uint32_t)nc * nbB * nup * 8u;
+          mbar_expect_tx(&full[st], hb + bb);
+          moved += hb + bb + (unsigned long long)(nyr + nyw) * nb * nx * 8u;
+          double* sH = stg + (size_t)st * G.stage;
+          double* sB = sH + G.SY;
+          // one bulk copy per array: the chunk is contiguous in the tile layout
+          bulk_g2s(sH, bht + tb0 + (int64_t)kc * nc * nx, hb, &full[st], pol);
+          if (bb > 0) bulk_g2s(sB, bdt + tb1 + (int64_t)kc * nc * nup, bb, &full[st], pol);
         }
         __syncwarp();
-        if (lane < nc) {
-          double* sY = stg + (size_t)st * G.stage;
-          double* sH = sY + 8 * G.SY;
-          double* sB = sH + 8 * G.SY;
-          const int64_t o = offc + (int64_t)kc * nx;
-          if (yrd) bulk_g2s(sY + lane * G.SY, Y + o, nb * nx * 8, &full[st], pol);
-          bulk_g2s(sH + lane * G.SY, bhat + o, nb * nx * 8, &full[st], pol);
-          if (nbB > 0)
-            bulk_g2s(sB + lane * G.SB, Bd + offBc + (int64_t)kc * nup, nbB * nup * 8, &full[st], pol);
-        }
+        if (++st == nst) { st = 0; ph ^= 1; }
       }
     }
     if (lane == 0 && v.pass_bytes) atomicAdd(v.pass_bytes, moved);
     return;
   }
   // ------------------------------------------------------------------ consumers
-  int n = 0;
+  int st = 0;
+  uint32_t ph = 0;
   for (int t = t0; t < t1; ++t) {
     const int* tl = tiles + (int64_t)t * kTI;
     const int K = tl[1], nc = tl[2];
@@ -182,44 +183,43 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
     const int cg = gv ? tl[4 + g] : 0;
     const int64_t offg = gv ? v.off[cg] : 0;
     const double sg = gv ? v.s[bg + cg] : 1.0;
-    const double omsp = (gv && v.iter > 1) ? 1.0 - sg : 0.0;   // != 0 <=> y_old was fetched
+    const double omsp = (gv && v.iter > 1) ? 1.0 - sg : 0.0;   // != 0 <=> y_old is read
     const bool wy = gv && (!v.ylazy || shat_of(v, sg) != 1.0);  // store y^l
     double nrm = 0.0;
 #pragma unroll
     for (int kk = 0; kk < KK; ++kk) {
       const int kc = NW * kk;
       if (kc > K) break;
-      const int st = n % kStages;
-      mbar_wait(&full[st], (n / kStages) & 1);
-      ++n;
-      const double* sY = stg + (size_t)st * G.stage;
-      const double* sH = sY + 8 * G.SY;
-      const double* sB = sH + 8 * G.SY;
       const int k = kc + warp;
-      if (k <= K) {
+      const bool act = k <= K;
+      double2 yo[NTI];
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) {
+        const int i0 = 2 * q + 8 * nt;
+        yo[nt] = make_double2(0.0, 0.0);
+        if (act && omsp != 0.0 && i0 < nx)
+          yo[nt] = __ldcs(reinterpret_cast<const double2*>(Y + offg + (int64_t)k * nx + i0));
+      }
+      mbar_wait(&full[st], ph);
+      const double* sH = stg + (size_t)st * G.stage;
+      const double* sB = sH + G.SY;
+      if (act) {
         double c[NTI][2];
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
           const int i0 = 2 * q + 8 * nt;
           c[nt][0] = 0.0; c[nt][1] = 0.0;
           if (gv && i0 < nx) {
-            const int e = g * G.SY + warp * nx + i0;
-            const double2 bh = *reinterpret_cast<const double2*>(sH + e);
-            if (omsp != 0.0) {
-              const double2 yo = *reinterpret_cast<const double2*>(sY + e);
-              c[nt][0] = bh.x + omsp * yo.x;
-              c[nt][1] = bh.y + omsp * yo.y;
-            } else {
-              c[nt][0] = bh.x;
-              c[nt][1] = bh.y;
-            }
+            const double2 bh = *reinterpret_cast<const double2*>(sH + (warp * nc + g) * nx + i0);
+            c[nt][0] = bh.x + omsp * yo[nt].x;
+            c[nt][1] = bh.y + omsp * yo[nt].y;
           }
         }
         if (k < K) {
 #pragma unroll
           for (int ks = 0; ks < NKS; ++ks) {
             const int m = q + 4 * ks;
-            const double a = (gv && m < nu) ? sB[g * G.SB + warp * nup + m] : 0.0;
+            const double a = (gv && m < nu) ? sB[(warp * nc + g) * nup + m] : 0.0;
 #pragma unroll
             for (int nt = 0; nt < NTI; ++nt) {
               const int i = g + 8 * nt;
@@ -239,6 +239,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == nst) { st = 0; ph ^= 1; }
     }
     // ---- norm partials -> ring slot; last consumer warp publishes the tile's norms
     nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
@@ -268,7 +269,6 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       }
     }
   }
-  (void)sidx;
 }
 
 // Control cones (single block at step k): y = D_k h' + (1 - s) y_old, ||y||^2,
@@ -369,16 +369,53 @@ cudaError_t launch_project(nrto_handle_s* h, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Tile-interleaved copies of b_hat and b (state tiles), one CTA per (instance, tile):
+//   bhat_t[b][ttb0 + (k nc + c) n_x + i] = bhat[b][off_c + k n_x + i],   k = 0..K
+//   Bd_t[b][ttb1 + (k nc + c) nup + m]   = Bd[b][offB_c + k nup + m],    k = 0..K-1
+__global__ void k_relayout(Dev v) {
+  const int t = blockIdx.x, b = blockIdx.y;
+  const int* tl = v.tiles + (int64_t)t * kTI;
+  const int K = tl[1], nc = tl[2];
+  const int nx = v.d.nx, nup = v.d.nup;
+  const double* bh = v.bhat + (int64_t)b * v.d.E;
+  const double* bd = v.Bd + (int64_t)b * v.d.EB;
+  double* oh = v.bhat_t + (int64_t)b * v.Est + v.ttb[2 * t];
+  double* ob = v.Bd_t + (int64_t)b * v.EBst + v.ttb[2 * t + 1];
+  const int nh = (K + 1) * nc * nx, nbb = K * nc * nup;
+  for (int r = threadIdx.x; r < nh; r += blockDim.x) {
+    const int i = r % nx, c = (r / nx) % nc, k = r / (nx * nc);
+    oh[r] = bh[v.off[tl[4 + c]] + (int64_t)k * nx + i];
+  }
+  for (int r = threadIdx.x; r < nbb; r += blockDim.x) {
+    const int m = r % nup, c = (r / nup) % nc, k = r / (nup * nc);
+    ob[r] = bd[v.offB[tl[4 + c]] + (int64_t)k * nup + m];
+  }
+}
+
+cudaError_t launch_relayout(nrto_handle_s* h, cudaStream_t st) {
+  const Dev& v = h->dev;
+  if (v.nstate_tiles > 0 && v.d.B > 0) {
+    k_relayout<<<dim3(v.nstate_tiles, v.d.B), 256, 0, st>>>(v);
+    h->launches++;
+  }
+  return cudaGetLastError();
+}
+
+static int tma_stages(const Dims& d) {
+  const TmaGeom G = tma_geom(d.nx, d.nup);
+  const size_t fixed = tma_fixed_doubles(d.T, d.nx, d.nu);
+  const size_t cap = 225 * 1024 / sizeof(double);
+  if (fixed >= cap) return 0;
+  return (int)std::min<size_t>(kMaxStages, (cap - fixed) / G.stage);
+}
+
 size_t tma_smem_bytes(const Dims& d) {
   const TmaGeom G = tma_geom(d.nx, d.nup);
-  const size_t dbl = 16 + kRingT * 16 * 8 + ((size_t)(d.T * d.nx * d.nu + 1) & ~(size_t)1) +
-                     (size_t)kStages * G.stage;
-  return dbl * sizeof(double);
+  return (tma_fixed_doubles(d.T, d.nx, d.nu) + (size_t)tma_stages(d) * G.stage) * sizeof(double);
 }
 
 bool tma_supported(const Dims& d) {
-  return (d.nx % 2 == 0) && d.nx <= 16 && d.nu <= 8 && d.T <= 111 &&
-         tma_smem_bytes(d) <= 220 * 1024;
+  return (d.nx % 2 == 0) && d.nx <= 16 && d.nu <= 8 && d.T <= 111 && tma_stages(d) >= 3;
 }
 
 template <int NTI, int NKS, int KK>
@@ -386,7 +423,7 @@ static cudaError_t launch_tma_t(nrto_handle_s* h, cudaStream_t st) {
   const size_t smem = tma_smem_bytes(h->dev.d);
   auto kfn = k_fa_tma<NTI, NKS, KK>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kfn<<<h->dev.nwitems, 544, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems);
+  kfn<<<h->dev.nwitems, 544, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems, tma_stages(h->dev.d));
   h->launches++;
   return cudaGetLastError();
 }
