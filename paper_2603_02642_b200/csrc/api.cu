@@ -235,7 +235,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   AL(v.U, B * T * nx * nx); AL(v.Ulam, B * T * nx); AL(v.Urep, B * T);
   for (EngineFactors* F : {&v.fa, &v.dr}) {
     AL(F->V, B * T * nu * nu); AL(F->den, B * T * nu * nx); AL(F->Kf, B * T * nu * nx);
-    AL(F->Acl, B * T * nx * nx); AL(F->Hinv, B * T * nu * nu); AL(F->HB, B * T * nu * nx);
+    AL(F->Acl, B * T * nx * nx); AL(F->AclT, B * T * nx * nx); AL(F->Hinv, B * T * nu * nu); AL(F->HB, B * T * nu * nx);
   }
   AL(v.Y, B * d.E); AL(v.s, B * ng); AL(v.tin, B * ng); AL(v.pt, B * ng); AL(v.ptprev, B * ng);
   AL(v.p, B * ng); AL(v.lamp, B * ng); AL(v.K, B * d.NK); AL(v.Ccur, B * T * nx * nu);
@@ -255,7 +255,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
     AL(v.H, B * T * nu * nx); AL(v.H0, B * T * nu * nx); AL(v.dH, B * T * nu * nx);
   }
   AL(v.Zctrl, B * T * nu * nx); AL(v.nrm2, B * ng);
-  AL(v.gnz, B * ng); AL(v.gidx, B * ng * 8); AL(v.gval, B * ng * 8);
+  AL(v.rowpk, B * ng); AL(v.gval, B * ng * 8);
   AL(v.pass_bytes, 1);
   cudaMemset(v.pass_bytes, 0, sizeof(unsigned long long));
   v.ylazy = 0;

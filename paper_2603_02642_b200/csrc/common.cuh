@@ -22,6 +22,7 @@ struct EngineFactors {
   double* den;   // [B][T][nu][nx]  1 / (2 + c tau sigma_a lambda_b)
   double* Kf;    // [B][T][nu][nx]  Riccati feedback of the QP x-step
   double* Acl;   // [B][T][nx][nx]  A_k - B_k Kf_k
+  double* AclT;  // [B][T][nx][nx]  its transpose (row i = column i of Acl_k)
   double* Hinv;  // [B][T][nu][nu]  H_uu^{-1}
   double* HB;    // [B][T][nu][nx]  H_uu^{-1} B_k^T
 };
@@ -85,9 +86,8 @@ struct Dev {
   double* H0;              // [B][T][nu][nx]
   double* dG;              // [B][T][nu][nu] this iteration's leave/enter update
   double* dH;              // [B][T][nu][nx]
-  uint8_t* gnz;            // [B][ng] nonzeros of each gradient row (255: dense)
-  int8_t* gidx;            // [B][ng][8] their indices
-  double* gval;            // [B][ng][8] their values
+  int4* rowpk;             // [B][ng] packed gradient-row record (qp.cu, k_sparse_rows)
+  double* gval;            // [B][ng][8] its nonzero values
   double* Zctrl;           // [B][T][nu][nx] exact adjoint of the control cones (fused == 2)
   int ntiles, nsplit, nwitems;
   int nstate_tiles;        // state tiles come first in `tiles`

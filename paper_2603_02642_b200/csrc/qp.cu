@@ -685,37 +685,146 @@ __global__ void __launch_bounds__(256, 5) k_qp_lite(Dev v, int engine, int l) {
 // iteration (SURVEY F4 products with B and B^T).
 constexpr int kRowNZ = 8;
 
-__device__ __forceinline__ void scatter_row(const Dev& v, int64_t ij, int kind, int k, double w,
-                                            const double* grad_j, double* gS, double* gU) {
+// Packed row record (setup, k_sparse_rows): {knot, kind | nz << 8, idx0..3, idx4..7}
+// (nz = 255: dense row, read from grad).  The values sit in gval[row][8].
+__device__ __forceinline__ int rec_idx(const int4& r, int s) {
+  const uint32_t w = (s < 4) ? (uint32_t)r.z : (uint32_t)r.w;
+  return (int)((w >> (8 * (s & 3))) & 0xffu);
+}
+
+// Rows of one QP iteration, 4 rows per thread in flight: (it) gather
+// bd_j = <grad_j, x_k> (x = dx~ for state rows, du~ for control rows), update
+// (p, z, y)_j, and (more) form the next iteration's rhs_p / w_j and scatter
+// w_j grad_j into S_k / U_k (FP64 RED.ADD).  first: only the rhs / scatter.
+constexpr int kRowBatch = 2;
+template <bool FIRST, int U>
+__device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int tid, int nt,
+                                        const double* __restrict__ grad,
+                                        const double* __restrict__ g0, double* p, double* zl,
+                                        double* yl, double* rp, const double* pt,
+                                        const double* lam, const double* sX, const double* gR,
+                                        double* gS, double* gU, bool more, double rho, double rq,
+                                        double sq, double aq, double den, double beta,
+                                        double rinv) {
   const int nx = v.d.nx, nu = v.d.nu;
-  const int nz = v.gnz[ij];
-  double* dst = (kind == 0) ? gS + (int64_t)k * nx : gU + (int64_t)k * nu;
-  if (nz <= kRowNZ) {
-    const int8_t* gi = v.gidx + ij * kRowNZ;
-    const double* gv = v.gval + ij * kRowNZ;
-    for (int s = 0; s < nz; ++s) atomicAdd(dst + gi[s], w * gv[s]);
-  } else {
-    const int n = (kind == 0) ? nx : nu;
-    for (int i = 0; i < n; ++i) atomicAdd(dst + i, w * grad_j[i]);
+  const int4* __restrict__ rows = v.rowpk + bg;
+  const double* __restrict__ gval = v.gval + bg * kRowNZ;
+  for (int j0 = tid; j0 < ng; j0 += U * nt) {
+    int4 rc[U];
+    double2 g01[U];
+    double rpj[U], pj[U], zlj[U], ylj[U], g0j[U], ptj[U], lmj[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * nt;
+      if (j < ng) {
+        rc[u] = rows[j];
+        g01[u] = *reinterpret_cast<const double2*>(gval + (int64_t)j * kRowNZ);
+        pj[u] = p[j]; zlj[u] = zl[j]; ylj[u] = yl[j]; ptj[u] = pt[j]; lmj[u] = lam[j];
+        if (!FIRST) { rpj[u] = rp[j]; g0j[u] = g0[j]; }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * nt;
+      if (j >= ng) continue;
+      const int k = rc[u].x, kind = rc[u].y & 0xff, nz = (rc[u].y >> 8) & 0xff;
+      const double* gj = grad + (int64_t)j * nx;
+      double pn = pj[u], zn = zlj[u], yn = ylj[u];
+      if (!FIRST) {
+        const double* x = (kind == 0) ? sX + (int64_t)k * nx : gR + (int64_t)k * nu;
+        double bd = 0.0;
+        if (nz <= kRowNZ) {
+          if (nz > 0) bd += g01[u].x * x[rec_idx(rc[u], 0)];
+          if (nz > 1) bd += g01[u].y * x[rec_idx(rc[u], 1)];
+          for (int q = 2; q < nz; ++q) bd += gval[(int64_t)j * kRowNZ + q] * x[rec_idx(rc[u], q)];
+        } else {
+          const int n = (kind == 0) ? nx : nu;
+          for (int i = 0; i < n; ++i) bd += gj[i] * x[i];
+        }
+        const double ptl = (rpj[u] - rq * bd) / den;
+        pn = aq * ptl + (1.0 - aq) * pj[u];
+        const double zh = aq * (bd + ptl) + (1.0 - aq) * zlj[u];
+        zn = fmin(zh + ylj[u] / rq, -g0j[u]);
+        yn = ylj[u] + rq * (zh - zn);
+        p[j] = pn; zl[j] = zn; yl[j] = yn;
+      }
+      if (FIRST || more) {
+        const double vj = ptj[u] - lmj[u] * rinv;
+        const double r = sq * pn + rho * vj + rq * zn - yn;
+        rp[j] = r;
+        const double w = rq * zn - yn - beta * r;
+        double* dst = (kind == 0) ? gS + (int64_t)k * nx : gU + (int64_t)k * nu;
+        if (nz <= kRowNZ) {
+          if (nz > 0) atomicAdd(dst + rec_idx(rc[u], 0), w * g01[u].x);
+          if (nz > 1) atomicAdd(dst + rec_idx(rc[u], 1), w * g01[u].y);
+          for (int q = 2; q < nz; ++q)
+            atomicAdd(dst + rec_idx(rc[u], q), w * gval[(int64_t)j * kRowNZ + q]);
+        } else {
+          const int n = (kind == 0) ? nx : nu;
+          for (int i = 0; i < n; ++i) atomicAdd(dst + i, w * gj[i]);
+        }
+      }
+    }
   }
 }
 
-__device__ __forceinline__ double gather_row(const Dev& v, int64_t ij, int kind,
-                                             const double* x, const double* grad_j) {
-  const int nx = v.d.nx, nu = v.d.nu;
-  const int nz = v.gnz[ij];
-  double acc = 0.0;
-  if (nz <= kRowNZ) {
-    const int8_t* gi = v.gidx + ij * kRowNZ;
-    const double* gv = v.gval + ij * kRowNZ;
-    for (int s = 0; s < nz; ++s) acc += gv[s] * x[gi[s]];
+// Debug timing of one QP CTA (instance 0, first two QP iterations): clock64 at
+// every phase boundary, read with nrto_debug_qp_clocks (not part of nrto.h).
+__device__ long long g_qp_clk[64];
+#define QP_CLK(ph) \
+  do { if (b == 0 && tid == 0 && it_dbg < 2) g_qp_clk[it_dbg * 32 + (ph)] = clock64(); } while (0)
+
+// sum_{q < n} fa(q) fb(q) + acc.  NM > 0 (a multiple of 8, n <= NM): loads issued
+// 8 at a time (predicated) so dependent latency is paid once per batch, not per
+// term; NM = 0: plain loop.
+template <int NM, class FA, class FB>
+__device__ __forceinline__ double dotn(int n, FA fa, FB fb, double acc) {
+  if constexpr (NM > 0) {
+    double c[4] = {acc, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q0 = 0; q0 < NM; q0 += 8) {
+      double av[8], bv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + u;
+        const bool ok = q < n;
+        av[u] = ok ? fa(q) : 0.0;
+        bv[u] = ok ? fb(q) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u & 3] = fma(av[u], bv[u], c[u & 3]);
+    }
+    return (c[0] + c[1]) + (c[2] + c[3]);
   } else {
-    const int n = (kind == 0) ? nx : nu;
-    for (int i = 0; i < n; ++i) acc += grad_j[i] * x[i];
+    for (int q = 0; q < n; ++q) acc += fa(q) * fb(q);
+    return acc;
   }
-  return acc;
 }
 
+// mbarrier / bulk-copy helpers for the recurrence ring (TMA, SASS UBLKCP)
+__device__ __forceinline__ void qp_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void qp_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void qp_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "QPW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra QPW_%=;\n"
+      "}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int NXM, int NUM>
 __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) {
   extern __shared__ double sm[];
   __shared__ double red[32];
@@ -735,7 +844,6 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
   const double* pt = v.pt + bg; double* lam = v.lamp + bg;
   double* zb = v.zb + (int64_t)b * (T + 1) * nx; double* yb = v.yb + (int64_t)b * (T + 1) * nx;
   double* du = v.du + (int64_t)b * T * nu;
-  double* gA = v.dxt + (int64_t)b * (T + 1) * nx;    // a_k, then e_k
   double* gK = v.kff + (int64_t)b * T * nu;           // kff_k
   double* gR = v.ru + (int64_t)b * T * nu;            // r_u,k, then du~_k
   double* gS = v.rx + (int64_t)b * (T + 1) * nx;      // S_k = sum_{state j@k} w_j grad_j (atomic)
@@ -751,45 +859,90 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
   const double rinv = (engine == NRTO_FULLADMM) ? 1.0 : 1.0 / rho;
   double* sS = sm;                                    // [(T+1) nx]
   double* ring = sS + (T + 1) * nx;                   // [kQPRing][nx nx]
+  uint64_t* qbar = reinterpret_cast<uint64_t*>(ring + kQPRing * nx * nx);   // [kQPRing]
+  int rslot = 0;                                      // recurrence ring position (warp 0)
+  uint32_t rph = 0;
   const int nn = nx * nx;
   const int nits = v.prm.qp_iters;
+  int it_dbg = 0;
 
+  if (NXM > 0 && tid == 0) {
+    for (int q = 0; q < kQPRing; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&qbar[q])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int r = tid; r < (T + 1) * nx; r += nt) gS[r] = 0.0;
   for (int r = tid; r < T * nu; r += nt) gU[r] = 0.0;
   __syncthreads();
+  QP_CLK(0);
   if (nits > 0) {                                     // rhs / w / scatter of iteration 0
-    for (int j = tid; j < ng; j += nt) {
-      const double vj = pt[j] - lam[j] * rinv;
-      const double r = sq * p[j] + rho * vj + rq * zl[j] - yl[j];
-      rp[j] = r;
-      const double w = rq * zl[j] - yl[j] - beta * r;
-      scatter_row(v, bg + j, v.kind[j], v.knot[j], w, grad + (int64_t)j * nx, gS, gU);
-    }
+    qp_rows<true, kRowBatch>(v, bg, ng, tid, nt, grad, g0, p, zl, yl, rp, pt, lam, sS, gR, gS, gU, true,
+                  rho, rq, sq, aq, den, beta, rinv);
     __syncthreads();
+    QP_CLK(1);
   }
   for (int it = 0; it < nits; ++it) {
+    it_dbg = it;
     for (int r = tid; r < T * nu; r += nt) {          // r_u (consumes and clears U)
       const int k = r / nu, m = r % nu;
-      double acc = sq * du[r] + gU[r];
+      const double* Rm = Ru + (k * nu + m) * nu;
+      const double* uk = uh + k * nu;
+      const double ru = dotn<NUM>(nu, [&](int q) { return Rm[q]; }, [&](int q) { return uk[q]; }, 0.0);
+      const double acc = sq * du[r] + gU[r] - 2.0 * ru;
       gU[r] = 0.0;
-      for (int q = 0; q < nu; ++q) acc -= 2.0 * Ru[(k * nu + m) * nu + q] * uh[k * nu + q];
       gR[r] = acc;
     }
     __syncthreads();
+    QP_CLK(2);
     for (int r = tid; r < (T + 1) * nx; r += nt) {    // r_x and a_k (consumes and clears S)
       const int k = r / nx, i = r % nx;
       double acc = (k > 0) ? gS[r] + rq * zb[r] - yb[r] : 0.0;
       gS[r] = 0.0;
       if (k < T) {
-        const double* Kk = Kf + (int64_t)k * nu * nx;
-        for (int m = 0; m < nu; ++m) acc -= Kk[m * nx + i] * gR[k * nu + m];
-        gA[r] = acc;
-      } else {
-        sS[r] = acc;
+        const double* Kk = Kf + (int64_t)k * nu * nx + i;
+        const double* rk = gR + k * nu;
+        acc -= dotn<NUM>(nu, [&](int m) { return Kk[m * nx]; }, [&](int m) { return rk[m]; }, 0.0);
       }
+      sS[r] = acc;        // a_k (k < T), s_T; the recurrence overwrites a_k by s_k
     }
     __syncthreads();
-    if (tid < 32) {                                   // backward recurrence, Acl ring
+    QP_CLK(3);
+    if (tid < 32) {                                   // backward recurrence
+      if constexpr (NXM > 0) {
+        // s_k[i] = a_k[i] + <AclT_k row i, s_{k+1}>: AclT_k arrives by one bulk copy
+        // per step into a kQPRing-slot ring (mbarrier), s_{k+1} by broadcast LDS.128
+        const double* AT = F.AclT + (int64_t)b * T * nn;
+        if (tid == 0)
+          for (int pf = 0; pf < kQPRing && pf < T; ++pf) {
+            const int sl = (rslot + pf) % kQPRing;
+            qp_expect_tx(&qbar[sl], nn * 8);
+            qp_bulk(ring + sl * nn, AT + (int64_t)(T - 1 - pf) * nn, nn * 8, &qbar[sl]);
+          }
+        const int ic = tid < nx ? tid : 0;
+        for (int k = T - 1; k >= 0; --k) {
+          qp_wait(&qbar[rslot], rph);
+          const double* Ar = ring + rslot * nn + ic * nx;
+          const double* sn = sS + (k + 1) * nx;
+          double c0 = sS[k * nx + ic], c1 = 0.0;
+#pragma unroll
+          for (int r = 0; r < NXM; r += 2)
+            if (r < nx) {
+              const double2 a = *reinterpret_cast<const double2*>(Ar + r);
+              const double2 x2 = *reinterpret_cast<const double2*>(sn + r);
+              c0 = fma(a.x, x2.x, c0);
+              c1 = fma(a.y, x2.y, c1);
+            }
+          __syncwarp();
+          if (tid < nx) sS[k * nx + tid] = c0 + c1;
+          __syncwarp();
+          const int kn = k - kQPRing;
+          if (tid == 0 && kn >= 0) {
+            qp_expect_tx(&qbar[rslot], nn * 8);
+            qp_bulk(ring + rslot * nn, AT + (int64_t)kn * nn, nn * 8, &qbar[rslot]);
+          }
+          if (++rslot == kQPRing) { rslot = 0; rph ^= 1; }
+        }
+      } else {
       for (int pf = 0; pf < kQPRing; ++pf) {
         const int k = T - 1 - pf;
         if (k >= 0) for (int e = tid; e < nn; e += 32) cpa8(ring + pf * nn + e, AclG + (int64_t)k * nn + e);
@@ -801,16 +954,9 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
         cpa_wait<kQPRing - 1>();
         __syncwarp();
         const double* Ak = ring + slot * nn + ic;
-        double a0 = gA[k * nx + ic], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int r = 0;
-        for (; r + 4 <= nx; r += 4) {
-          a0 += Ak[(r + 0) * nx] * __shfl_sync(0xffffffffu, s, r + 0);
-          a1 += Ak[(r + 1) * nx] * __shfl_sync(0xffffffffu, s, r + 1);
-          a2 += Ak[(r + 2) * nx] * __shfl_sync(0xffffffffu, s, r + 2);
-          a3 += Ak[(r + 3) * nx] * __shfl_sync(0xffffffffu, s, r + 3);
-        }
-        for (; r < nx; ++r) a0 += Ak[r * nx] * __shfl_sync(0xffffffffu, s, r);
-        s = (a0 + a1) + (a2 + a3);
+        const double* sn = sS + (k + 1) * nx;       // s_{k+1} (broadcast reads)
+        s = dotn<NXM>(nx, [&](int r) { return Ak[r * nx]; }, [&](int r) { return sn[r]; },
+                      sS[k * nx + ic]);
         if (tid < nx) sS[k * nx + tid] = s;
         __syncwarp();
         const int kn = k - kQPRing;
@@ -818,27 +964,68 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
         cpa_commit();
       }
       cpa_wait<0>();
+      }
     }
     __syncthreads();
+    QP_CLK(4);
     for (int r = tid; r < T * nu; r += nt) {          // kff_k
       const int k = r / nu, m = r % nu;
-      const double* H = Hi + (int64_t)k * nu * nu;
-      const double* hb = HB + (int64_t)k * nu * nx;
-      double acc = 0.0;
-      for (int q = 0; q < nu; ++q) acc += H[m * nu + q] * gR[k * nu + q];
-      for (int i = 0; i < nx; ++i) acc += hb[m * nx + i] * sS[(k + 1) * nx + i];
+      const double* H = Hi + (int64_t)k * nu * nu + m * nu;
+      const double* hb = HB + (int64_t)k * nu * nx + m * nx;
+      const double* rk = gR + k * nu;
+      const double* sk = sS + (k + 1) * nx;
+      double acc = dotn<NUM>(nu, [&](int q) { return H[q]; }, [&](int q) { return rk[q]; }, 0.0);
+      acc = dotn<NXM>(nx, [&](int q) { return hb[q]; }, [&](int q) { return sk[q]; }, acc);
       gK[r] = acc;
     }
     __syncthreads();
+    QP_CLK(5);
     for (int r = tid; r < T * nx; r += nt) {          // e_k = B_k kff_k
       const int k = r / nx, i = r % nx;
-      const double* Bk = Bm + (int64_t)k * nx * nu;
-      double acc = 0.0;
-      for (int m = 0; m < nu; ++m) acc += Bk[i * nu + m] * gK[k * nu + m];
-      gA[r] = acc;
+      const double* Bk = Bm + (int64_t)k * nx * nu + i * nu;
+      const double* kk = gK + k * nu;
+      const double acc = dotn<NUM>(nu, [&](int m) { return Bk[m]; }, [&](int m) { return kk[m]; }, 0.0);
+      sS[r + nx] = acc;   // e_k at slot k+1; the forward recurrence overwrites it by dx_{k+1}
     }
     __syncthreads();
-    if (tid < 32) {                                   // forward recurrence, Acl ring
+    QP_CLK(6);
+    if (tid < 32) {                                   // forward recurrence
+      if constexpr (NXM > 0) {
+        // dx_{k+1}[i] = e_k[i] + <Acl_k row i, dx_k>
+        const double* AG = F.Acl + (int64_t)b * T * nn;
+        if (tid == 0)
+          for (int pf = 0; pf < kQPRing && pf < T; ++pf) {
+            const int sl = (rslot + pf) % kQPRing;
+            qp_expect_tx(&qbar[sl], nn * 8);
+            qp_bulk(ring + sl * nn, AG + (int64_t)pf * nn, nn * 8, &qbar[sl]);
+          }
+        const int ic = tid < nx ? tid : 0;
+        if (tid < nx) sS[tid] = 0.0;
+        __syncwarp();
+        for (int k = 0; k < T; ++k) {
+          qp_wait(&qbar[rslot], rph);
+          const double* Ar = ring + rslot * nn + ic * nx;
+          const double* xk = sS + k * nx;
+          double c0 = sS[(k + 1) * nx + ic], c1 = 0.0;
+#pragma unroll
+          for (int r = 0; r < NXM; r += 2)
+            if (r < nx) {
+              const double2 a = *reinterpret_cast<const double2*>(Ar + r);
+              const double2 x2 = *reinterpret_cast<const double2*>(xk + r);
+              c0 = fma(a.x, x2.x, c0);
+              c1 = fma(a.y, x2.y, c1);
+            }
+          __syncwarp();
+          if (tid < nx) sS[(k + 1) * nx + tid] = c0 + c1;
+          __syncwarp();
+          const int kn = k + kQPRing;
+          if (tid == 0 && kn < T) {
+            qp_expect_tx(&qbar[rslot], nn * 8);
+            qp_bulk(ring + rslot * nn, AG + (int64_t)kn * nn, nn * 8, &qbar[rslot]);
+          }
+          if (++rslot == kQPRing) { rslot = 0; rph ^= 1; }
+        }
+      } else {
       for (int pf = 0; pf < kQPRing; ++pf) {
         if (pf < T) for (int e = tid; e < nn; e += 32) cpa8(ring + pf * nn + e, AclG + (int64_t)pf * nn + e);
         cpa_commit();
@@ -850,16 +1037,9 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
         cpa_wait<kQPRing - 1>();
         __syncwarp();
         const double* Ak = ring + slot * nn + ic * nx;
-        double a0 = gA[k * nx + ic], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int r = 0;
-        for (; r + 4 <= nx; r += 4) {
-          a0 += Ak[r + 0] * __shfl_sync(0xffffffffu, x, r + 0);
-          a1 += Ak[r + 1] * __shfl_sync(0xffffffffu, x, r + 1);
-          a2 += Ak[r + 2] * __shfl_sync(0xffffffffu, x, r + 2);
-          a3 += Ak[r + 3] * __shfl_sync(0xffffffffu, x, r + 3);
-        }
-        for (; r < nx; ++r) a0 += Ak[r] * __shfl_sync(0xffffffffu, x, r);
-        x = (a0 + a1) + (a2 + a3);
+        const double* xk = sS + k * nx;             // dx_k (broadcast reads)
+        x = dotn<NXM>(nx, [&](int r) { return Ak[r]; }, [&](int r) { return xk[r]; },
+                      sS[(k + 1) * nx + ic]);
         if (tid < nx) sS[(k + 1) * nx + tid] = x;
         __syncwarp();
         const int kn = k + kQPRing;
@@ -867,37 +1047,24 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
         cpa_commit();
       }
       cpa_wait<0>();
-    }
-    __syncthreads();
-    for (int r = tid; r < T * nu; r += nt) {          // du~_k
-      const int k = r / nu, m = r % nu;
-      const double* Kk = Kf + (int64_t)k * nu * nx;
-      double acc = gK[r];
-      for (int q = 0; q < nx; ++q) acc -= Kk[m * nx + q] * sS[k * nx + q];
-      gR[r] = acc;
-    }
-    __syncthreads();
-    const bool more = it + 1 < nits;
-    for (int j = tid; j < ng; j += nt) {              // rows: gather, update, next rhs, scatter
-      const int k = v.knot[j], kind = v.kind[j];
-      const double* gj = grad + (int64_t)j * nx;
-      const double bd = gather_row(v, bg + j, kind, (kind == 0) ? sS + (int64_t)k * nx : gR + (int64_t)k * nu, gj);
-      const double ptl = (rp[j] - rq * bd) / den;
-      const double pn = aq * ptl + (1.0 - aq) * p[j];
-      const double zl0 = zl[j], yl0 = yl[j];
-      const double zh = aq * (bd + ptl) + (1.0 - aq) * zl0;
-      const double zn = fmin(zh + yl0 / rq, -g0[j]);
-      const double yn = yl0 + rq * (zh - zn);
-      p[j] = pn; zl[j] = zn; yl[j] = yn;
-      if (more) {
-        const double vj = pt[j] - lam[j] * rinv;
-        const double r = sq * pn + rho * vj + rq * zn - yn;
-        rp[j] = r;
-        scatter_row(v, bg + j, kind, k, rq * zn - yn - beta * r, gj, gS, gU);
       }
     }
+    __syncthreads();
+    QP_CLK(7);
+    for (int r = tid; r < T * nu; r += nt) {          // du~_k
+      const int k = r / nu, m = r % nu;
+      const double* Kk = Kf + (int64_t)k * nu * nx + m * nx;
+      const double* xk = sS + k * nx;
+      gR[r] = gK[r] - dotn<NXM>(nx, [&](int q) { return Kk[q]; }, [&](int q) { return xk[q]; }, 0.0);
+    }
+    __syncthreads();
+    QP_CLK(8);
+    const bool more = it + 1 < nits;
+    qp_rows<false, kRowBatch>(v, bg, ng, tid, nt, grad, g0, p, zl, yl, rp, pt, lam, sS, gR, gS, gU, more,
+                   rho, rq, sq, aq, den, beta, rinv);
     for (int r = tid; r < T * nu; r += nt) du[r] = aq * gR[r] + (1.0 - aq) * du[r];
     __syncthreads();
+    QP_CLK(9);
     double nb = 0.0;                                  // trust-region ball
     for (int r = tid; r < (T + 1) * nx; r += nt) {
       const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
@@ -914,6 +1081,7 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
       zb[r] = zn;
     }
     __syncthreads();
+    QP_CLK(10);
   }
   double ap = 0.0, ad = 0.0;
   double* tin = v.tin + bg;
@@ -950,20 +1118,31 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
 }
 
 // Setup: compressed rows of the constraint gradients (state rows: n_x entries,
-// control rows: the first n_u); nnz > kRowNZ keeps the dense row (gnz = 255).
+// control rows: the first n_u) as packed records {knot, kind | nz << 8, idx0..3,
+// idx4..7} + values gval[row][8]; nnz > kRowNZ keeps the dense row (nz = 255).
 __global__ void k_sparse_rows(Dev v) {
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= (int64_t)v.d.B * v.d.ng) return;
   const int j = (int)(id % v.d.ng);
-  const int n = (v.kind[j] == 0) ? v.d.nx : v.d.nu;
+  const int kind = v.kind[j];
+  const int n = (kind == 0) ? v.d.nx : v.d.nu;
   const double* g = v.grad + id * v.d.nx;
   int nz = 0;
   for (int i = 0; i < n; ++i) nz += (g[i] != 0.0);
-  if (nz > kRowNZ) { v.gnz[id] = (uint8_t)255; return; }
-  int s = 0;
-  for (int i = 0; i < n; ++i)
-    if (g[i] != 0.0) { v.gidx[id * kRowNZ + s] = (int8_t)i; v.gval[id * kRowNZ + s] = g[i]; ++s; }
-  v.gnz[id] = (uint8_t)nz;
+  uint32_t w0 = 0, w1 = 0;
+  if (nz > kRowNZ) {
+    nz = 255;
+  } else {
+    int s = 0;
+    for (int i = 0; i < n; ++i)
+      if (g[i] != 0.0) {
+        v.gval[id * kRowNZ + s] = g[i];
+        if (s < 4) w0 |= (uint32_t)i << (8 * s); else w1 |= (uint32_t)i << (8 * (s - 4));
+        ++s;
+      }
+    for (; s < kRowNZ; ++s) v.gval[id * kRowNZ + s] = 0.0;
+  }
+  v.rowpk[id] = make_int4(v.knot[j], kind | (nz << 8), (int)w0, (int)w1);
 }
 
 cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
@@ -977,10 +1156,11 @@ cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
 
 cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st) {
   const Dims& d = h->dev.d;
-  const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx) * sizeof(double);
+  const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx + kQPRing) * sizeof(double);
   if (smem > 48 * 1024) return launch_qp(h, engine, l, st);
   if (d.nx <= 127) {
-    k_qp_sparse<<<d.B, 256, smem, st>>>(h->dev, engine, l);
+    if (d.nx <= 16 && d.nu <= 8 && d.nx % 2 == 0) k_qp_sparse<16, 8><<<d.B, 256, smem, st>>>(h->dev, engine, l);
+    else k_qp_sparse<0, 0><<<d.B, 256, smem, st>>>(h->dev, engine, l);
     h->launches++;
     return cudaGetLastError();
   }
@@ -1079,3 +1259,7 @@ cudaError_t launch_dr_arm(nrto_handle_s* h, cudaStream_t st) {
 }
 
 }  // namespace nrto
+
+extern "C" int nrto_debug_qp_clocks(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, nrto::g_qp_clk, sizeof(long long) * 64);
+}

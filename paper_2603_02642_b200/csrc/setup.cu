@@ -392,6 +392,7 @@ __global__ void k_riccati(Dev v, int eng) {
       double acc = A[r];
       for (int q = 0; q < nu; ++q) acc -= B[i * nu + q] * Kf[q * nx + c];
       F.Acl[bk * nx * nx + r] = acc;
+      F.AclT[bk * nx * nx + c * nx + i] = acc;
     }
     if (k >= 1) {                                   // P = Qt_k + A^T P A - Hux^T Kf
       __syncthreads();

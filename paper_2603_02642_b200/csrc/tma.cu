@@ -404,7 +404,12 @@ cudaError_t launch_relayout(nrto_handle_s* h, cudaStream_t st) {
 static int tma_stages(const Dims& d) {
   const TmaGeom G = tma_geom(d.nx, d.nup);
   const size_t fixed = tma_fixed_doubles(d.T, d.nx, d.nu);
-  const size_t cap = 225 * 1024 / sizeof(double);
+  // leave room for one k_qp_sparse CTA beside the pass CTA (overlapped QP)
+  const size_t qp = ((size_t)(d.T + 1) * d.nx + 8 * (size_t)d.nx * d.nx) * sizeof(double);
+  size_t capb = 225 * 1024;
+  if (228 * 1024 > qp + 2048 + 3 * G.stage * sizeof(double) + fixed * sizeof(double))
+    capb = std::min<size_t>(capb, 228 * 1024 - 2048 - qp);
+  const size_t cap = capb / sizeof(double);
   if (fixed >= cap) return 0;
   return (int)std::min<size_t>(kMaxStages, (cap - fixed) / G.stage);
 }
