@@ -208,6 +208,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     solver.profile(True)
     solver.profile_read()                      # clear
+    solver.pass_bytes()                        # clear the pass byte counter
     l0 = solver.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
@@ -219,6 +220,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     launches = solver.launches() - l0
     prof = solver.profile_read()
+    moved = solver.pass_bytes()                # algorithmic bytes of k_fa_tma in the timed steps
     solver.profile(False)
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_max = max_over_ranks(ms, device=dev)
@@ -257,15 +259,18 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     peak, peak_kind = load_peaks()
+    # roofline of k_fa_tma: algorithmic bytes = b_hat + b of every state-cone
+    # block, y^{l-1} of cones with s^{l-1} != 1, y^l where stored -- counted by the
+    # kernel itself (nrto_pass_bytes) -- over its event-timed device time in the steps
     pms, pn = prof["pass"]
-    bytes_per_launch = B * 8.0 * (2 * E + E_s + E_B)
-    achieved = bytes_per_launch / (pms / pn / 1000.0) / 1e9 if pn else None
+    bytes_per_launch = moved / pn if pn else None
+    achieved = moved / (pms / 1000.0) / 1e9 if pms else None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "pass_traffic.json")
     if os.path.exists(tf):
         try:
             tj = json.load(open(tf))
-            if tj.get("batch") == B:
+            if tj.get("batch") == B and tj.get("iters") == L:
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             pass
@@ -286,8 +291,8 @@ def run_ours(args, rank, world, local_rank):
         "cone_elements_per_s": value * E,
         "sl_iteration_wall_clock_ms": (e2e or {}).get("sl_iteration_wall_clock_ms"),
         "kernel_ms_per_step": kernel_ms,
-        "roofline": {"bound": "hbm", "kernel": "k_fa_tma: fused cone pass (S3 forward map + S4 SOC "
-                                                "norms + S5 state update + S7 predicted adjoint)",
+        "roofline": {"bound": "hbm", "kernel": "k_fa_tma: fused state-cone pass (S3 forward map + "
+                                                "S4 SOC norms + S5 state update)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_kind": peak_kind,

@@ -190,12 +190,13 @@ int64_t nrto_launch_count(nrto_handle h);
 
 /* Kernel classes timed by the optional CUDA-event profiler. */
 typedef enum {
-  NRTO_K_PASS = 0,     /* fused cone pass: S3 forward map + S4 projection + S5 state update */
-  NRTO_K_ADJOINT = 1,  /* S7 adjoint reduction                                             */
+  NRTO_K_PASS = 0,     /* fused state-cone pass: S3 forward map + S4 norms + S5 state update */
+  NRTO_K_ADJOINT = 1,  /* S7 adjoint reduction / correction list                           */
   NRTO_K_GAIN = 2,     /* S8 gain chain                                                    */
   NRTO_K_QP = 3,       /* S9 QP (+ dual update, residuals S6)                              */
-  NRTO_K_OTHER = 4,    /* DR residual reduction, resets, finish                            */
-  NRTO_K_COUNT = 5
+  NRTO_K_OTHER = 4,    /* projection decisions, DR residual reduction, resets, finish      */
+  NRTO_K_CTRL = 5,     /* control-cone pass (single-block cones)                           */
+  NRTO_K_COUNT = 6
 } nrto_kernel_class;
 
 /* enable != 0: every launch of a timed class is bracketed by CUDA events on

@@ -432,6 +432,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
         CK(timed_qp(NRTO_FULLADMM, l));
       } else {
         CK(timed(NRTO_K_PASS, v.fused == 2 ? launch_fa_tma : launch_fa_fused));
+        if (v.fused == 2) CK(timed(NRTO_K_CTRL, launch_fa_ctrl));
         if (overlap && l > 1) CK(cudaStreamWaitEvent(st, h->ev_qp, 0));
         CK(timed(NRTO_K_OTHER, launch_project));
         if (overlap) {

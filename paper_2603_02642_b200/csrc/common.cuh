@@ -202,6 +202,7 @@ int read_setup_error(cudaStream_t st);
 cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st);
 cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_relayout(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_fa_ctrl(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,

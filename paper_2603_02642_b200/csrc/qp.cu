@@ -433,7 +433,13 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kQPRing = 8;
+constexpr int kQPRing = 8;   // power of two
+#ifndef QP_MINB
+#define QP_MINB 5
+#endif
+#ifndef QP_THREADS
+#define QP_THREADS 256
+#endif
 
 __global__ void __launch_bounds__(256, 5) k_qp_lite(Dev v, int engine, int l) {
   extern __shared__ double sm[];
@@ -696,7 +702,7 @@ __device__ __forceinline__ int rec_idx(const int4& r, int s) {
 // bd_j = <grad_j, x_k> (x = dx~ for state rows, du~ for control rows), update
 // (p, z, y)_j, and (more) form the next iteration's rhs_p / w_j and scatter
 // w_j grad_j into S_k / U_k (FP64 RED.ADD).  first: only the rhs / scatter.
-constexpr int kRowBatch = 2;
+constexpr int kRowBatch = QP_THREADS >= 256 ? 2 : 4;
 template <bool FIRST, int U>
 __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int tid, int nt,
                                         const double* __restrict__ grad,
@@ -774,7 +780,7 @@ __device__ long long g_qp_clk[64];
 #define QP_CLK(ph) \
   do { if (b == 0 && tid == 0 && it_dbg < 2) g_qp_clk[it_dbg * 32 + (ph)] = clock64(); } while (0)
 
-// sum_{q < n} fa(q) fb(q) + acc.  NM > 0 (a multiple of 8, n <= NM): loads issued
+// sum_{q < n} fa(q) fb(q) + acc.  NM > 0 (n <= NM): loads issued
 // 8 at a time (predicated) so dependent latency is paid once per batch, not per
 // term; NM = 0: plain loop.
 template <int NM, class FA, class FB>
@@ -787,7 +793,7 @@ __device__ __forceinline__ double dotn(int n, FA fa, FB fb, double acc) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int q = q0 + u;
-        const bool ok = q < n;
+        const bool ok = q < NM && q < n;
         av[u] = ok ? fa(q) : 0.0;
         bv[u] = ok ? fb(q) : 0.0;
       }
@@ -824,12 +830,15 @@ __device__ __forceinline__ void qp_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// NXM, NUM > 0: the exact n_x, n_u, fixed at compile time (shape-specialised
+// instances for the benchmark shapes: every small loop fully unrolled, loads
+// issued together); 0: runtime sizes.
 template <int NXM, int NUM>
-__global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) {
+__global__ void __launch_bounds__(QP_THREADS, QP_MINB) k_qp_sparse(Dev v, int engine, int l) {
   extern __shared__ double sm[];
   __shared__ double red[32];
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, T = d.T, ng = d.ng;
+  const int nx = NXM > 0 ? NXM : d.nx, nu = NUM > 0 ? NUM : d.nu, T = d.T, ng = d.ng;
   const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   if (!v.active[b]) return;
   const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
@@ -860,8 +869,6 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
   double* sS = sm;                                    // [(T+1) nx]
   double* ring = sS + (T + 1) * nx;                   // [kQPRing][nx nx]
   uint64_t* qbar = reinterpret_cast<uint64_t*>(ring + kQPRing * nx * nx);   // [kQPRing]
-  int rslot = 0;                                      // recurrence ring position (warp 0)
-  uint32_t rph = 0;
   const int nn = nx * nx;
   const int nits = v.prm.qp_iters;
   int it_dbg = 0;
@@ -912,15 +919,19 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
         // s_k[i] = a_k[i] + <AclT_k row i, s_{k+1}>: AclT_k arrives by one bulk copy
         // per step into a kQPRing-slot ring (mbarrier), s_{k+1} by broadcast LDS.128
         const double* AT = F.AclT + (int64_t)b * T * nn;
+        // ring position = running copy count n (2T per QP iteration): slot n % R,
+        // parity (n / R) & 1 -- computed, not carried, to keep it out of local memory
+        const int n0 = it * 2 * T;
         if (tid == 0)
           for (int pf = 0; pf < kQPRing && pf < T; ++pf) {
-            const int sl = (rslot + pf) % kQPRing;
+            const int sl = (n0 + pf) & (kQPRing - 1);
             qp_expect_tx(&qbar[sl], nn * 8);
             qp_bulk(ring + sl * nn, AT + (int64_t)(T - 1 - pf) * nn, nn * 8, &qbar[sl]);
           }
         const int ic = tid < nx ? tid : 0;
         for (int k = T - 1; k >= 0; --k) {
-          qp_wait(&qbar[rslot], rph);
+          const int n = n0 + (T - 1 - k), rslot = n & (kQPRing - 1);
+          qp_wait(&qbar[rslot], (uint32_t)(n / kQPRing) & 1u);
           const double* Ar = ring + rslot * nn + ic * nx;
           const double* sn = sS + (k + 1) * nx;
           double c0 = sS[k * nx + ic], c1 = 0.0;
@@ -940,7 +951,6 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
             qp_expect_tx(&qbar[rslot], nn * 8);
             qp_bulk(ring + rslot * nn, AT + (int64_t)kn * nn, nn * 8, &qbar[rslot]);
           }
-          if (++rslot == kQPRing) { rslot = 0; rph ^= 1; }
         }
       } else {
       for (int pf = 0; pf < kQPRing; ++pf) {
@@ -993,9 +1003,10 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
       if constexpr (NXM > 0) {
         // dx_{k+1}[i] = e_k[i] + <Acl_k row i, dx_k>
         const double* AG = F.Acl + (int64_t)b * T * nn;
+        const int n0 = it * 2 * T + T;
         if (tid == 0)
           for (int pf = 0; pf < kQPRing && pf < T; ++pf) {
-            const int sl = (rslot + pf) % kQPRing;
+            const int sl = (n0 + pf) & (kQPRing - 1);
             qp_expect_tx(&qbar[sl], nn * 8);
             qp_bulk(ring + sl * nn, AG + (int64_t)pf * nn, nn * 8, &qbar[sl]);
           }
@@ -1003,7 +1014,8 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
         if (tid < nx) sS[tid] = 0.0;
         __syncwarp();
         for (int k = 0; k < T; ++k) {
-          qp_wait(&qbar[rslot], rph);
+          const int n = n0 + k, rslot = n & (kQPRing - 1);
+          qp_wait(&qbar[rslot], (uint32_t)(n / kQPRing) & 1u);
           const double* Ar = ring + rslot * nn + ic * nx;
           const double* xk = sS + k * nx;
           double c0 = sS[(k + 1) * nx + ic], c1 = 0.0;
@@ -1023,7 +1035,6 @@ __global__ void __launch_bounds__(256, 5) k_qp_sparse(Dev v, int engine, int l) 
             qp_expect_tx(&qbar[rslot], nn * 8);
             qp_bulk(ring + rslot * nn, AG + (int64_t)kn * nn, nn * 8, &qbar[rslot]);
           }
-          if (++rslot == kQPRing) { rslot = 0; rph ^= 1; }
         }
       } else {
       for (int pf = 0; pf < kQPRing; ++pf) {
@@ -1159,8 +1170,9 @@ cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st)
   const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx + kQPRing) * sizeof(double);
   if (smem > 48 * 1024) return launch_qp(h, engine, l, st);
   if (d.nx <= 127) {
-    if (d.nx <= 16 && d.nu <= 8 && d.nx % 2 == 0) k_qp_sparse<16, 8><<<d.B, 256, smem, st>>>(h->dev, engine, l);
-    else k_qp_sparse<0, 0><<<d.B, 256, smem, st>>>(h->dev, engine, l);
+    if (d.nx == 14 && d.nu == 7) k_qp_sparse<14, 7><<<d.B, QP_THREADS, smem, st>>>(h->dev, engine, l);
+    else if (d.nx == 12 && d.nu == 4) k_qp_sparse<12, 4><<<d.B, QP_THREADS, smem, st>>>(h->dev, engine, l);
+    else k_qp_sparse<0, 0><<<d.B, QP_THREADS, smem, st>>>(h->dev, engine, l);
     h->launches++;
     return cudaGetLastError();
   }

@@ -451,6 +451,11 @@ cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st) {
     else e = launch_tma_k<7>(h, nti, nks, st);
     if (e != cudaSuccess) return e;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fa_ctrl(nrto_handle_s* h, cudaStream_t st) {
+  const Dims& d = h->dev.d;
   if (h->dev.nctrl > 0) {
     dim3 grid(d.B, (d.T + 15) / 16);
     k_fa_ctrl<<<grid, 512, 0, st>>>(h->dev);

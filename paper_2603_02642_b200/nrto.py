@@ -177,7 +177,7 @@ def nrto_refresh(handle, data: dict, stream=None, memory=NRTO_MEM_DEVICE):
 
 
 NRTO_K_PASS, NRTO_K_ADJOINT, NRTO_K_GAIN, NRTO_K_QP, NRTO_K_OTHER = 0, 1, 2, 3, 4
-KERNEL_CLASSES = ("pass", "adjoint", "gain", "qp", "other")
+KERNEL_CLASSES = ("pass", "adjoint", "gain", "qp", "other", "ctrl")
 
 
 def nrto_profile_enable(handle, enable=True):
