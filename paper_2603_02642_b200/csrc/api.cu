@@ -216,6 +216,11 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
     }
   }
   v.Est = est; v.EBst = ebst;
+  std::vector<int32_t> ktile0(T + 1, nstate_tiles);
+  if (use_tma)
+    for (int k = T; k >= 0; --k)
+      for (int t = 0; t < nstate_tiles; ++t)
+        if (tiles[t * 12 + 1] > k) { ktile0[k] = t; break; }
 
   const int64_t B = d.B;
   int32_t *dknot, *dkind, *dkptr, *dkcone, *dsptr, *dsrow, *dcptr, *dcrow;
@@ -250,7 +255,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   v.tiles = dtiles; v.witems = dwitems;
   AL(v.Zpart, (v.fused == 1 ? B * nsplit : 1) * T * nu * nx); AL(v.Zc, B * T * nu * nx);
   if (v.fused == 2) {
-    AL(v.ttb, ttb.size()); AL(v.bhat_t, B * est); AL(v.Bd_t, B * ebst);
+    AL(v.ttb, ttb.size()); AL(v.bhat_t, B * est); AL(v.Bd_t, B * ebst); AL(v.ktile0, T + 1);
     AL(v.G, B * T * nu * nu); AL(v.G0, B * T * nu * nu); AL(v.dG, B * T * nu * nu);
     AL(v.H, B * T * nu * nx); AL(v.H0, B * T * nu * nx); AL(v.dH, B * T * nu * nx);
   }
@@ -272,7 +277,10 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   hup(dsptr, sptr.data(), (T + 2) * 4); hup(dsrow, srow.data(), srow.size() * 4);
   hup(dcptr, cptr.data(), (T + 1) * 4); hup(dcrow, crow.data(), crow.size() * 4);
   hup(dtiles, tiles.data(), tiles.size() * 4); hup(dwitems, witems.data(), witems.size() * 4);
-  if (v.fused == 2) hup(v.ttb, ttb.data(), ttb.size() * 4);
+  if (v.fused == 2) {
+    hup(v.ttb, ttb.data(), ttb.size() * 4);
+    hup(v.ktile0, ktile0.data(), (T + 1) * 4);
+  }
   if (ce != cudaSuccess) { free_all(h); delete h; return cuda_fail(ce, "nrto_setup shape upload"); }
   nrto_err re = nrto_refresh(h, data, stream);
   if (re != NRTO_OK) { free_all(h); delete h; return re; }
@@ -393,7 +401,15 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     // staged variant (Acl in shared memory, 1024 threads) is used in order.
     int nsm = 148;
     { int dev = 0; if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); }
+#ifndef QP_OVERLAP_CTAS_PER_SM
+#define QP_OVERLAP_CTAS_PER_SM 2
+#endif
+#ifdef NRTO_NOOVERLAP
+    const bool overlap = false;
+#else
     const bool overlap = v.fused >= 1 && prm.fixed_iters && d.B >= nsm;
+#endif
+    const bool wide = v.fused >= 1 && d.B >= nsm;   // enough instances for the light QP
     if (overlap && !h->aux) {
       // the cone-pass chain gets the highest stream priority so that SM slots freed
       // by finishing pass CTAs go to pass CTAs; QP CTAs fill the leftover room
@@ -438,7 +454,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
         if (overlap) {
           CK(cudaEventRecord(h->ev_proj, st));
           CK(cudaStreamWaitEvent(st2, h->ev_proj, 0));
-          CK(timed2(st2, NRTO_K_QP, [&](cudaStream_t s2) { return launch_qp_lite(h, NRTO_FULLADMM, l, s2); }));
+          CK(timed2(st2, NRTO_K_QP, [&](cudaStream_t s2) { return launch_qp_lite(h, NRTO_FULLADMM, l, s2, QP_OVERLAP_CTAS_PER_SM * nsm); }));
           CK(cudaEventRecord(h->ev_qp, st2));
         }
         CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
@@ -446,7 +462,10 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
           return launch_zlist(hh, w.Y, w.clist, w.cw, nullptr, w.ncorr, 0, w.active, w.Zc, s2, w.ylazy,
                               w.fused == 2 ? 1 : 0, w.dG, w.dH); }));
         CK(timed(NRTO_K_GAIN, launch_fa_gain));
-        if (!overlap) CK(timed_qp(NRTO_FULLADMM, l));
+        if (!overlap) {
+          if (wide) CK(timed2(st, NRTO_K_QP, [&](cudaStream_t s2) { return launch_qp_lite(h, NRTO_FULLADMM, l, s2); }));
+          else CK(timed_qp(NRTO_FULLADMM, l));
+        }
       }
       if (!prm.fixed_iters && l % prm.check_every == 0 && l < prm.max_iter) {
         const int c = poll_active(h, dcount, 0, st, &ce);

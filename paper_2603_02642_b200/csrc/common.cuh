@@ -96,6 +96,7 @@ struct Dev {
   int32_t* ttb;            // [nstate_tiles][2] tile base (b_hat_t, Bd_t) within an instance
   int64_t Est, EBst;       // per-instance sizes of b_hat_t / Bd_t
   double* bhat_t;          // [B][Est]
+  int32_t* ktile0;         // [T+1] first state tile with knot > k (tiles ascend in knot)
   double* Bd_t;            // [B][EBst]
   const int32_t* tiles;    // [ntiles][12] kind, knot, nc, klo, cone[8]
   const int32_t* witems;   // [nwitems][4] b, t0, t1, split index
@@ -202,6 +203,7 @@ int read_setup_error(cudaStream_t st);
 cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st);
 cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_relayout(nrto_handle_s* h, cudaStream_t st);
+cudaError_t launch_gram_tiles(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_ctrl(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
@@ -213,6 +215,6 @@ bool tma_supported(const Dims& d);
 cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_project(nrto_handle_s* h, cudaStream_t st);
-cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st);
+cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid = 0);
 
 }  // namespace nrto

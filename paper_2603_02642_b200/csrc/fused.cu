@@ -813,14 +813,15 @@ cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st) {
   dim3 grid(d.B, (d.T + 15) / 16);
   k_lam_mma<<<grid, 512, 0, st>>>(v);
   h->launches++;
-  // Zb_k = sum_j b_{j,k} b_hat_{j,k}^T : the list adjoint with y = b_hat
-  cudaError_t e = launch_zlist(h, v.bhat, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, v.Zb, st);
-  if (e != cudaSuccess || v.fused != 2) return e;
-  e = launch_relayout(h, st);
+  if (v.fused != 2) {
+    // Zb_k = sum_j b_{j,k} b_hat_{j,k}^T : the list adjoint with y = b_hat
+    return launch_zlist(h, v.bhat, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, v.Zb, st);
+  }
+  // TMA path: tile layout, then G0 = sum b b^T, H0 = sum b b_hat^T over state cones
+  // from it; control rows have b_hat = 0, so Zb = H0.
+  cudaError_t e = launch_relayout(h, st);
   if (e != cudaSuccess) return e;
-  // G0_k = sum_{state j} b b^T, H0_k = sum_{state j} b b_hat^T (TMA path predicted adjoint)
-  return launch_zlist(h, nullptr, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, nullptr, st,
-                      0, 2, v.G0, v.H0);
+  return launch_gram_tiles(h, st);
 }
 
 static int fused_variant(const Dims& d, int* nti, int* nks) {

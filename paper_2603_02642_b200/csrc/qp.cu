@@ -834,12 +834,11 @@ __device__ __forceinline__ void qp_wait(uint64_t* bar, uint32_t parity) {
 // instances for the benchmark shapes: every small loop fully unrolled, loads
 // issued together); 0: runtime sizes.
 template <int NXM, int NUM>
-__global__ void __launch_bounds__(QP_THREADS, QP_MINB) k_qp_sparse(Dev v, int engine, int l) {
-  extern __shared__ double sm[];
-  __shared__ double red[32];
+__device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int b, double* sm,
+                                            double* red) {
   const Dims d = v.d;
   const int nx = NXM > 0 ? NXM : d.nx, nu = NUM > 0 ? NUM : d.nu, T = d.T, ng = d.ng;
-  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
   if (!v.active[b]) return;
   const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
   const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
@@ -1128,6 +1127,19 @@ __global__ void __launch_bounds__(QP_THREADS, QP_MINB) k_qp_sparse(Dev v, int en
   }
 }
 
+// One CTA per instance (grid = B, all resident: in-order schedule) or a
+// persistent grid looping over instances (overlapped schedule: one QP CTA per SM
+// beside the cone pass, so the QP never holds more than that share of the SMs).
+template <int NXM, int NUM>
+__global__ void __launch_bounds__(QP_THREADS, QP_MINB) k_qp_sparse(Dev v, int engine, int l) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  for (int b = blockIdx.x; b < v.d.B; b += gridDim.x) {
+    qp_instance<NXM, NUM>(v, engine, l, b, sm, red);
+    __syncthreads();
+  }
+}
+
 // Setup: compressed rows of the constraint gradients (state rows: n_x entries,
 // control rows: the first n_u) as packed records {knot, kind | nz << 8, idx0..3,
 // idx4..7} + values gval[row][8]; nnz > kRowNZ keeps the dense row (nz = 255).
@@ -1165,14 +1177,15 @@ cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st) {
+cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid) {
   const Dims& d = h->dev.d;
   const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx + kQPRing) * sizeof(double);
   if (smem > 48 * 1024) return launch_qp(h, engine, l, st);
   if (d.nx <= 127) {
-    if (d.nx == 14 && d.nu == 7) k_qp_sparse<14, 7><<<d.B, QP_THREADS, smem, st>>>(h->dev, engine, l);
-    else if (d.nx == 12 && d.nu == 4) k_qp_sparse<12, 4><<<d.B, QP_THREADS, smem, st>>>(h->dev, engine, l);
-    else k_qp_sparse<0, 0><<<d.B, QP_THREADS, smem, st>>>(h->dev, engine, l);
+    const int g = (grid > 0 && grid < d.B) ? grid : d.B;
+    if (d.nx == 14 && d.nu == 7) k_qp_sparse<14, 7><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
+    else if (d.nx == 12 && d.nu == 4) k_qp_sparse<12, 4><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
+    else k_qp_sparse<0, 0><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
     h->launches++;
     return cudaGetLastError();
   }

@@ -23,6 +23,7 @@ __device__ __forceinline__ void dmma2(double (&c)[2], double a, double b) {
       : "+d"(c[0]), "+d"(c[1])
       : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) { dmma2(c, a, b); }
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -398,6 +399,70 @@ cudaError_t launch_relayout(nrto_handle_s* h, cudaStream_t st) {
     k_relayout<<<dim3(v.nstate_tiles, v.d.B), 256, 0, st>>>(v);
     h->launches++;
   }
+  return cudaGetLastError();
+}
+
+// G0_k = sum_{state c, K_c > k} b_{c,k} b_{c,k}^T, H0_k = sum b_{c,k} b_hat_{c,k}^T (= Zb_k,
+// control rows have b_hat = 0), one warp per (instance, k), from the tile layout: the
+// 8 cones of a tile at block k are one contiguous slab; DMMA over the cone index.
+template <int NTI>
+__global__ void __launch_bounds__(256) k_gram_tiles(Dev v) {
+  const Dims d = v.d;
+  const int nx = d.nx, nu = d.nu, nup = d.nup, T = d.T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + warp;
+  if (gw >= (int64_t)d.B * T) return;
+  const int b = (int)(gw / T), k = (int)(gw % T);
+  const double* bht = v.bhat_t + (int64_t)b * v.Est;
+  const double* bdt = v.Bd_t + (int64_t)b * v.EBst;
+  double gz[2] = {0.0, 0.0}, hz[NTI][2];
+#pragma unroll
+  for (int nt = 0; nt < NTI; ++nt) hz[nt][0] = hz[nt][1] = 0.0;
+  for (int t = v.ktile0[k]; t < v.nstate_tiles; ++t) {
+    const int nc = v.tiles[(int64_t)t * kTI + 2];
+    const double* sb = bdt + v.ttb[2 * t + 1] + (int64_t)k * nc * nup;
+    const double* sh = bht + v.ttb[2 * t] + (int64_t)k * nc * nx;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int c = q + 4 * ks;
+      const bool cv = c < nc;
+      const double bcg = (cv && g < nu) ? sb[c * nup + g] : 0.0;
+      dmma(gz, bcg, bcg);
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) {
+        const int i = g + 8 * nt;
+        dmma(hz[nt], bcg, (cv && i < nx) ? sh[c * nx + i] : 0.0);
+      }
+    }
+  }
+  if (g < nu) {
+    const int64_t bk = (int64_t)b * T + k;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int m2 = 2 * q + r;
+      if (m2 < nu) v.G0[bk * nu * nu + g * nu + m2] = gz[r];
+    }
+#pragma unroll
+    for (int nt = 0; nt < NTI; ++nt)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int i = 2 * q + r + 8 * nt;
+        if (i < nx) {
+          v.H0[bk * nu * nx + g * nx + i] = hz[nt][r];
+          v.Zb[bk * nu * nx + g * nx + i] = hz[nt][r];
+        }
+      }
+  }
+}
+
+cudaError_t launch_gram_tiles(nrto_handle_s* h, cudaStream_t st) {
+  const Dev& v = h->dev;
+  const int64_t nw = (int64_t)v.d.B * v.d.T;
+  if (nw == 0) return cudaSuccess;
+  if (v.d.nx <= 8) k_gram_tiles<1><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(v);
+  else k_gram_tiles<2><<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(v);
+  h->launches++;
   return cudaGetLastError();
 }
 
