@@ -81,8 +81,21 @@ __host__ __device__ inline TmaGeom tma_geom(int nx, int nup) {
   g.stage = g.SY + g.SB;
   return g;
 }
+// Per-tile metadata staged by the producer in shared memory (kMetaT-slot ring,
+// tile t -> slot t % kMetaT), visible to the consumers once they pass the
+// tile's first stage barrier (the producer's arrive releases it).
+constexpr int kMetaT = 16;
+struct TileMeta {
+  int K, nc;
+  int cone[8];
+  int wy[8];
+  long long off[8];
+  double omsp[8];
+  double pad[7];
+};
+static_assert(sizeof(TileMeta) == 256, "TileMeta is 32 doubles");
 __host__ __device__ inline size_t tma_fixed_doubles(int T, int nx, int nu) {
-  return kHdr + kRingT * 16 * 8 + (((size_t)T * nx * nu + 1) & ~(size_t)1);
+  return kHdr + kRingT * 16 * 8 + kMetaT * 32 + (((size_t)T * nx * nu + 1) & ~(size_t)1);
 }
 
 // Fused state-cone pass (norm-only form).  Per cone block k:
@@ -92,20 +105,24 @@ __host__ __device__ inline size_t tma_fixed_doubles(int T, int nx, int nu) {
 // b_hat and b reach shared memory by TMA bulk copies (producer warp, nst-stage
 // mbarrier ring); y^{l-1} of the few cones with s^{l-1} != 1 is loaded by the
 // consumers straight from global memory, issued before the stage wait.
-template <int NTI, int NKS, int KK>
+// NXE, NUE > 0: exact n_x, n_u fixed at compile time (benchmark shapes): every
+// bounds predicate of the inner block folds away.
+template <int NTI, int NKS, int KK, int NXE, int NUE>
 __global__ void __launch_bounds__(544, 1)
 k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems, int nst) {
   extern __shared__ __align__(128) double sm[];
   constexpr int NW = 16;
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, nup = d.nup, T = d.T;
+  const int nx = NXE > 0 ? NXE : d.nx, nu = NUE > 0 ? NUE : d.nu, T = d.T;
+  const int nup = NUE > 0 ? (NUE + (NUE & 1)) : d.nup;
   const TmaGeom G = tma_geom(nx, nup);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + kMaxStages;
   int* cnt = reinterpret_cast<int*>(empty + kMaxStages);
   int* tag = cnt + kRingT;
   double* ring = sm + kHdr;                                // [kRingT][NW][8]
-  double* Ds = ring + kRingT * NW * 8;                     // [T][nx][nu]
+  TileMeta* meta = reinterpret_cast<TileMeta*>(ring + kRingT * NW * 8);   // [kMetaT]
+  double* Ds = ring + kRingT * NW * 8 + kMetaT * 32;       // [T][nx][nu]
   double* stg = sm + tma_fixed_doubles(T, nx, nu);         // stages
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
@@ -134,25 +151,37 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
     uint32_t ph = 0;
     unsigned long long moved = 0;
     const uint64_t pol = policy_evict_first();
-    bool ynext = false, wnext = false;
-    auto cone_flags = [&](int j, bool& yr, bool& yw) {
-      const double sp = v.s[bg + j];
-      yr = v.iter > 1 && sp != 1.0;
-      yw = !v.ylazy || shat_of(v, sp) != 1.0;
+    // per-lane prefetch (one tile ahead) of the cone id, offset, s^{l-1}
+    int jn = 0, Kn = 0, ncn = 0;
+    long long offn = 0;
+    double sn = 1.0;
+    auto fetch = [&](int t) {
+      const int* tl = tiles + (int64_t)t * kTI;
+      Kn = tl[1]; ncn = tl[2];
+      if (lane < ncn) { jn = tl[4 + lane]; offn = v.off[jn]; sn = v.s[bg + jn]; }
     };
-    if (t0 < t1 && lane < tiles[(int64_t)t0 * kTI + 2])
-      cone_flags(tiles[(int64_t)t0 * kTI + 4 + lane], ynext, wnext);
+    if (t0 < t1) fetch(t0);
     const double* __restrict__ bht = v.bhat_t + (int64_t)b * v.Est;
     const double* __restrict__ bdt = v.Bd_t + (int64_t)b * v.EBst;
     for (int t = t0; t < t1; ++t) {
-      const int* tl = tiles + (int64_t)t * kTI;
-      const int K = tl[1], nc = tl[2];
+      const int K = Kn, nc = ncn, jc = jn;
+      const long long offc = offn;
+      const double sc = sn;
       const int64_t tb0 = v.ttb[2 * t], tb1 = v.ttb[2 * t + 1];
-      const bool yrd = ynext, ywr = wnext;
-      if (t + 1 < t1 && lane < tiles[(int64_t)(t + 1) * kTI + 2])   // flags of the next tile
-        cone_flags(tiles[(int64_t)(t + 1) * kTI + 4 + lane], ynext, wnext);
-      const uint32_t nyr = __popc(__ballot_sync(0xffffffffu, lane < nc && yrd));
-      const uint32_t nyw = __popc(__ballot_sync(0xffffffffu, lane < nc && ywr));
+      if (t + 1 < t1) fetch(t + 1);
+      const bool yrd = lane < nc && v.iter > 1 && sc != 1.0;
+      const bool ywr = lane < nc && (!v.ylazy || shat_of(v, sc) != 1.0);
+      TileMeta* M = meta + ((t - t0) & (kMetaT - 1));
+      if (lane < 8) {
+        M->cone[lane] = jc;
+        M->off[lane] = offc;
+        M->omsp[lane] = yrd ? 1.0 - sc : 0.0;
+        M->wy[lane] = ywr;
+      }
+      if (lane == 0) { M->K = K; M->nc = nc; }
+      __syncwarp();
+      const uint32_t nyr = __popc(__ballot_sync(0xffffffffu, yrd));
+      const uint32_t nyw = __popc(__ballot_sync(0xffffffffu, ywr));
       for (int kc = 0; kc <= K; kc += 16) {
         const int nb = min(16, K + 1 - kc), nbB = max(0, min(16, K - kc));
         if (lane == 0) {
@@ -177,15 +206,15 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
   int st = 0;
   uint32_t ph = 0;
   for (int t = t0; t < t1; ++t) {
-    const int* tl = tiles + (int64_t)t * kTI;
-    const int K = tl[1], nc = tl[2];
     const int lt = t - t0, slot = lt % kRingT;
+    mbar_wait(&full[st], ph);                     // first stage of the tile: meta visible
+    const TileMeta* M = meta + (lt & (kMetaT - 1));
+    const int K = M->K, nc = M->nc;
     const bool gv = g < nc;
-    const int cg = gv ? tl[4 + g] : 0;
-    const int64_t offg = gv ? v.off[cg] : 0;
-    const double sg = gv ? v.s[bg + cg] : 1.0;
-    const double omsp = (gv && v.iter > 1) ? 1.0 - sg : 0.0;   // != 0 <=> y_old is read
-    const bool wy = gv && (!v.ylazy || shat_of(v, sg) != 1.0);  // store y^l
+    const int64_t offg = gv ? M->off[g] : 0;
+    const double omsp = gv ? M->omsp[g] : 0.0;    // != 0 <=> y_old is read
+    const bool wy = gv && M->wy[g];               // store y^l
+    const bool hist = __any_sync(0xffffffffu, omsp != 0.0);     // any y_old in this tile
     double nrm = 0.0;
 #pragma unroll
     for (int kk = 0; kk < KK; ++kk) {
@@ -198,10 +227,10 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       for (int nt = 0; nt < NTI; ++nt) {
         const int i0 = 2 * q + 8 * nt;
         yo[nt] = make_double2(0.0, 0.0);
-        if (act && omsp != 0.0 && i0 < nx)
+        if (hist && act && omsp != 0.0 && i0 < nx)
           yo[nt] = __ldcs(reinterpret_cast<const double2*>(Y + offg + (int64_t)k * nx + i0));
       }
-      mbar_wait(&full[st], ph);
+      if (kk > 0) mbar_wait(&full[st], ph);
       const double* sH = stg + (size_t)st * G.stage;
       const double* sB = sH + G.SY;
       if (act) {
@@ -212,8 +241,13 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
           c[nt][0] = 0.0; c[nt][1] = 0.0;
           if (gv && i0 < nx) {
             const double2 bh = *reinterpret_cast<const double2*>(sH + (warp * nc + g) * nx + i0);
-            c[nt][0] = bh.x + omsp * yo[nt].x;
-            c[nt][1] = bh.y + omsp * yo[nt].y;
+            if (hist) {
+              c[nt][0] = bh.x + omsp * yo[nt].x;
+              c[nt][1] = bh.y + omsp * yo[nt].y;
+            } else {
+              c[nt][0] = bh.x;
+              c[nt][1] = bh.y;
+            }
           }
         }
         if (k < K) {
@@ -260,7 +294,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       if (lane < nc) {
         double n2 = 0.0;
         for (int w = 0; w < NW; ++w) n2 += ring[(slot * NW + w) * 8 + lane];
-        v.nrm2[bg + tl[4 + lane]] = n2;     // projection decided by k_project
+        v.nrm2[bg + M->cone[lane]] = n2;    // projection decided by k_project
       }
       __syncwarp();
       if (lane == 0) {
@@ -488,10 +522,10 @@ bool tma_supported(const Dims& d) {
   return (d.nx % 2 == 0) && d.nx <= 16 && d.nu <= 8 && d.T <= 111 && tma_stages(d) >= 3;
 }
 
-template <int NTI, int NKS, int KK>
+template <int NTI, int NKS, int KK, int NXE = 0, int NUE = 0>
 static cudaError_t launch_tma_t(nrto_handle_s* h, cudaStream_t st) {
   const size_t smem = tma_smem_bytes(h->dev.d);
-  auto kfn = k_fa_tma<NTI, NKS, KK>;
+  auto kfn = k_fa_tma<NTI, NKS, KK, NXE, NUE>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kfn<<<h->dev.nwitems, 544, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems, tma_stages(h->dev.d));
   h->launches++;
@@ -511,7 +545,9 @@ cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st) {
   const int nti = (d.nx + 7) / 8, nks = (d.nu + 3) / 4;
   cudaError_t e = cudaSuccess;
   if (h->dev.nwitems > 0) {
-    if (d.T < 32) e = launch_tma_k<2>(h, nti, nks, st);
+    if (d.nx == 14 && d.nu == 7 && d.T >= 64) e = launch_tma_t<2, 2, 7, 14, 7>(h, st);
+    else if (d.nx == 12 && d.nu == 4 && d.T >= 32 && d.T < 64) e = launch_tma_t<2, 1, 4, 12, 4>(h, st);
+    else if (d.T < 32) e = launch_tma_k<2>(h, nti, nks, st);
     else if (d.T < 64) e = launch_tma_k<4>(h, nti, nks, st);
     else e = launch_tma_k<7>(h, nti, nks, st);
     if (e != cudaSuccess) return e;
