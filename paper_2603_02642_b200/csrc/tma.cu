@@ -216,20 +216,27 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
     const bool wy = gv && M->wy[g];               // store y^l
     const bool hist = __any_sync(0xffffffffu, omsp != 0.0);     // any y_old in this tile
     double nrm = 0.0;
+    // y_old of history cones (s^{l-1} != 1) comes from global memory; each
+    // chunk's loads are issued one chunk ahead so their latency overlaps the
+    // previous chunk's work
+    double2 yo[NTI], yn[NTI];
+    auto load_y = [&](double2 (&dst)[NTI], int kb) {
+#pragma unroll
+      for (int nt = 0; nt < NTI; ++nt) {
+        const int i0 = 2 * q + 8 * nt;
+        dst[nt] = make_double2(0.0, 0.0);
+        if (kb <= K && omsp != 0.0 && i0 < nx)
+          dst[nt] = __ldcs(reinterpret_cast<const double2*>(Y + offg + (int64_t)kb * nx + i0));
+      }
+    };
+    if (hist) load_y(yo, warp);
 #pragma unroll
     for (int kk = 0; kk < KK; ++kk) {
       const int kc = NW * kk;
       if (kc > K) break;
       const int k = kc + warp;
       const bool act = k <= K;
-      double2 yo[NTI];
-#pragma unroll
-      for (int nt = 0; nt < NTI; ++nt) {
-        const int i0 = 2 * q + 8 * nt;
-        yo[nt] = make_double2(0.0, 0.0);
-        if (hist && act && omsp != 0.0 && i0 < nx)
-          yo[nt] = __ldcs(reinterpret_cast<const double2*>(Y + offg + (int64_t)k * nx + i0));
-      }
+      if (hist && kc + NW <= K) load_y(yn, k + NW);
       if (kk > 0) mbar_wait(&full[st], ph);
       const double* sH = stg + (size_t)st * G.stage;
       const double* sB = sH + G.SY;
@@ -275,6 +282,10 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
       if (++st == nst) { st = 0; ph ^= 1; }
+      if (hist) {
+#pragma unroll
+        for (int nt = 0; nt < NTI; ++nt) yo[nt] = yn[nt];
+      }
     }
     // ---- norm partials -> ring slot; last consumer warp publishes the tile's norms
     nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
