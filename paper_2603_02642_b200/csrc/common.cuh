@@ -112,6 +112,7 @@ struct Dev {
 struct nrto_prof_rec { int cls; cudaEvent_t a, b; };
 
 struct nrto_handle_s {
+  int tma_margin = 0;      // k_fa_tma launch mode: 1 = finish margins (||C^L b + b_hat||)
   nrto::Dev dev;
   int64_t launches = 0;
   int dr_fresh = 1;

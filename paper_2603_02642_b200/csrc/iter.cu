@@ -427,7 +427,7 @@ __global__ void k_dr_reduce(Dev v) {
 // lam_nu^L = (1 - s) y^L + (C^L - C^{L-1}) b  ( = lam^{L-1} + a(k^L) - nu^L ).
 // Both engines: margin_cone = p~ - ||C^L b + b_hat||.
 __global__ void k_finish_cones(Dev v, int engine, double* nu_out, double* lam_out,
-                               double* mc_out) {
+                               double* mc_out, int state_norms) {
   const Dims d = v.d;
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= (int64_t)d.B * d.ng) return;
@@ -442,6 +442,13 @@ __global__ void k_finish_cones(Dev v, int engine, double* nu_out, double* lam_ou
   const double* Cc = v.Ccur + (int64_t)b * d.T * nx * nu;
   const double* Cp = v.Cprev + (int64_t)b * d.T * nx * nu;
   const double s = v.s[ij];
+  // state_norms: ||C^L b + b_hat||^2 of state cones already in nrm2 (k_fa_tma margin mode)
+  const bool pre = state_norms && g.kind == 0;
+  const bool outs = engine == NRTO_FULLADMM && (nu_out || lam_out);
+  if (pre && !outs) {
+    if (lane == 0 && mc_out) mc_out[ij] = v.pt[ij] - sqrt(v.nrm2[ij]);
+    return;
+  }
   double n2 = 0.0;
   for (int e = lane; e < g.L; e += 32) {
     const int kb = e / nx, i = e - kb * nx;
@@ -452,13 +459,14 @@ __global__ void k_finish_cones(Dev v, int engine, double* nu_out, double* lam_ou
       for (int m = 0; m < nu; ++m) { a += Cc[r + m] * br[m]; dlt += (Cc[r + m] - Cp[r + m]) * br[m]; }
     }
     n2 += a * a;
-    if (engine == NRTO_FULLADMM) {
+    if (outs) {
       const double y = Y[e];
       if (nu_out) nu_out[(int64_t)b * d.E + g.off + e] = s * y;
       if (lam_out) lam_out[(int64_t)b * d.E + g.off + e] = (1.0 - s) * y + dlt;
     }
   }
   n2 = warp_sum(n2);
+  if (pre) n2 = v.nrm2[ij];
   if (lane == 0 && mc_out) mc_out[ij] = v.pt[ij] - sqrt(n2);
 }
 
@@ -609,9 +617,17 @@ cudaError_t launch_dr_reduce(nrto_handle_s* h, cudaStream_t st) {
 cudaError_t launch_finish(nrto_handle_s* h, int engine, const nrto_out* o, cudaStream_t st) {
   Dev& v = h->dev;
   const Dims& d = v.d;
+  int pre = 0;
+  if (v.fused == 2 && o->margin_cone && v.nwitems > 0) {   // state-cone margins by the TMA pass
+    h->tma_margin = 1;
+    cudaError_t e = launch_fa_tma(h, st);
+    h->tma_margin = 0;
+    if (e != cudaSuccess) return e;
+    pre = 1;
+  }
   if ((int64_t)d.B * d.ng > 0) {
     k_finish_cones<<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(
-        v, engine, o->nu, o->lam_nu, o->margin_cone);
+        v, engine, o->nu, o->lam_nu, o->margin_cone, pre);
     h->launches++;
   }
   k_finish_inst<<<d.B, 128, (d.T + 1) * d.nx * sizeof(double), st>>>(v, o->margin_lin,

@@ -109,7 +109,8 @@ __host__ __device__ inline size_t tma_fixed_doubles(int T, int nx, int nu) {
 // bounds predicate of the inner block folds away.
 template <int NTI, int NKS, int KK, int NXE, int NUE>
 __global__ void __launch_bounds__(544, 1)
-k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems, int nst) {
+k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems, int nst,
+         int margin) {
   extern __shared__ __align__(128) double sm[];
   constexpr int NW = 16;
   const Dims d = v.d;
@@ -128,11 +129,12 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
   const int g = lane >> 2, q = lane & 3;
   const int b = witems[4 * blockIdx.x], t0 = witems[4 * blockIdx.x + 1];
   const int t1 = witems[4 * blockIdx.x + 2];
-  if (!v.active[b]) return;
+  if (!margin && !v.active[b]) return;
   double* __restrict__ Y = v.Y + (int64_t)b * d.E;
   const int64_t bg = (int64_t)b * d.ng;
   {
-    const double* Dg = v.D + (int64_t)b * T * nx * nu;
+    // margin mode (finish): ||C^L_k b + b_hat|| of every state cone, no history, no store
+    const double* Dg = (margin ? v.Ccur : v.D) + (int64_t)b * T * nx * nu;
     for (int r = threadIdx.x; r < T * nx * nu; r += blockDim.x) Ds[r] = Dg[r];
   }
   if (threadIdx.x == 0) {
@@ -169,8 +171,8 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       const double sc = sn;
       const int64_t tb0 = v.ttb[2 * t], tb1 = v.ttb[2 * t + 1];
       if (t + 1 < t1) fetch(t + 1);
-      const bool yrd = lane < nc && v.iter > 1 && sc != 1.0;
-      const bool ywr = lane < nc && (!v.ylazy || shat_of(v, sc) != 1.0);
+      const bool yrd = !margin && lane < nc && v.iter > 1 && sc != 1.0;
+      const bool ywr = !margin && lane < nc && (!v.ylazy || shat_of(v, sc) != 1.0);
       TileMeta* M = meta + ((t - t0) & (kMetaT - 1));
       if (lane < 8) {
         M->cone[lane] = jc;
@@ -199,7 +201,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
         if (++st == nst) { st = 0; ph ^= 1; }
       }
     }
-    if (lane == 0 && v.pass_bytes) atomicAdd(v.pass_bytes, moved);
+    if (lane == 0 && v.pass_bytes && !margin) atomicAdd(v.pass_bytes, moved);
     return;
   }
   // ------------------------------------------------------------------ consumers
@@ -538,7 +540,8 @@ static cudaError_t launch_tma_t(nrto_handle_s* h, cudaStream_t st) {
   const size_t smem = tma_smem_bytes(h->dev.d);
   auto kfn = k_fa_tma<NTI, NKS, KK, NXE, NUE>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kfn<<<h->dev.nwitems, 544, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems, tma_stages(h->dev.d));
+  kfn<<<h->dev.nwitems, 544, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems, tma_stages(h->dev.d),
+                                         h->tma_margin);
   h->launches++;
   return cudaGetLastError();
 }
