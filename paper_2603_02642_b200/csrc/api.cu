@@ -237,7 +237,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   v.A = A; v.Bm = Bm; v.grad = grad; v.g0 = g0; v.Psi = Psi; v.tau = tau; v.W = W; v.Ru = Ru;
   v.uhat = uhat; v.rtrust = rtrust;
   AL(v.bhat, B * d.E); AL(v.Bd, B * d.EB); AL(v.Zb, B * T * nu * nx); AL(v.Lam, B * T * nu * nu);
-  AL(v.U, B * T * nx * nx); AL(v.Ulam, B * T * nx); AL(v.Urep, B * T);
+  AL(v.U, B * T * nx * nx); AL(v.Ulam, B * T * nx); AL(v.Urep, B * T); AL(v.psame, B * T);
   for (EngineFactors* F : {&v.fa, &v.dr}) {
     AL(F->V, B * T * nu * nu); AL(F->den, B * T * nu * nx); AL(F->Kf, B * T * nu * nx);
     AL(F->Acl, B * T * nx * nx); AL(F->AclT, B * T * nx * nx); AL(F->Hinv, B * T * nu * nu); AL(F->HB, B * T * nu * nx);

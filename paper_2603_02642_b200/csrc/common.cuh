@@ -96,6 +96,7 @@ struct Dev {
   int32_t* ttb;            // [nstate_tiles][2] tile base (b_hat_t, Bd_t) within an instance
   int64_t Est, EBst;       // per-instance sizes of b_hat_t / Bd_t
   double* bhat_t;          // [B][Est]
+  int32_t* psame;          // [B][T] Psi_k == Psi_{k-1} (setup)
   int32_t* ktile0;         // [T+1] first state tile with knot > k (tiles ascend in knot)
   double* Bd_t;            // [B][EBst]
   const int32_t* tiles;    // [ntiles][12] kind, knot, nc, klo, cone[8]

@@ -675,6 +675,10 @@ __global__ void __launch_bounds__(256) k_costate_mma(Dev v, const int32_t* __res
   const double* Psi = v.Psi + (int64_t)b * (d.T + 1) * nx * nx;
   double* bh = v.bhat + (int64_t)b * d.E + (gv ? v.off[cg] : 0);
   double* Bd = v.Bd + (int64_t)b * d.EB + (gv ? v.offB[cg] : 0);
+  // TMA path: also the tile-interleaved copies ([k][cone][.], tma.cu) -- same tiles
+  const bool tl2 = v.fused == 2;
+  double* bht = tl2 ? v.bhat_t + (int64_t)b * v.Est + v.ttb[2 * t] + g * nx : nullptr;
+  double* bdt = tl2 ? v.Bd_t + (int64_t)b * v.EBst + v.ttb[2 * t + 1] + g * nup : nullptr;
   const double* grad = v.grad + ((int64_t)b * d.ng + cg) * nx;
   double C[NTI][2];
 #pragma unroll
@@ -710,7 +714,11 @@ __global__ void __launch_bounds__(256) k_costate_mma(Dev v, const int32_t* __res
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const int m = 2 * q + rr;
-          if (m < nup) Bd[(int64_t)k * nup + m] = (m < nu) ? bb[rr] : 0.0;
+          if (m < nup) {
+            const double val = (m < nu) ? bb[rr] : 0.0;
+            Bd[(int64_t)k * nup + m] = val;
+            if (tl2) bdt[(int64_t)k * nc * nup + m] = val;
+          }
         }
       }
 #pragma unroll
@@ -737,7 +745,10 @@ __global__ void __launch_bounds__(256) k_costate_mma(Dev v, const int32_t* __res
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const int i = 2 * q + rr + 8 * nt;
-          if (i < nx) bh[(int64_t)k * nx + i] = st * h[nt][rr];
+          if (i < nx) {
+            bh[(int64_t)k * nx + i] = st * h[nt][rr];
+            if (tl2) bht[(int64_t)k * nc * nx + i] = st * h[nt][rr];
+          }
         }
     }
   }
@@ -817,11 +828,9 @@ cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st) {
     // Zb_k = sum_j b_{j,k} b_hat_{j,k}^T : the list adjoint with y = b_hat
     return launch_zlist(h, v.bhat, nullptr, nullptr, nullptr, nullptr, d.ng, nullptr, v.Zb, st);
   }
-  // TMA path: tile layout, then G0 = sum b b^T, H0 = sum b b_hat^T over state cones
+  // TMA path: G0 = sum b b^T, H0 = sum b b_hat^T over state cones
   // from it; control rows have b_hat = 0, so Zb = H0.
-  cudaError_t e = launch_relayout(h, st);
-  if (e != cudaSuccess) return e;
-  return launch_gram_tiles(h, st);
+  return launch_gram_tiles(h, st);   // the tile layout was written by k_costate_mma
 }
 
 static int fused_variant(const Dims& d, int* nti, int* nks) {

@@ -97,7 +97,7 @@ __device__ void warp_jacobi(double* A, double* V, int n) {
       if (r / n == r % n) dia += a * a; else off += a * a;
     }
     off = warp_sum(off); dia = warp_sum(dia);
-    if (off <= 1e-32 * dia || off == 0.0) break;
+    if (off <= 1e-30 * dia || off == 0.0) break;   // off-diagonal at 1e-15 of the diagonal
     for (int p = 0; p < n - 1; ++p) {
       for (int q = p + 1; q < n; ++q) {
         const double apq = A[p * n + q];
@@ -134,6 +134,22 @@ __device__ void warp_jacobi(double* A, double* V, int n) {
 // chain K = V [(V^T R U) ./ (2 + c tau sigma_a lambda_b)] U^T with
 // Lambda V = W' V diag(sigma), V^T W' V = I, Sigma = U diag(lambda) U^T.
 // Engine FullADMM: W' = W, c = rho.  DR (F3): W' = W + sigma_dr/2, c = r_s.
+// psame[b][k] = (Psi_k bit-identical to Psi_{k-1}), one warp per (instance, step).
+__global__ void k_psi_same(Dev v) {
+  const Dims d = v.d;
+  const int nn = d.nx * d.nx, lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= (int64_t)d.B * d.T) return;
+  const int b = (int)(gw / d.T), k = (int)(gw % d.T);
+  int same = k > 0;
+  if (k > 0) {
+    const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + k) * nn;
+    for (int r = lane; r < nn; r += 32) same &= (Pk[r - nn] == Pk[r]);
+  }
+  same = __all_sync(0xffffffffu, same);
+  if (lane == 0) v.psame[gw] = same;
+}
+
 __global__ void k_chain(Dev v) {
   extern __shared__ double sm[];
   const Dims d = v.d;
@@ -157,14 +173,8 @@ __global__ void k_chain(Dev v) {
   // Sigma_k depends on Psi_k only: the warp for the first step of a run of
   // bit-identical Psi blocks (S = blkdiag(S_0, S_d, ..., S_d)) does the
   // eigen-decomposition; the others wait for it in k_chain_copy.
-  int k0 = k;
-  while (k0 > 0) {
-    const double* Pp = v.Psi + ((int64_t)b * (d.T + 1) + k0 - 1) * nx * nx;
-    int same = 1;
-    for (int r = lane; r < nx * nx; r += 32) same &= (Pp[r] == Pk[r]);
-    if (!__all_sync(0xffffffffu, same)) break;
-    --k0;
-  }
+  int k0 = k;                                   // start of the run (k_psi_same flags)
+  while (k0 > 0 && v.psame[(int64_t)b * d.T + k0]) --k0;
   v.Urep[bk] = k0;
   if (k0 == k) {
     for (int r = lane; r < nx * nx; r += 32) {   // Sigma = Psi^T Psi
@@ -437,6 +447,8 @@ cudaError_t launch_setup(nrto_handle_s* h, cudaStream_t st) {
   const int per = 2 * d.nx * d.nx + 4 * d.nu * d.nu + d.nx + d.nu;
   const int wpb = 4;
   const int64_t nw = (int64_t)d.B * d.T;
+  k_psi_same<<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(v);
+  h->launches++;
   k_chain<<<(unsigned)((nw + wpb - 1) / wpb), 32 * wpb, wpb * per * sizeof(double), st>>>(v);
   h->launches++;
   h->dr_ready = 0;
