@@ -707,26 +707,30 @@ template <bool FIRST, int U>
 __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int tid, int nt,
                                         const double* __restrict__ grad,
                                         const double* __restrict__ g0, double* p, double* zl,
-                                        double* yl, double* rp, const double* pt,
+                                        double* yl, double* vv, const double* pt,
                                         const double* lam, const double* sX, const double* gR,
                                         double* gS, double* gU, bool more, double rho, double rq,
                                         double sq, double aq, double den, double beta,
                                         double rinv) {
+  // vv[j] = v_j = p~_j - lam_j rinv, constant over the QP iterations of a launch
+  // (formed in the FIRST pass); rhs_p,j = sq p_j + rho v_j + rq z_j - y_j is
+  // recomputed from the row's current (p, z, y) instead of being stored.
   const int nx = v.d.nx, nu = v.d.nu;
   const int4* __restrict__ rows = v.rowpk + bg;
   const double* __restrict__ gval = v.gval + bg * kRowNZ;
   for (int j0 = tid; j0 < ng; j0 += U * nt) {
     int4 rc[U];
     double2 g01[U];
-    double rpj[U], pj[U], zlj[U], ylj[U], g0j[U], ptj[U], lmj[U];
+    double vj[U], pj[U], zlj[U], ylj[U], g0j[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = j0 + u * nt;
       if (j < ng) {
         rc[u] = rows[j];
         g01[u] = *reinterpret_cast<const double2*>(gval + (int64_t)j * kRowNZ);
-        pj[u] = p[j]; zlj[u] = zl[j]; ylj[u] = yl[j]; ptj[u] = pt[j]; lmj[u] = lam[j];
-        if (!FIRST) { rpj[u] = rp[j]; g0j[u] = g0[j]; }
+        pj[u] = p[j]; zlj[u] = zl[j]; ylj[u] = yl[j];
+        if (FIRST) vj[u] = pt[j] - lam[j] * rinv;
+        else { vj[u] = vv[j]; g0j[u] = g0[j]; }
       }
     }
 #pragma unroll
@@ -736,6 +740,7 @@ __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int ti
       const int k = rc[u].x, kind = rc[u].y & 0xff, nz = (rc[u].y >> 8) & 0xff;
       const double* gj = grad + (int64_t)j * nx;
       double pn = pj[u], zn = zlj[u], yn = ylj[u];
+      if (FIRST) vv[j] = vj[u];
       if (!FIRST) {
         const double* x = (kind == 0) ? sX + (int64_t)k * nx : gR + (int64_t)k * nu;
         double bd = 0.0;
@@ -747,7 +752,8 @@ __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int ti
           const int n = (kind == 0) ? nx : nu;
           for (int i = 0; i < n; ++i) bd += gj[i] * x[i];
         }
-        const double ptl = (rpj[u] - rq * bd) / den;
+        const double r0 = sq * pj[u] + rho * vj[u] + rq * zlj[u] - ylj[u];
+        const double ptl = (r0 - rq * bd) / den;
         pn = aq * ptl + (1.0 - aq) * pj[u];
         const double zh = aq * (bd + ptl) + (1.0 - aq) * zlj[u];
         zn = fmin(zh + ylj[u] / rq, -g0j[u]);
@@ -755,9 +761,7 @@ __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int ti
         p[j] = pn; zl[j] = zn; yl[j] = yn;
       }
       if (FIRST || more) {
-        const double vj = ptj[u] - lmj[u] * rinv;
-        const double r = sq * pn + rho * vj + rq * zn - yn;
-        rp[j] = r;
+        const double r = sq * pn + rho * vj[u] + rq * zn - yn;
         const double w = rq * zn - yn - beta * r;
         double* dst = (kind == 0) ? gS + (int64_t)k * nx : gU + (int64_t)k * nu;
         if (nz <= kRowNZ) {
