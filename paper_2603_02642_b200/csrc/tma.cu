@@ -326,7 +326,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
 __global__ void __launch_bounds__(512)
 k_fa_ctrl(Dev v) {
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, nup = d.nup;
+  const int nx = d.nx, nu = d.nu;
   const int b = blockIdx.x;
   if (!v.active[b]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -342,32 +342,44 @@ k_fa_ctrl(Dev v) {
   double drow[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) drow[m] = (lane < nx && m < nu) ? Dk[lane * nu + m] : 0.0;
-  for (int q = v.cptr[k]; q < v.cptr[k + 1]; ++q) {
-    const int j = v.crow[q];
-    const int64_t ij = bg + j;
-    const double* bj = Bd + v.offB[j];
-    double bm[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) bm[m] = (m < nu) ? bj[m] : 0.0;
-    double y = 0.0;
-    if (lane < nx) {
-      y = (1.0 - v.s[ij]) * Y[v.off[j] + lane];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) y += drow[m] * bm[m];
-      Y[v.off[j] + lane] = y;
+  const int q0 = v.cptr[k], q1 = v.cptr[k + 1];
+  for (int qb = q0; qb < q1; qb += 32) {
+    // lane c holds the metadata of cone qb + c (all loads issued together)
+    int64_t offc = 0, offBc = 0;
+    double sc = 1.0;
+    int jc = 0;
+    if (qb + lane < q1) {
+      jc = v.crow[qb + lane];
+      offc = v.off[jc]; offBc = v.offB[jc]; sc = v.s[bg + jc];
     }
-    const double n2 = warp_sum(y * y);
-    const double sh = shat_of(v, v.s[ij]);          // predicted scale (k_project corrects)
-    __syncwarp();
-    if (lane == 0) v.nrm2[ij] = n2;
+    const int nq = min(32, q1 - qb);
+    for (int c = 0; c < nq; ++c) {
+      const int64_t off = __shfl_sync(0xffffffffu, offc, c);
+      const int64_t offB = __shfl_sync(0xffffffffu, offBc, c);
+      const double sj = __shfl_sync(0xffffffffu, sc, c);
+      const int j = __shfl_sync(0xffffffffu, jc, c);
+      const double* bj = Bd + offB;
+      double bm[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) zc[m] += sh * bm[m] * y;
+      for (int m = 0; m < 8; ++m) bm[m] = (m < nu) ? bj[m] : 0.0;
+      double y = 0.0;
+      if (lane < nx) {
+        y = (sj != 1.0) ? (1.0 - sj) * Y[off + lane] : 0.0;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) y += drow[m] * bm[m];
+        Y[off + lane] = y;
+      }
+      const double n2 = warp_sum(y * y);
+      const double sh = shat_of(v, sj);          // predicted scale (k_project corrects)
+      if (lane == 0) v.nrm2[bg + j] = n2;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) zc[m] += sh * bm[m] * y;
+    }
   }
   if (lane < nx) {
     double* Zo = v.Zctrl + ((int64_t)b * d.T + k) * nu * nx;
     for (int m = 0; m < nu; ++m) Zo[m * nx + lane] = zc[m];
   }
-  (void)nup;
 }
 
 // Projection of every cone of the batch from its ||y^l||^2 (SM Eq.(18)):
