@@ -134,6 +134,11 @@ typedef struct {
   int32_t* status;         /* [b] nrto_inst_status                             */
   double* r_p;             /* [b] final ||p - p~||                             */
   double* r_d;             /* [b] final rho ||p~^l - p~^(l-1)||                */
+  double* hist;            /* [b][L][3] optional residual trace, L = max_iter
+                              (FullADMM) / max_admm_iter (DR): row l-1 holds
+                              (r_p, r_d, r_dr of the last DR iteration; 0 for
+                              FullADMM) after outer iteration l (P:505-507,
+                              P:380-382); rows after an instance stops are 0 */
 } nrto_out;
 
 /* Fill p with the defaults of DESIGN §4 (rho=10, rho_admm=40, alpha_dr=0.9,

@@ -376,6 +376,21 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     if (o->margin_lin) ml_d = h->stage_ng2 + B * d.ng;
   }
   int32_t* dcount = h->dcount;
+  // optional residual trace: handle-owned device buffer, zeroed per solve
+  const int histL = engine == NRTO_FULLADMM ? prm.max_iter : prm.max_admm_iter;
+  v.hist = nullptr;
+  v.hist_L = histL;
+  if (o->hist && histL > 0) {
+    const size_t need = (size_t)B * histL * 3;
+    if (h->hist_cap < need) {
+      if (h->hist_buf) cudaFree(h->hist_buf);
+      h->hist_buf = nullptr; h->hist_cap = 0;
+      CK(cudaMalloc((void**)&h->hist_buf, need * sizeof(double)));
+      h->hist_cap = need;
+    }
+    CK(cudaMemsetAsync(h->hist_buf, 0, need * sizeof(double), st));
+    v.hist = h->hist_buf;
+  }
 
   cudaError_t ce = cudaSuccess;
   auto timed = [&](int cls, cudaError_t (*fn)(nrto_handle_s*, cudaStream_t)) -> cudaError_t {
@@ -523,6 +538,8 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
   CK(copy_out(o->status, v.status, B * 4, host, st));
   CK(copy_out(o->r_p, v.r_p, B * D8, host, st));
   CK(copy_out(o->r_d, v.r_d, B * D8, host, st));
+  if (v.hist) CK(copy_out(o->hist, v.hist, (size_t)B * v.hist_L * 3 * D8, host, st));
+  v.hist = nullptr;
   if (host) {
     CK(copy_out(o->nu, nu_d, B * d.E * D8, true, st));
     CK(copy_out(o->lam_nu, lam_d, B * d.E * D8, true, st));
@@ -564,6 +581,7 @@ extern "C" nrto_err nrto_destroy(nrto_handle h) {
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->dcount) cudaFree(h->dcount);
+  if (h->hist_buf) cudaFree(h->hist_buf);
   if (h->stage_ng2) cudaFree(h->stage_ng2);
   if (h->stage_b) cudaFree(h->stage_b);
   if (h->stage_e2) cudaFree(h->stage_e2);

@@ -75,6 +75,8 @@ struct Dev {
                            // correction; 2: k_fa_tma (state tiles) + k_fa_ctrl + correction
   int nctrl;               // number of control cones
   int iter;                // outer iteration l of the launch (set by the host loop)
+  double* hist;            // [B][hist_L][3] residual trace (nullptr: not requested)
+  int hist_L;
   int ylazy;               // 1: lazy y storage in this iteration
   unsigned long long* pass_bytes;  // algorithmic bytes moved by k_fa_tma (device counter)
   double* nrm2;            // [B][ng] ||y^l||^2 written by the fused pass
@@ -113,6 +115,8 @@ struct Dev {
 struct nrto_prof_rec { int cls; cudaEvent_t a, b; };
 
 struct nrto_handle_s {
+  double* hist_buf = nullptr;   // device residual-trace buffer (grown on demand)
+  size_t hist_cap = 0;
   int tma_margin = 0;      // k_fa_tma launch mode: 1 = finish margins (||C^L b + b_hat||)
   nrto::Dev dev;
   int64_t launches = 0;
@@ -177,6 +181,15 @@ constexpr int kEnter = 1 << 28;       // state cone enters {s = 1}: G += b b^T, 
 // l = 1 (cold start, t = p^0 + lam_p^0 = 0): a state cone with a > 0 is in
 // case 3 with s = (0 + a)/(2a) = 1/2 exactly, so shat = 1/2.  l > 1: shat =
 // [s^{l-1} == 1] (case 1 persists).  Mispredictions are corrected exactly.
+// Residual trace row l-1 of instance b (QP kernels, after r_p / r_d of iteration l).
+__device__ __forceinline__ void record_hist(const Dev& v, int b, int l, double rp, double rd,
+                                            int engine) {
+  if (v.hist && l >= 1 && l <= v.hist_L) {
+    double* h = v.hist + ((int64_t)b * v.hist_L + (l - 1)) * 3;
+    h[0] = rp; h[1] = rd; h[2] = engine == NRTO_FULLADMM ? 0.0 : v.rdr[b];
+  }
+}
+
 __device__ __forceinline__ double shat_of(const Dev& v, double sprev) {
   if (v.iter == 1) return 0.5;
   return (sprev == 1.0) ? 1.0 : 0.0;

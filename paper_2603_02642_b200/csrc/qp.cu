@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(128) k_qp(Dev v, int engine, int l) {
     const double rpv = sqrt(ap), rdv = rho * sqrt(ad);
     v.r_p[b] = rpv;
     v.r_d[b] = rdv;
+    record_hist(v, b, l, rpv, rdv, engine);
     v.iters[b] = l;
     if (!isfinite(rpv) || !isfinite(rdv)) {
       v.status[b] = NRTO_DIVERGED;
@@ -407,6 +408,7 @@ __global__ void __launch_bounds__(1024) k_qp_staged(Dev v, int engine, int l, in
     const double rpv = sqrt(ap), rdv = rho * sqrt(ad);
     v.r_p[b] = rpv;
     v.r_d[b] = rdv;
+    record_hist(v, b, l, rpv, rdv, engine);
     v.iters[b] = l;
     if (!isfinite(rpv) || !isfinite(rdv)) {
       v.status[b] = NRTO_DIVERGED;
@@ -670,6 +672,7 @@ __global__ void __launch_bounds__(256, 5) k_qp_lite(Dev v, int engine, int l) {
     const double rpv = sqrt(ap), rdv = rho * sqrt(ad);
     v.r_p[b] = rpv;
     v.r_d[b] = rdv;
+    record_hist(v, b, l, rpv, rdv, engine);
     v.iters[b] = l;
     if (!isfinite(rpv) || !isfinite(rdv)) {
       v.status[b] = NRTO_DIVERGED;
@@ -1119,6 +1122,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
     const double rpv = sqrt(ap), rdv = rho * sqrt(ad);
     v.r_p[b] = rpv;
     v.r_d[b] = rdv;
+    record_hist(v, b, l, rpv, rdv, engine);
     v.iters[b] = l;
     if (!isfinite(rpv) || !isfinite(rdv)) {
       v.status[b] = NRTO_DIVERGED;

@@ -44,7 +44,7 @@ class nrto_params(C.Structure):
 
 
 OUT_FIELDS = ("kv", "du", "p", "p_tilde", "lam_p", "nu", "lam_nu", "objective", "margin_cone",
-              "margin_lin", "iters", "status", "r_p", "r_d")
+              "margin_lin", "iters", "status", "r_p", "r_d", "hist")
 
 
 class nrto_out(C.Structure):

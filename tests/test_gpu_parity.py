@@ -169,6 +169,51 @@ def test_dr_parity(case, La, Ld):
     assert_parity(g, o, engine=1)
 
 
+def _solve_hist(shape, batch, engine, L, **pkw):
+    _require_gpu()
+    data = nrto.to_tensors(batch, device="cuda")
+    s = nrto.InnerSolver(shape, data, **pkw)
+    out = nrto.alloc_out(shape, 1, s.E, device="cuda")
+    out["hist"] = torch.full((1, L, 3), -1.0, dtype=torch.float64, device="cuda")
+    s.solve(engine, out=out)
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    s.close()
+    return res
+
+
+@pytest.mark.parametrize("case", ["c1", "c3s"])
+def test_residual_trace_fulladmm(case):
+    """hist[l-1] = (r_p, r_d, 0) after iteration l (P:505-507) vs the oracle's trace;
+    rows after the instance stops are 0."""
+    shape, data = CASES[case]()
+    L = 60
+    kw = dict(max_iter=L, eps_p=1e-4, eps_d=1e-4)
+    g = _solve_hist(shape, single(shape, data), nrto.NRTO_FULLADMM, L, **kw)
+    o = oracle_run(shape, data, nrto.NRTO_FULLADMM, **kw)
+    n = int(o["iters"])
+    assert int(g["iters"][0]) == n
+    H = g["hist"][0]
+    np.testing.assert_allclose(H[:n, 0], o["hist"][:, 0], rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose(H[:n, 1], o["hist"][:, 1], rtol=1e-6, atol=1e-9)
+    assert np.all(H[:n, 2] == 0.0) and np.all(H[n:] == 0.0)
+
+
+def test_residual_trace_dr():
+    shape, data = CASES["c1"]()
+    La, Ld = 5, 20
+    kw = dict(max_admm_iter=La, max_dr_iter=Ld, fixed_iters=1)
+    g = _solve_hist(shape, single(shape, data), nrto.NRTO_DR, La, **kw)
+    tr = []
+    sp = st.StructuredProblem(shape, data)
+    st.nrto_admm_dr(sp, make_params(**kw), trace=tr)
+    H = g["hist"][0]
+    for l, t in enumerate(tr):
+        assert H[l, 0] == pytest.approx(t["r_p"], rel=1e-6, abs=1e-9)
+        assert H[l, 1] == pytest.approx(t["r_d"], rel=1e-6, abs=1e-9)
+        assert H[l, 2] == pytest.approx(t["r_dr"], rel=1e-6, abs=1e-9)
+
+
 def test_dr_early_stop_parity():
     shape, data = CASES["c1"]()
     kw = dict(max_admm_iter=8, max_dr_iter=100, eps_dr=1e-6, eps_p=1e-6, eps_d=1e-6)
