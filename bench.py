@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--workload", default="c5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dr", action="store_true")
     return ap.parse_args()
 
 
@@ -253,6 +254,33 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": world * B * L / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "sl_iteration_wall_clock_ms": ems}
 
+    # secondary line: the NRTO-DR engine on its own config (c2 quadcopter, one
+    # instance, 40 NRTO-ADMM x 100 DR iterations, fixed) -- latency-bound, reported
+    # as DR iterations/s (S3-S8 per DR iteration) and NRTO-ADMM iterations/s
+    dr = None
+    if not args.no_dr and rank == 0:
+        from gen import make_instance
+        from gen.problems import stack_instances
+        shp2, d2 = make_instance("c2")
+        dd2 = nrto.to_tensors(stack_instances([(shp2, d2)])[1], device=dev)
+        s2 = nrto.InnerSolver(shp2, dd2, fixed_iters=1)
+        o2 = nrto.alloc_out(shp2, 1, s2.E, device=dev, full=False)
+        s2.solve(nrto.NRTO_DR, out=o2)
+        torch.cuda.synchronize()
+        e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e4.record(stream)
+        for _ in range(2):
+            s2.solve(nrto.NRTO_DR, out=o2)
+        e5.record(stream)
+        torch.cuda.synchronize()
+        dms = e4.elapsed_time(e5) / 2
+        La, Ld = s2.params.max_admm_iter, s2.params.max_dr_iter
+        dr = {"workload": "c2: quadcopter NRTO-DR, 1 instance (n_x=12, n_u=4, T=50, n_g=%d), "
+                          "%d NRTO-ADMM x %d DR iterations, fixed" % (shp2.n_g, La, Ld),
+              "dr_iters_per_s": La * Ld / (dms / 1000.0),
+              "admm_iters_per_s": La / (dms / 1000.0), "ms_per_solve": dms}
+        s2.close()
+
     # batch-wide residual statistics over NVLink (the only collective)
     max_rp, n_unconv, any_div = batch_stats(out["r_p"], out["status"], device=dev)
 
@@ -301,6 +329,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
+        "dr_engine": dr,
         "residuals": {"max_r_p": max_rp, "unconverged_instances": n_unconv,
                       "any_diverged": any_div},
     }
