@@ -64,6 +64,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+#ifndef TMA_NW
+#define TMA_NW 16
+#endif
 constexpr int kMaxStages = 8;
 constexpr int kRingT = 4;
 constexpr int kTI = 12;   // ints per tile
@@ -107,12 +110,13 @@ __host__ __device__ inline size_t tma_fixed_doubles(int T, int nx, int nu) {
 // consumers straight from global memory, issued before the stage wait.
 // NXE, NUE > 0: exact n_x, n_u fixed at compile time (benchmark shapes): every
 // bounds predicate of the inner block folds away.
-template <int NTI, int NKS, int KK, int NXE, int NUE>
-__global__ void __launch_bounds__(544, 1)
+template <int NTI, int NKS, int KK, int NXE, int NUE, int NW = 16>
+__global__ void __launch_bounds__((NW + 1) * 32, 1)
 k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems, int nst,
          int margin) {
   extern __shared__ __align__(128) double sm[];
-  constexpr int NW = 16;
+  constexpr int CH = 16;          // blocks per chunk (stage)
+  constexpr int BPW = CH / NW;    // blocks per consumer warp per chunk
   const Dims d = v.d;
   const int nx = NXE > 0 ? NXE : d.nx, nu = NUE > 0 ? NUE : d.nu, T = d.T;
   const int nup = NUE > 0 ? (NUE + (NUE & 1)) : d.nup;
@@ -221,7 +225,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
     // y_old of history cones (s^{l-1} != 1) comes from global memory; each
     // chunk's loads are issued one chunk ahead so their latency overlaps the
     // previous chunk's work
-    double2 yo[NTI], yn[NTI];
+    double2 yo[BPW][NTI], yn[BPW][NTI];
     auto load_y = [&](double2 (&dst)[NTI], int kb) {
 #pragma unroll
       for (int nt = 0; nt < NTI; ++nt) {
@@ -231,28 +235,36 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
           dst[nt] = __ldcs(reinterpret_cast<const double2*>(Y + offg + (int64_t)kb * nx + i0));
       }
     };
-    if (hist) load_y(yo, warp);
+    if (hist) {
+#pragma unroll
+      for (int bb = 0; bb < BPW; ++bb) load_y(yo[bb], warp + NW * bb);
+    }
 #pragma unroll
     for (int kk = 0; kk < KK; ++kk) {
-      const int kc = NW * kk;
+      const int kc = CH * kk;
       if (kc > K) break;
-      const int k = kc + warp;
-      const bool act = k <= K;
-      if (hist && kc + NW <= K) load_y(yn, k + NW);
+      if (hist && kc + CH <= K) {
+#pragma unroll
+        for (int bb = 0; bb < BPW; ++bb) load_y(yn[bb], kc + CH + warp + NW * bb);
+      }
       if (kk > 0) mbar_wait(&full[st], ph);
       const double* sH = stg + (size_t)st * G.stage;
       const double* sB = sH + G.SY;
-      if (act) {
+#pragma unroll
+      for (int bb = 0; bb < BPW; ++bb) {
+        const int lb = warp + NW * bb;            // block within the chunk
+        const int k = kc + lb;
+        if (k > K) continue;
         double c[NTI][2];
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt) {
           const int i0 = 2 * q + 8 * nt;
           c[nt][0] = 0.0; c[nt][1] = 0.0;
           if (gv && i0 < nx) {
-            const double2 bh = *reinterpret_cast<const double2*>(sH + (warp * nc + g) * nx + i0);
+            const double2 bh = *reinterpret_cast<const double2*>(sH + (lb * nc + g) * nx + i0);
             if (hist) {
-              c[nt][0] = bh.x + omsp * yo[nt].x;
-              c[nt][1] = bh.y + omsp * yo[nt].y;
+              c[nt][0] = bh.x + omsp * yo[bb][nt].x;
+              c[nt][1] = bh.y + omsp * yo[bb][nt].y;
             } else {
               c[nt][0] = bh.x;
               c[nt][1] = bh.y;
@@ -263,12 +275,12 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
 #pragma unroll
           for (int ks = 0; ks < NKS; ++ks) {
             const int m = q + 4 * ks;
-            const double a = (gv && m < nu) ? sB[(warp * nc + g) * nup + m] : 0.0;
+            const double a = (gv && m < nu) ? sB[(lb * nc + g) * nup + m] : 0.0;
 #pragma unroll
             for (int nt = 0; nt < NTI; ++nt) {
               const int i = g + 8 * nt;
-              const double bb = (m < nu && i < nx) ? Ds[((size_t)k * nx + i) * nu + m] : 0.0;
-              dmma2(c[nt], a, bb);
+              const double bq = (m < nu && i < nx) ? Ds[((size_t)k * nx + i) * nu + m] : 0.0;
+              dmma2(c[nt], a, bq);
             }
           }
         }
@@ -286,7 +298,9 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
       if (++st == nst) { st = 0; ph ^= 1; }
       if (hist) {
 #pragma unroll
-        for (int nt = 0; nt < NTI; ++nt) yo[nt] = yn[nt];
+        for (int bb = 0; bb < BPW; ++bb)
+#pragma unroll
+          for (int nt = 0; nt < NTI; ++nt) yo[bb][nt] = yn[bb][nt];
       }
     }
     // ---- norm partials -> ring slot; last consumer warp publishes the tile's norms
@@ -547,12 +561,12 @@ bool tma_supported(const Dims& d) {
   return (d.nx % 2 == 0) && d.nx <= 16 && d.nu <= 8 && d.T <= 111 && tma_stages(d) >= 3;
 }
 
-template <int NTI, int NKS, int KK, int NXE = 0, int NUE = 0>
+template <int NTI, int NKS, int KK, int NXE = 0, int NUE = 0, int NW = 16>
 static cudaError_t launch_tma_t(nrto_handle_s* h, cudaStream_t st) {
   const size_t smem = tma_smem_bytes(h->dev.d);
-  auto kfn = k_fa_tma<NTI, NKS, KK, NXE, NUE>;
+  auto kfn = k_fa_tma<NTI, NKS, KK, NXE, NUE, NW>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kfn<<<h->dev.nwitems, 544, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems, tma_stages(h->dev.d),
+  kfn<<<h->dev.nwitems, (NW + 1) * 32, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems, tma_stages(h->dev.d),
                                          h->tma_margin);
   h->launches++;
   return cudaGetLastError();
@@ -571,7 +585,7 @@ cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st) {
   const int nti = (d.nx + 7) / 8, nks = (d.nu + 3) / 4;
   cudaError_t e = cudaSuccess;
   if (h->dev.nwitems > 0) {
-    if (d.nx == 14 && d.nu == 7 && d.T >= 64) e = launch_tma_t<2, 2, 7, 14, 7>(h, st);
+    if (d.nx == 14 && d.nu == 7 && d.T >= 64) e = launch_tma_t<2, 2, 7, 14, 7, TMA_NW>(h, st);
     else if (d.nx == 12 && d.nu == 4 && d.T >= 32 && d.T < 64) e = launch_tma_t<2, 1, 4, 12, 4>(h, st);
     else if (d.T < 32) e = launch_tma_k<2>(h, nti, nks, st);
     else if (d.T < 64) e = launch_tma_k<4>(h, nti, nks, st);
