@@ -258,8 +258,14 @@ __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
       sK[r] = Kb[i * nu + m];
     }
     __syncwarp();
-    for (int r = lane; r < nu * nx; r += 32) v.H[bk * nu * nx + r] += v.dH[bk * nu * nx + r];
-    for (int r = lane; r < nu * nu; r += 32) v.G[bk * nu * nu + r] += v.dG[bk * nu * nu + r];
+    // l = 1: G, H restart from the entering cones (k_project lists s^1 = 1 only)
+    if (v.iter == 1) {
+      for (int r = lane; r < nu * nx; r += 32) v.H[bk * nu * nx + r] = v.dH[bk * nu * nx + r];
+      for (int r = lane; r < nu * nu; r += 32) v.G[bk * nu * nu + r] = v.dG[bk * nu * nu + r];
+    } else {
+      for (int r = lane; r < nu * nx; r += 32) v.H[bk * nu * nx + r] += v.dH[bk * nu * nx + r];
+      for (int r = lane; r < nu * nu; r += 32) v.G[bk * nu * nu + r] += v.dG[bk * nu * nu + r];
+    }
   } else {
     for (int r = lane; r < nu * nx; r += 32) {
       double z = v.Zc[bk * nu * nx + r];

@@ -412,17 +412,18 @@ __global__ void k_project(Dev v) {
   v.s[id] = s;
   v.pt[id] = tp;
   // TMA path: state cones leaving / entering the interior set {s = 1} update
-  // the Gram sums G, H of the predicted adjoint; at l = 1 every
-  // state cone counts as interior before the projection.
+  // the Gram sums G, H of the predicted adjoint.
+  // At l = 1 the interior set restarts from empty (the gain kernel replaces G, H by
+  // this iteration's updates), so only the cones with s^1 = 1 are listed (enter).
   const bool gh = v.fused == 2 && v.kind[j] == 0;
   const bool first = v.iter == 1;
-  const bool leave = gh && s != 1.0 && (first || shat == 1.0);
-  const bool enter = gh && !first && shat == 0.0 && s == 1.0;
+  const bool leave = gh && !first && shat == 1.0 && s != 1.0;
+  const bool enter = gh && s == 1.0 && (first || shat == 0.0);
   if (s != shat || leave) {
     // lazy y: a state cone predicted interior (shat = 1) was not stored by the
     // pass; flag it so the correction rebuilds y^l (blocks k < K there, the
     // b-free last block y_K = b_hat_K here).
-    const bool rec = v.ylazy && leave && !first;
+    const bool rec = v.ylazy && leave;
     const int pos = atomicAdd(&v.ncorr[b], 1);
     v.clist[(int64_t)b * v.d.ng + pos] = j | (rec ? kRecompute : 0) | (leave ? kLeave : 0) |
                                          (enter ? kEnter : 0);
