@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Fused FullADMM cone pass (S3 forward map + S4 SOC projection + S5 state
 // update + S7 adjoint) in ONE streaming pass over the ragged cone data, with
 // both small contractions on the FP64 tensor cores (DMMA m8n8k4).
@@ -468,7 +469,7 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
-  const int k = blockIdx.y * 16 + warp;
+  const int k = blockIdx.y * (blockDim.x >> 5) + warp;
   if (k >= d.T) return;
   if (act && !act[b]) return;
   // lazy y: entries flagged kRecompute were not stored by the pass
@@ -499,6 +500,7 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
   double z[NTI][2], hz[NTI][2], gz[2] = {0.0, 0.0};
 #pragma unroll
   for (int nt = 0; nt < NTI; ++nt) { z[nt][0] = z[nt][1] = 0.0; hz[nt][0] = hz[nt][1] = 0.0; }
+  bool any = false;                     // this split saw a cone with a block at k
   for (int base = lo; base < hi; base += 32) {
     // lane l inspects entry base + l
     int j = 0, rec = 0, sgn = 0;
@@ -522,6 +524,7 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
     }
     const unsigned mask = __ballot_sync(0xffffffffu, has || hasg);
     const int nv = __popc(mask);
+    any |= nv > 0;
     // per-lane row pointers of valid entries (computed by their owner lanes)
     int64_t yoff = 0, boff = 0;
     if (has || hasg) {
@@ -599,6 +602,7 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
       }
     }
   }
+  if (nsp > 1 && !any) return;         // slices pre-zeroed; nothing to add
   if (g < nu) {
     const int64_t bk = (int64_t)b * d.T + k;
     if (Zout) {
@@ -614,18 +618,24 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
           }
         }
     }
-    if (ghmode) {                       // launched unsplit (nsp == 1)
+    if (ghmode) {                       // split: pre-zeroed, accumulated
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const int m2 = 2 * q + r;
-        if (m2 < nu) dG[bk * nu * nu + g * nu + m2] = gz[r];
+        if (m2 < nu) {
+          if (nsp == 1) dG[bk * nu * nu + g * nu + m2] = gz[r];
+          else atomicAdd(&dG[bk * nu * nu + g * nu + m2], gz[r]);
+        }
       }
 #pragma unroll
       for (int nt = 0; nt < NTI; ++nt)
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const int i = 2 * q + r + 8 * nt;
-          if (i < nx) dH[bk * nu * nx + g * nx + i] = hz[nt][r];
+          if (i < nx) {
+            if (nsp == 1) dH[bk * nu * nx + g * nx + i] = hz[nt][r];
+            else atomicAdd(&dH[bk * nu * nx + g * nx + i], hz[nt][r]);
+          }
         }
     }
   }
@@ -907,16 +917,29 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
       const int64_t ctas = (int64_t)v.d.B * ((v.d.T + 15) / 16);
       while (nsp < 64 && ctas * nsp < 296 && (nfixed / (nsp * 2)) >= 64) nsp *= 2;
     }
+    // device-sized lists (TMA path): a fixed split so that long lists (early
+    // iterations: most cones in case 3) are walked by nsp warps per step; splits
+    // past the list end exit at once, empty splits add nothing
+    static const int lsp = [] { const char* e = getenv("NRTO_ZLIST_SPLIT"); return e ? atoi(e) : 1; }();
+    if (ncnt && ghmode && lsp > 1) nsp = lsp;
     if (nsp > 1) {           // zero the slices of the instances that will be accumulated
       const int64_t per = (int64_t)v.d.T * v.d.nu * v.d.nx;
       k_zero_active<<<(unsigned)(((int64_t)v.d.B * per + 255) / 256), 256, 0, st>>>(Zout, per, v.d.B, act);
       h->launches++;
+      if (ghmode) {
+        const int64_t pg = (int64_t)v.d.T * v.d.nu * v.d.nu;
+        k_zero_active<<<(unsigned)(((int64_t)v.d.B * pg + 255) / 256), 256, 0, st>>>(dG, pg, v.d.B, act);
+        k_zero_active<<<(unsigned)(((int64_t)v.d.B * per + 255) / 256), 256, 0, st>>>(dH, per, v.d.B, act);
+        h->launches += 2;
+      }
     }
-    dim3 grid(v.d.B, (v.d.T + 15) / 16, nsp);
+    // warps (steps) per CTA: small CTAs fit beside the co-resident QP CTAs
+    static const int zw = [] { const char* e = getenv("NRTO_ZLIST_WARPS"); return e ? atoi(e) : 16; }();
+    dim3 grid(v.d.B, (v.d.T + zw - 1) / zw, nsp);
     if (v.d.nx <= 8)
-      k_zlist_mma<1><<<grid, 512, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
+      k_zlist_mma<1><<<grid, 32 * zw, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
     else
-      k_zlist_mma<2><<<grid, 512, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
+      k_zlist_mma<2><<<grid, 32 * zw, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
     h->launches++;
     return cudaGetLastError();
   }
