@@ -240,7 +240,11 @@ __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
   double* sX = sR + nu * nx;
   double* sK = sX + nu * nx;
   const double st = sqrt(v.tau[b]);
-  const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + k) * nx * nx;
+  // Psi_k and the Sigma_k eigenvectors U_k are read from the first step of their
+  // run of bit-identical Psi blocks (Urep, setup): same values, one cached copy
+  // per instance instead of T
+  const int kr = v.Urep[bk];
+  const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + kr) * nx * nx;
   const double* Wk = v.W + bk * nu * nu;
   double* Kb = v.K + (int64_t)b * d.NK + (int64_t)k * nu * nx;
   if (v.fused == 2) {
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
     sR[r] = 2.0 * wk + rho * st * gp;
   }
   __syncwarp();
-  chain_solve_w(v.fa.V + bk * nu * nu, v.U + bk * nx * nx, v.fa.den + bk * nu * nx, sR, sX,
+  chain_solve_w(v.fa.V + bk * nu * nu, v.U + ((int64_t)b * d.T + kr) * nx * nx, v.fa.den + bk * nu * nx, sR, sX,
                 nu, nx, lane);
   for (int r = lane; r < nu * nx; r += 32) {
     const int m = r / nx, i = r % nx;
