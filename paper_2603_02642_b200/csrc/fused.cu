@@ -457,8 +457,8 @@ k_zlist(Dev v, const double* __restrict__ y, const int32_t* __restrict__ clist,
 // keeps (ballot) the cones that have a b-block at k, and folds them into
 // Z_k with DMMA 8 cones at a time:
 //   Z_k[m][i] += sum_c (w_c b_{c,k,m}) y_{c,k,i}   ([8 m x 4 c] x [4 c x 8 i]).
-template <int NTI>
-__global__ void __launch_bounds__(512)
+template <int NTI, int NTH = 512, int MINB = 1>
+__global__ void __launch_bounds__(NTH, MINB)
 k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ clist,
             const double* __restrict__ cw, const double* __restrict__ scale,
             const int32_t* __restrict__ ncnt, int nfixed, const int32_t* __restrict__ act,
@@ -474,18 +474,9 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
   if (act && !act[b]) return;
   // lazy y: entries flagged kRecompute were not stored by the pass
   // (s^{l-1} = 1 predicted s^l = 1); their block y_{c,k} = D_k b_{c,k} + b_hat_{c,k}
-  // is rebuilt here from D_k (rows i = g + 8 nt in registers) and stored.
-  double dk[NTI][8];
-  if (lazy) {
-    const double* Dk = v.D + ((int64_t)b * d.T + k) * nx * nu;
-#pragma unroll
-    for (int nt = 0; nt < NTI; ++nt)
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const int i = g + 8 * nt;
-        dk[nt][m] = (i < nx && m < nu) ? Dk[i * nu + m] : 0.0;
-      }
-  }
+  // is rebuilt here from D_k and stored.
+  // (rows i = g + 8 nt of D_k, read through L1 only by the rare rebuilt entries)
+  const double* __restrict__ Dk = v.D + ((int64_t)b * d.T + k) * nx * nu;
   const int n = ncnt ? ncnt[b] : nfixed;
   // blockIdx.z splits the list (small batches); partial sums are added atomically
   const int nsp = gridDim.z, sp = blockIdx.z;
@@ -572,7 +563,7 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
             double acc = 0.0;
             if (i < nx) {
 #pragma unroll
-              for (int m = 0; m < 8; ++m) acc += dk[nt][m] * bm[m];
+              for (int m = 0; m < 8; ++m) acc += (m < nu) ? __ldg(Dk + i * nu + m) * bm[m] : 0.0;
               acc += bh[ks][nt];
               yw[i] = acc;
             }
@@ -934,10 +925,16 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
       }
     }
     // warps (steps) per CTA: small CTAs fit beside the co-resident QP CTAs
-    static const int zw = [] { const char* e = getenv("NRTO_ZLIST_WARPS"); return e ? atoi(e) : 16; }();
+    static const int zw = [] { const char* e = getenv("NRTO_ZLIST_WARPS"); return e ? atoi(e) : 4; }();
     dim3 grid(v.d.B, (v.d.T + zw - 1) / zw, nsp);
+    // NRTO_ZLIST_WARPS = 4: 128-thread CTAs; NRTO_ZLIST_MINB = 8 / 6: capped at 64 / 80 registers
+    static const int zmb = [] { const char* e = getenv("NRTO_ZLIST_MINB"); return e ? atoi(e) : 8; }();
     if (v.d.nx <= 8)
       k_zlist_mma<1><<<grid, 32 * zw, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
+    else if (zw == 4 && zmb == 8)
+      k_zlist_mma<2, 128, 8><<<grid, 128, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
+    else if (zw == 4 && zmb == 6)
+      k_zlist_mma<2, 128, 6><<<grid, 128, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
     else
       k_zlist_mma<2><<<grid, 32 * zw, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
     h->launches++;

@@ -1,6 +1,7 @@
 // Per-iteration kernels of the inner loop and the
 // output/finish kernels.
 #include "common.cuh"
+#include <cstdlib>
 
 namespace nrto {
 
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
   const Dims d = v.d;
   const int nx = d.nx, nu = d.nu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (gw >= (int64_t)d.B * d.T) return;
   const int b = (int)(gw / d.T), k = (int)(gw % d.T);
   if (!v.active[b]) return;
@@ -591,7 +592,9 @@ cudaError_t launch_fa_gain(nrto_handle_s* h, cudaStream_t st) {
   const Dims& d = v.d;
   if (v.fused) {
     const int64_t nw = (int64_t)d.B * d.T;
-    k_fa_gain_w<<<(unsigned)((nw + 7) / 8), 256, 8 * 3 * d.nu * d.nx * sizeof(double), st>>>(v);
+    // small CTAs (NRTO_GAIN_WARPS, default 4) fit beside the co-resident QP CTAs
+    static const int gwp = [] { const char* e = getenv("NRTO_GAIN_WARPS"); return e ? atoi(e) : 4; }();
+    k_fa_gain_w<<<(unsigned)((nw + gwp - 1) / gwp), 32 * gwp, gwp * 3 * d.nu * d.nx * sizeof(double), st>>>(v);
     h->launches++;
     return cudaGetLastError();
   }

@@ -15,6 +15,7 @@
 // adjoint contribution s b y^T are completed inside one warp (k_fa_ctrl).
 #include "common.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace nrto {
 
@@ -599,8 +600,10 @@ cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st) {
 cudaError_t launch_fa_ctrl(nrto_handle_s* h, cudaStream_t st) {
   const Dims& d = h->dev.d;
   if (h->dev.nctrl > 0) {
-    dim3 grid(d.B, (d.T + 15) / 16);
-    k_fa_ctrl<<<grid, 512, 0, st>>>(h->dev);
+    // warps (steps) per CTA, NRTO_CTRL_WARPS (default 4): small CTAs fit beside the QP CTAs
+    static const int cwp = [] { const char* e = getenv("NRTO_CTRL_WARPS"); return e ? atoi(e) : 4; }();
+    dim3 grid(d.B, (d.T + cwp - 1) / cwp);
+    k_fa_ctrl<<<grid, 32 * cwp, 0, st>>>(h->dev);
     h->launches++;
   }
   return cudaGetLastError();
