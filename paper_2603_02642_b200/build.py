@@ -49,4 +49,5 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
 
 if __name__ == "__main__":
     xt = ["-Xptxas", "-v"] if "-v" in sys.argv else []
+    xt += [a for a in sys.argv[1:] if a.startswith("-D")]   # probe variants (compile-time knobs)
     print(build(force=True, verbose=True, extra=xt))

@@ -260,7 +260,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
     AL(v.H, B * T * nu * nx); AL(v.H0, B * T * nu * nx); AL(v.dH, B * T * nu * nx);
   }
   AL(v.Zctrl, B * T * nu * nx); AL(v.nrm2, B * ng);
-  AL(v.rowpk, B * ng); AL(v.gval, B * ng * 8);
+  AL(v.rowpk, B * ng); AL(v.gval, B * ng * 8); AL(v.cu2, B * T * nu);
   AL(v.pass_bytes, 1);
   cudaMemset(v.pass_bytes, 0, sizeof(unsigned long long));
   v.ylazy = 0;

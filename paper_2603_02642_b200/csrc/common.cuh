@@ -89,6 +89,7 @@ struct Dev {
   double* dG;              // [B][T][nu][nu] this iteration's leave/enter update
   double* dH;              // [B][T][nu][nx]
   int4* rowpk;             // [B][ng] packed gradient-row record (qp.cu, k_sparse_rows)
+  double* cu2;             // [B][T][nu] -2 R_u u_hat (qp.cu, setup)
   double* gval;            // [B][ng][8] its nonzero values
   double* Zctrl;           // [B][T][nu][nx] exact adjoint of the control cones (fused == 2)
   int ntiles, nsplit, nwitems;

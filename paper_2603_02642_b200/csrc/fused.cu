@@ -477,7 +477,11 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
   // is rebuilt here from D_k and stored.
   // (rows i = g + 8 nt of D_k, read through L1 only by the rare rebuilt entries)
   const double* __restrict__ Dk = v.D + ((int64_t)b * d.T + k) * nx * nu;
-  const int n = ncnt ? ncnt[b] : nfixed;
+  // dense mode (no list, every cone): walk the static per-step cone list
+  // kcone[kptr[k] .. kptr[k+1]) -- exactly the cones with a b-block at k
+  const bool dense = !clist && nfixed == d.ng;
+  const int kp0 = dense ? v.kptr[k] : 0;
+  const int n = ncnt ? ncnt[b] : (dense ? v.kptr[k + 1] - kp0 : nfixed);
   // blockIdx.z splits the list (small batches); partial sums are added atomically
   const int nsp = gridDim.z, sp = blockIdx.z;
   const int per = (((n + nsp - 1) / nsp) + 31) & ~31;
@@ -498,7 +502,7 @@ k_zlist_mma(Dev v, const double* __restrict__ y, const int32_t* __restrict__ cli
     double w = 0.0;
     bool has = false, hasg = false;
     if (base + lane < hi) {
-      const int raw = clist ? clist[bg + base + lane] : base + lane;
+      const int raw = clist ? clist[bg + base + lane] : (dense ? v.kcone[kp0 + base + lane] : base + lane);
       rec = (raw >> 30) & 1;
       sgn = ((raw >> 28) & 1) - ((raw >> 29) & 1);
       j = raw & kListMask;

@@ -417,6 +417,74 @@ __global__ void k_dr_pass(Dev v) {
   }
 }
 
+// Same arithmetic as k_dr_pass, element for element; the forward map a and the
+// old eta~ of the cone are computed / loaded once (first sweep, loads batched by
+// unrolling, n_u fixed at compile time) and kept in the warp's shared memory for
+// the update sweep instead of being recomputed from global memory.
+template <int NUM>
+__global__ void __launch_bounds__(128) k_dr_pass_s(Dev v, int lmax) {
+  extern __shared__ double sm[];
+  const Dims d = v.d;
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gw >= (int64_t)d.B * d.ng) return;
+  const int b = (int)(gw / d.ng), j = (int)(gw % d.ng);
+  if (!v.active[b] || !v.dr_active[b]) return;
+  const int lane = threadIdx.x & 31;
+  const int nx = d.nx, nu = NUM > 0 ? NUM : d.nu;
+  double* sa = sm + (size_t)(threadIdx.x >> 5) * 2 * lmax;
+  double* sy = sa + lmax;
+  const ConeGeom g = cone_geom(v, j);
+  const int64_t ij = (int64_t)b * d.ng + j;
+  const double sg = v.prm.sigma_dr, rs = v.prm.r_s, al = v.prm.alpha_dr, rho = v.prm.rho_admm;
+  const double pit = v.pit[ij], tt = v.tt[ij];
+  const double pi = (sg * pit + rho * v.p[ij] + v.lamp[ij] + rs * tt) / (rho + sg + rs);
+  double* Y = v.Y + (int64_t)b * d.E + g.off;
+  const double* bh = v.bhat + (int64_t)b * d.E + g.off;
+  const double* Bd = v.Bd + (int64_t)b * d.EB + g.offB;
+  const double* Cm = v.Ccur + (int64_t)b * d.T * nx * nu;
+  double n2 = 0.0;
+#pragma unroll 4
+  for (int e = lane; e < g.L; e += 32) {
+    const int kb = e / nx, i = e - kb * nx;
+    double a = (g.kind == 0) ? bh[e] : 0.0;
+    if (kb < g.nbB) {
+      const double* Cr = Cm + ((int64_t)(g.klo + kb) * nx + i) * nu;
+      const double* br = Bd + kb * d.nup;
+      if constexpr (NUM > 0) {
+#pragma unroll
+        for (int m = 0; m < NUM; ++m) a += Cr[m] * br[m];
+      } else {
+        for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
+      }
+    }
+    const double et = Y[e];
+    sa[e] = a;
+    sy[e] = et;
+    const double er = 2.0 * a - et;
+    n2 += er * er;
+  }
+  n2 = warp_sum(n2);
+  double sc;
+  const double tpi = soc_case(2.0 * pi - tt, sqrt(n2), &sc);
+  double d2 = 0.0;
+  for (int e = lane; e < g.L; e += 32) {
+    const double a = sa[e], et = sy[e];
+    const double er = 2.0 * a - et;
+    const double en = et + al * (sc * er - a);
+    Y[e] = en;
+    d2 += (en - et) * (en - et);
+  }
+  d2 = warp_sum(d2);
+  if (lane == 0) {
+    const double ttn = tt + al * (tpi - pi);
+    d2 += (ttn - tt) * (ttn - tt);
+    v.tt[ij] = ttn;
+    v.pit[ij] = pit + al * (pi - pit);
+    v.pt[ij] = pi;
+    v.rdr_part[ij] = d2;
+  }
+}
+
 // r_dr = ||s~^l - s~^{l-1}||_2 per instance; DR stop test.
 __global__ void k_dr_reduce(Dev v) {
   __shared__ double sh[32];
@@ -615,7 +683,21 @@ cudaError_t launch_dr_pass(nrto_handle_s* h, cudaStream_t st) {
   Dev& v = h->dev;
   const Dims& d = v.d;
   if ((int64_t)d.B * d.ng > 0) {
-    k_dr_pass<<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(v);
+    const int lmax = (d.T + 1) * d.nx;                 // longest cone
+    const size_t smem = 4 * 2 * (size_t)lmax * sizeof(double);
+    if (smem <= 100 * 1024) {
+      const unsigned grid = warp_grid((int64_t)d.B * d.ng, 4);
+      if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_dr_pass_s<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_dr_pass_s<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_dr_pass_s<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      }
+      if (d.nu == 4) k_dr_pass_s<4><<<grid, 128, smem, st>>>(v, lmax);
+      else if (d.nu == 7) k_dr_pass_s<7><<<grid, 128, smem, st>>>(v, lmax);
+      else k_dr_pass_s<0><<<grid, 128, smem, st>>>(v, lmax);
+    } else {
+      k_dr_pass<<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(v);
+    }
     h->launches++;
   }
   return cudaGetLastError();

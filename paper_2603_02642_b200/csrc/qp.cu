@@ -863,8 +863,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
   double* gR = v.ru + (int64_t)b * T * nu;            // r_u,k, then du~_k
   double* gS = v.rx + (int64_t)b * (T + 1) * nx;      // S_k = sum_{state j@k} w_j grad_j (atomic)
   double* gU = v.dut + (int64_t)b * T * nu;           // U_k = sum_{ctrl j@k} w_j h'_j   (atomic)
-  const double* __restrict__ Ru = v.Ru + (int64_t)b * T * nu * nu;
-  const double* __restrict__ uh = v.uhat + (int64_t)b * T * nu;
+  const double* __restrict__ cu2 = v.cu2 + (int64_t)b * T * nu;
   const double* __restrict__ Bm = v.Bm + (int64_t)b * T * nx * nu;
   const double* __restrict__ Kf = F.Kf + (int64_t)b * T * nu * nx;
   const double* __restrict__ AclG = F.Acl + (int64_t)b * T * nx * nx;
@@ -897,11 +896,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
   for (int it = 0; it < nits; ++it) {
     it_dbg = it;
     for (int r = tid; r < T * nu; r += nt) {          // r_u (consumes and clears U)
-      const int k = r / nu, m = r % nu;
-      const double* Rm = Ru + (k * nu + m) * nu;
-      const double* uk = uh + k * nu;
-      const double ru = dotn<NUM>(nu, [&](int q) { return Rm[q]; }, [&](int q) { return uk[q]; }, 0.0);
-      const double acc = sq * du[r] + gU[r] - 2.0 * ru;
+      const double acc = sq * du[r] + gU[r] + cu2[r];  // cu2 = -2 R_u u_hat (setup)
       gU[r] = 0.0;
       gR[r] = acc;
     }
@@ -1176,7 +1171,26 @@ __global__ void k_sparse_rows(Dev v) {
   v.rowpk[id] = make_int4(v.knot[j], kind | (nz << 8), (int)w0, (int)w1);
 }
 
+// Setup: c_u,k = -2 R_u,k u_hat_k, the constant part of the QP's r_u (it does not
+// change across QP iterations or outer iterations of one setup).
+__global__ void k_qp_cu(Dev v) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nu = v.d.nu;
+  if (id >= (int64_t)v.d.B * v.d.T * nu) return;
+  const int64_t bk = id / nu;
+  const int m = (int)(id % nu);
+  const double* Rm = v.Ru + (bk * nu + m) * nu;
+  const double* uk = v.uhat + bk * nu;
+  double ru = 0.0;
+  for (int q = 0; q < nu; ++q) ru += Rm[q] * uk[q];
+  v.cu2[id] = -2.0 * ru;
+}
+
 cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
+  {
+    const int64_t m = (int64_t)h->dev.d.B * h->dev.d.T * h->dev.d.nu;
+    if (m > 0) { k_qp_cu<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(h->dev); h->launches++; }
+  }
   const int64_t n = (int64_t)h->dev.d.B * h->dev.d.ng;
   if (n > 0) {
     k_sparse_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->dev);

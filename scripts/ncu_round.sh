@@ -14,5 +14,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fa
    -o gpurun_out/prof_pass python scripts/solve_once.py 512 50 10 > gpurun_out/ncu_pass.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_qp_sparse -s 20 -c 1 \
    -o gpurun_out/prof_qp python scripts/solve_once.py 512 50 10 > gpurun_out/ncu_qp.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_zlist_mma -s 30 -c 1 \
+   -o gpurun_out/prof_zlist python scripts/solve_once.py 512 50 10 > gpurun_out/ncu_zlist.log 2>&1
 timeout 600 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.log 2>&1
 ls -la gpurun_out | head -40
