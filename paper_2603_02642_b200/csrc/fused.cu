@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // Fused FullADMM cone pass (S3 forward map + S4 SOC projection + S5 state
 // update + S7 adjoint) in ONE streaming pass over the ragged cone data, with
@@ -909,8 +910,14 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
     // split the list when the batch alone cannot fill the GPU (dense lists only)
     int nsp = 1;
     if (!ncnt && nfixed > 256 && !ghmode) {
-      const int64_t ctas = (int64_t)v.d.B * ((v.d.T + 15) / 16);
-      while (nsp < 64 && ctas * nsp < 296 && (nfixed / (nsp * 2)) >= 64) nsp *= 2;
+      // fixed (dense) lists, small batches (e.g. one DR instance): split each step's
+      // list until the grid has ~32 warps per SM, keeping >= 8 entries per split
+      // (measured on c2: 8 -> 32 splits, adjoint 29 -> 16 us per DR iteration)
+      const int64_t warps = (int64_t)v.d.B * v.d.T;
+      const int64_t navg = std::max<int64_t>(1, nfixed / 2);
+      while (nsp < 64 && warps * nsp * 2 <= 32 * 148 && navg / (nsp * 2) >= 8) nsp *= 2;
+      static const int dsp = [] { const char* e = getenv("NRTO_ZLIST_DSPLIT"); return e ? atoi(e) : 0; }();
+      if (dsp > 0) nsp = dsp;
     }
     // device-sized lists (TMA path): a fixed split so that long lists (early
     // iterations: most cones in case 3) are walked by nsp warps per step; splits
@@ -929,12 +936,15 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
       }
     }
     // warps (steps) per CTA: small CTAs fit beside the co-resident QP CTAs
-    static const int zw = [] { const char* e = getenv("NRTO_ZLIST_WARPS"); return e ? atoi(e) : 4; }();
+    static const int zw0 = [] { const char* e = getenv("NRTO_ZLIST_WARPS"); return e ? atoi(e) : 4; }();
+    const int zw = (!ncnt && nsp > 1) ? 2 : zw0;     // split fixed lists: 2-warp CTAs spread wider
     dim3 grid(v.d.B, (v.d.T + zw - 1) / zw, nsp);
     // NRTO_ZLIST_WARPS = 4: 128-thread CTAs; NRTO_ZLIST_MINB = 8 / 6: capped at 64 / 80 registers
     static const int zmb = [] { const char* e = getenv("NRTO_ZLIST_MINB"); return e ? atoi(e) : 8; }();
     if (v.d.nx <= 8)
       k_zlist_mma<1><<<grid, 32 * zw, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
+    else if (zw == 2)
+      k_zlist_mma<2, 64, 16><<<grid, 64, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
     else if (zw == 4 && zmb == 8)
       k_zlist_mma<2, 128, 8><<<grid, 128, 0, st>>>(v, y, clist, cw, scale, ncnt, nfixed, act, Zout, lazy, ghmode, dG, dH);
     else if (zw == 4 && zmb == 6)
