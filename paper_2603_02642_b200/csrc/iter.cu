@@ -316,42 +316,69 @@ __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
 //   (Q_v + sigma I + r_s sum A^T A) k = sigma k~ + r_s sum A^T (eta~ - b_hat)
 // per step k: R = sigma K~ + r_s sqrt(tau) (Z - Zb) Psi_k, chain with (W+sigma/2, r_s);
 // then chi~ += alpha (chi - chi~) for the k_v part (11c).
+__device__ __forceinline__ void cpa8_g(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src) : "memory");
+}
+// One CTA per (instance, k).  Every operand (Z, Zb, K~, Psi_k, V, U, den) is
+// staged into shared memory with cp.async first -- one global round trip
+// instead of one per small-matrix loop step (single-instance DR is latency
+// bound); Psi_k / U_k come from the first step of their identical-Psi run.
 __global__ void k_dr_gain(Dev v) {
   extern __shared__ double sm[];
   const Dims d = v.d;
   const int nx = d.nx, nu = d.nu;
+  const int NA = nu * nx, NN = nx * nx, NG = nu * nu;
   const int b = blockIdx.x / d.T, k = blockIdx.x % d.T;
   if (!v.active[b] || !v.dr_active[b]) return;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int64_t bk = (int64_t)b * d.T + k;
   double* sR = sm;
-  double* sX = sR + nu * nx;
+  double* sX = sR + NA;
+  double* sZ = sX + NA;
+  double* sKt = sZ + NA;
+  double* sden = sKt + NA;
+  double* sP = sden + NA;
+  double* sU = sP + NN;
+  double* sV = sU + NN;
+  const int kr = v.Urep[bk];
   const double st = sqrt(v.tau[b]);
-  const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + k) * nx * nx;
   double* Kt = v.Kt + (int64_t)b * d.NK + (int64_t)k * nu * nx;
   const double sg = v.prm.sigma_dr, rs = v.prm.r_s, al = v.prm.alpha_dr;
-  for (int r = tid; r < nu * nx; r += nt) sX[r] = v.Z[bk * nu * nx + r] - v.Zb[bk * nu * nx + r];
+  {
+    const double* Z = v.Z + bk * NA;
+    const double* Pk = v.Psi + ((int64_t)b * (d.T + 1) + kr) * NN;
+    const double* Uk = v.U + ((int64_t)b * d.T + kr) * NN;
+    for (int r = tid; r < NA; r += nt) {
+      cpa8_g(sZ + r, Z + r); cpa8_g(sX + r, v.Zb + bk * NA + r);
+      cpa8_g(sKt + r, Kt + r); cpa8_g(sden + r, v.dr.den + bk * NA + r);
+    }
+    for (int r = tid; r < NN; r += nt) { cpa8_g(sP + r, Pk + r); cpa8_g(sU + r, Uk + r); }
+    for (int r = tid; r < NG; r += nt) cpa8_g(sV + r, v.dr.V + bk * NG + r);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
   __syncthreads();
-  for (int r = tid; r < nu * nx; r += nt) {
+  for (int r = tid; r < NA; r += nt) sX[r] = sZ[r] - sX[r];
+  __syncthreads();
+  for (int r = tid; r < NA; r += nt) {
     const int m = r / nx, i = r % nx;
     double gp = 0.0;
-    for (int q = 0; q < nx; ++q) gp += sX[m * nx + q] * Pk[q * nx + i];
-    sR[r] = sg * Kt[i * nu + m] + rs * st * gp;
+    for (int q = 0; q < nx; ++q) gp += sX[m * nx + q] * sP[q * nx + i];
+    sR[r] = sg * sKt[i * nu + m] + rs * st * gp;
   }
   __syncthreads();
-  chain_solve(v.dr.V + bk * nu * nu, v.U + bk * nx * nx, v.dr.den + bk * nu * nx, sR, sX,
-              nu, nx, tid, nt);
+  chain_solve(sV, sU, sden, sR, sX, nu, nx, tid, nt);
   double* Ko = v.K + (int64_t)b * d.NK + (int64_t)k * nu * nx;
-  for (int r = tid; r < nu * nx; r += nt) {
+  for (int r = tid; r < NA; r += nt) {
     const int m = r / nx, i = r % nx;
     Ko[i * nu + m] = sR[r];
-    Kt[i * nu + m] += al * (sR[r] - Kt[i * nu + m]);
+    Kt[i * nu + m] = sKt[i * nu + m] + al * (sR[r] - sKt[i * nu + m]);
   }
-  for (int r = tid; r < nx * nu; r += nt) {
+  for (int r = tid; r < NA; r += nt) {
     const int i = r / nu, m = r % nu;
     double acc = 0.0;
-    for (int q = 0; q < nx; ++q) acc += Pk[i * nx + q] * sR[m * nx + q];
-    v.Ccur[bk * nx * nu + r] = st * acc;
+    for (int q = 0; q < nx; ++q) acc += sP[i * nx + q] * sR[m * nx + q];
+    v.Ccur[bk * NA + r] = st * acc;
   }
 }
 
@@ -674,7 +701,9 @@ cudaError_t launch_fa_gain(nrto_handle_s* h, cudaStream_t st) {
 cudaError_t launch_dr_gain(nrto_handle_s* h, cudaStream_t st) {
   Dev& v = h->dev;
   const Dims& d = v.d;
-  k_dr_gain<<<d.B * d.T, 128, 2 * d.nu * d.nx * sizeof(double), st>>>(v);
+  const size_t smem = (5 * (size_t)d.nu * d.nx + 2 * (size_t)d.nx * d.nx + (size_t)d.nu * d.nu) * sizeof(double);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_dr_gain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_dr_gain<<<d.B * d.T, 128, smem, st>>>(v);
   h->launches++;
   return cudaGetLastError();
 }
@@ -704,7 +733,8 @@ cudaError_t launch_dr_pass(nrto_handle_s* h, cudaStream_t st) {
 }
 
 cudaError_t launch_dr_reduce(nrto_handle_s* h, cudaStream_t st) {
-  k_dr_reduce<<<h->dev.d.B, 128, 0, st>>>(h->dev);
+  // one partial per thread for n_g <= 1024 (the per-instance sum is a latency chain otherwise)
+  k_dr_reduce<<<h->dev.d.B, h->dev.d.ng >= 512 ? 1024 : 256, 0, st>>>(h->dev);
   h->launches++;
   return cudaGetLastError();
 }
