@@ -134,6 +134,12 @@ struct nrto_handle_s {
   cudaStream_t aux = nullptr;     // low priority: QP
   cudaStream_t hi = nullptr;      // high priority: cone pass chain
   cudaEvent_t ev_proj = nullptr, ev_qp = nullptr, ev_in = nullptr, ev_out = nullptr;
+  // CUDA graph of the fixed-iteration DR loop (api.cu): replayed while the device
+  // state descriptor it was captured with (Dev, by value) is unchanged
+  cudaStream_t gst = nullptr;
+  cudaGraphExec_t dr_exec = nullptr;
+  nrto::Dev dr_key;
+  int64_t dr_graph_launches = 0;
   // persistent staging for host-memory outputs and the active-count poll
   double* stage_ng2 = nullptr;   // [2][B][ng]  margins
   double* stage_b = nullptr;     // [B]         objective

@@ -342,3 +342,28 @@ def test_dr_long_horizon():
     g = gpu_solve(shape, single(shape, data), nrto.NRTO_DR, **kw)
     o = oracle_run(shape, data, nrto.NRTO_DR, **kw)
     assert_parity(g, o, engine=1)
+
+
+@pytest.mark.gpu
+def test_dr_graph_replay_matches_stream_path():
+    """The fixed-iteration DR loop runs as a captured CUDA graph (replayed on the
+    second solve of a handle); with the profiler on it runs launch by launch.
+    Both orders of the same kernels must give the same warm-started result."""
+    _require_gpu()
+    shape, data = CASES["c2"]()
+    kw = dict(max_admm_iter=3, max_dr_iter=10, fixed_iters=1)
+    outs = []
+    for prof in (False, True):
+        s = nrto.InnerSolver(shape, nrto.to_tensors(single(shape, data), device="cuda"), **kw)
+        o = nrto.alloc_out(shape, 1, s.E, device="cuda")
+        s.solve(nrto.NRTO_DR, out=o)
+        s.solve(nrto.NRTO_DR, out=o)            # graph replay (prof off)
+        if prof:
+            s.profile(True)
+        s.solve(nrto.NRTO_DR, out=o)
+        torch.cuda.synchronize()
+        outs.append({k: v.cpu().numpy() for k, v in o.items()})
+        s.close()
+    g, e = outs
+    for k in ("kv", "du", "p", "p_tilde", "lam_p"):
+        assert close(g[k], e[k], tol=1e-12), k
