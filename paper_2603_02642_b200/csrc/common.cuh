@@ -5,6 +5,12 @@
 #include <vector>
 #include "../../include/nrto.h"
 
+// slots of the QP's per-step bulk-copy ring for Acl_k (qp.cu); the TMA pass
+// leaves room for one QP CTA of this size beside it (tma.cu)
+#ifndef QP_RING
+#define QP_RING 8
+#endif
+
 namespace nrto {
 
 // Problem dimensions shared by every instance of a batch.

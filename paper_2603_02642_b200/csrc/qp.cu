@@ -435,7 +435,7 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kQPRing = 8;   // power of two
+constexpr int kQPRing = QP_RING;   // power of two (common.cuh)
 #ifndef QP_MINB
 #define QP_MINB 5
 #endif

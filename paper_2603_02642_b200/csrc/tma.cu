@@ -545,7 +545,7 @@ static int tma_stages(const Dims& d) {
   const TmaGeom G = tma_geom(d.nx, d.nup);
   const size_t fixed = tma_fixed_doubles(d.T, d.nx, d.nu);
   // leave room for one k_qp_sparse CTA beside the pass CTA (overlapped QP)
-  const size_t qp = ((size_t)(d.T + 1) * d.nx + 8 * (size_t)d.nx * d.nx) * sizeof(double);
+  const size_t qp = ((size_t)(d.T + 1) * d.nx + (size_t)QP_RING * d.nx * d.nx) * sizeof(double);
   size_t capb = 225 * 1024;
   if (228 * 1024 > qp + 2048 + 3 * G.stage * sizeof(double) + fixed * sizeof(double))
     capb = std::min<size_t>(capb, 228 * 1024 - 2048 - qp);
