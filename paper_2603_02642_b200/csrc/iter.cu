@@ -512,6 +512,75 @@ __global__ void __launch_bounds__(128) k_dr_pass_s(Dev v, int lmax) {
   }
 }
 
+// Small batches (latency bound, e.g. one c2 instance): one 128-thread CTA per
+// cone instead of one warp, so a long cone (up to (T+1) n_x elements) is covered
+// by 4x the lanes; same element arithmetic as k_dr_pass, the norm is a block
+// reduction (partial sums in a different order).
+template <int NUM>
+__global__ void __launch_bounds__(128) k_dr_pass_c(Dev v, int lmax) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const Dims d = v.d;
+  const int64_t gc = blockIdx.x;
+  if (gc >= (int64_t)d.B * d.ng) return;
+  const int b = (int)(gc / d.ng), j = (int)(gc % d.ng);
+  if (!v.active[b] || !v.dr_active[b]) return;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nx = d.nx, nu = NUM > 0 ? NUM : d.nu;
+  double* sa = sm;
+  double* sy = sa + lmax;
+  const ConeGeom g = cone_geom(v, j);
+  const int64_t ij = (int64_t)b * d.ng + j;
+  const double sg = v.prm.sigma_dr, rs = v.prm.r_s, al = v.prm.alpha_dr, rho = v.prm.rho_admm;
+  const double pit = v.pit[ij], tt = v.tt[ij];
+  const double pi = (sg * pit + rho * v.p[ij] + v.lamp[ij] + rs * tt) / (rho + sg + rs);
+  double* Y = v.Y + (int64_t)b * d.E + g.off;
+  const double* bh = v.bhat + (int64_t)b * d.E + g.off;
+  const double* Bd = v.Bd + (int64_t)b * d.EB + g.offB;
+  const double* Cm = v.Ccur + (int64_t)b * d.T * nx * nu;
+  double n2 = 0.0;
+#pragma unroll 2
+  for (int e = tid; e < g.L; e += nt) {
+    const int kb = e / nx, i = e - kb * nx;
+    double a = (g.kind == 0) ? bh[e] : 0.0;
+    if (kb < g.nbB) {
+      const double* Cr = Cm + ((int64_t)(g.klo + kb) * nx + i) * nu;
+      const double* br = Bd + kb * d.nup;
+      if constexpr (NUM > 0) {
+#pragma unroll
+        for (int m = 0; m < NUM; ++m) a += Cr[m] * br[m];
+      } else {
+        for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
+      }
+    }
+    const double et = Y[e];
+    sa[e] = a;
+    sy[e] = et;
+    const double er = 2.0 * a - et;
+    n2 += er * er;
+  }
+  n2 = block_sum(n2, red);
+  double sc;
+  const double tpi = soc_case(2.0 * pi - tt, sqrt(n2), &sc);
+  double d2 = 0.0;
+  for (int e = tid; e < g.L; e += nt) {
+    const double a = sa[e], et = sy[e];
+    const double er = 2.0 * a - et;
+    const double en = et + al * (sc * er - a);
+    Y[e] = en;
+    d2 += (en - et) * (en - et);
+  }
+  d2 = block_sum(d2, red);
+  if (tid == 0) {
+    const double ttn = tt + al * (tpi - pi);
+    d2 += (ttn - tt) * (ttn - tt);
+    v.tt[ij] = ttn;
+    v.pit[ij] = pit + al * (pi - pit);
+    v.pt[ij] = pi;
+    v.rdr_part[ij] = d2;
+  }
+}
+
 // r_dr = ||s~^l - s~^{l-1}||_2 per instance; DR stop test.
 __global__ void k_dr_reduce(Dev v) {
   __shared__ double sh[32];
@@ -714,7 +783,13 @@ cudaError_t launch_dr_pass(nrto_handle_s* h, cudaStream_t st) {
   if ((int64_t)d.B * d.ng > 0) {
     const int lmax = (d.T + 1) * d.nx;                 // longest cone
     const size_t smem = 4 * 2 * (size_t)lmax * sizeof(double);
-    if (smem <= 100 * 1024) {
+    const int64_t ncone = (int64_t)d.B * d.ng;
+    if (ncone <= 8192 && 2 * (size_t)lmax * sizeof(double) <= 48 * 1024) {   // CTA per cone
+      const size_t sm1 = 2 * (size_t)lmax * sizeof(double);
+      if (d.nu == 4) k_dr_pass_c<4><<<(unsigned)ncone, 128, sm1, st>>>(v, lmax);
+      else if (d.nu == 7) k_dr_pass_c<7><<<(unsigned)ncone, 128, sm1, st>>>(v, lmax);
+      else k_dr_pass_c<0><<<(unsigned)ncone, 128, sm1, st>>>(v, lmax);
+    } else if (smem <= 100 * 1024) {
       const unsigned grid = warp_grid((int64_t)d.B * d.ng, 4);
       if (smem > 48 * 1024) {
         cudaFuncSetAttribute(k_dr_pass_s<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
