@@ -522,7 +522,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
           for (int m = 1; m <= prm.max_dr_iter && e == cudaSuccess; ++m) {
             if (e == cudaSuccess) e = launch_dr_gain(h, h->gst);
             if (e == cudaSuccess) e = launch_dr_pass(h, h->gst);
-            if (e == cudaSuccess) e = launch_adjoint(h, v.Y, nullptr, v.dr_active, h->gst);
+            if (e == cudaSuccess) e = launch_dr_adjoint(h, h->gst);
             if (e == cudaSuccess) e = launch_dr_reduce(h, h->gst);
           }
           if (e == cudaSuccess) e = launch_qp(h, NRTO_DR, l, h->gst);
@@ -549,8 +549,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
       for (int m = 1; m <= prm.max_dr_iter; ++m) {
         CK(timed(NRTO_K_GAIN, launch_dr_gain));
         CK(timed(NRTO_K_PASS, launch_dr_pass));
-        CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
-          return launch_adjoint(hh, hh->dev.Y, nullptr, hh->dev.dr_active, s2); }));
+        CK(timed(NRTO_K_ADJOINT, launch_dr_adjoint));
         CK(timed(NRTO_K_OTHER, launch_dr_reduce));
         if (!prm.fixed_iters && (m % 4) == 0 && m < prm.max_dr_iter) {
           const int c = poll_active(h, dcount, 1, st, &ce);

@@ -237,7 +237,8 @@ cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,
                          double* Zout, cudaStream_t st, int lazy = 0, int ghmode = 0,
-                         double* dG = nullptr, double* dH = nullptr);
+                         double* dG = nullptr, double* dH = nullptr, int prezeroed = 0);
+cudaError_t launch_dr_adjoint(nrto_handle_s* h, cudaStream_t st);
 bool fused_supported(const Dims& d);
 bool tma_supported(const Dims& d);
 cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st);

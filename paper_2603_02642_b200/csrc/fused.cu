@@ -904,7 +904,7 @@ __global__ void k_zero_active(double* Z, int64_t per, int B, const int32_t* act)
 cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist, const double* cw,
                          const double* scale, const int32_t* ncnt, int nfixed, const int32_t* act,
                          double* Zout, cudaStream_t st, int lazy, int ghmode, double* dG,
-                         double* dH) {
+                         double* dH, int prezeroed) {
   Dev& v = h->dev;
   if (v.d.nu <= 8 && v.d.nx <= 16) {
     // split the list when the batch alone cannot fill the GPU (dense lists only)
@@ -924,7 +924,7 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
     // past the list end exit at once, empty splits add nothing
     static const int lsp = [] { const char* e = getenv("NRTO_ZLIST_SPLIT"); return e ? atoi(e) : 1; }();
     if (ncnt && ghmode && lsp > 1) nsp = lsp;
-    if (nsp > 1) {           // zero the slices of the instances that will be accumulated
+    if (nsp > 1 && !prezeroed) {   // zero the slices of the instances that will be accumulated
       const int64_t per = (int64_t)v.d.T * v.d.nu * v.d.nx;
       k_zero_active<<<(unsigned)(((int64_t)v.d.B * per + 255) / 256), 256, 0, st>>>(Zout, per, v.d.B, act);
       h->launches++;

@@ -392,6 +392,11 @@ __global__ void k_dr_pass(Dev v) {
   if (gw >= (int64_t)d.B * d.ng) return;
   const int b = (int)(gw / d.ng), j = (int)(gw % d.ng);
   if (!v.active[b] || !v.dr_active[b]) return;
+  {   // Z is re-accumulated by the (split) adjoint right after this pass: zero it here
+    const int64_t nz = (int64_t)d.T * d.nu * d.nx;
+    double* Zb = v.Z + (int64_t)b * nz;
+    for (int64_t e = (int64_t)j * 32 + (threadIdx.x & 31); e < nz; e += (int64_t)d.ng * 32) Zb[e] = 0.0;
+  }
   const int lane = threadIdx.x & 31;
   const int nx = d.nx, nu = d.nu;
   const ConeGeom g = cone_geom(v, j);
@@ -456,6 +461,11 @@ __global__ void __launch_bounds__(128) k_dr_pass_s(Dev v, int lmax) {
   if (gw >= (int64_t)d.B * d.ng) return;
   const int b = (int)(gw / d.ng), j = (int)(gw % d.ng);
   if (!v.active[b] || !v.dr_active[b]) return;
+  {   // Z is re-accumulated by the (split) adjoint right after this pass: zero it here
+    const int64_t nz = (int64_t)d.T * d.nu * d.nx;
+    double* Zb = v.Z + (int64_t)b * nz;
+    for (int64_t e = (int64_t)j * 32 + (threadIdx.x & 31); e < nz; e += (int64_t)d.ng * 32) Zb[e] = 0.0;
+  }
   const int lane = threadIdx.x & 31;
   const int nx = d.nx, nu = NUM > 0 ? NUM : d.nu;
   double* sa = sm + (size_t)(threadIdx.x >> 5) * 2 * lmax;
@@ -525,6 +535,11 @@ __global__ void __launch_bounds__(128) k_dr_pass_c(Dev v, int lmax) {
   if (gc >= (int64_t)d.B * d.ng) return;
   const int b = (int)(gc / d.ng), j = (int)(gc % d.ng);
   if (!v.active[b] || !v.dr_active[b]) return;
+  {   // Z is re-accumulated by the (split) adjoint right after this pass: zero it here
+    const int64_t nz = (int64_t)d.T * d.nu * d.nx;
+    double* Zb = v.Z + (int64_t)b * nz;
+    for (int64_t e = (int64_t)j * blockDim.x + threadIdx.x; e < nz; e += (int64_t)d.ng * blockDim.x) Zb[e] = 0.0;
+  }
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nx = d.nx, nu = NUM > 0 ? NUM : d.nu;
   double* sa = sm;
@@ -805,6 +820,15 @@ cudaError_t launch_dr_pass(nrto_handle_s* h, cudaStream_t st) {
     h->launches++;
   }
   return cudaGetLastError();
+}
+
+// DR adjoint Z_k = sum_j b_{j,k} eta~_{j,k}^T over every cone; Z was zeroed by the pass.
+cudaError_t launch_dr_adjoint(nrto_handle_s* h, cudaStream_t st) {
+  Dev& v = h->dev;
+  if (v.d.nu <= 8 && v.d.nx <= 16)
+    return launch_zlist(h, v.Y, nullptr, nullptr, nullptr, nullptr, v.d.ng, v.dr_active, v.Z, st, 0, 0,
+                        nullptr, nullptr, 1);
+  return launch_adjoint(h, v.Y, nullptr, v.dr_active, st);
 }
 
 cudaError_t launch_dr_reduce(nrto_handle_s* h, cudaStream_t st) {
