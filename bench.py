@@ -281,6 +281,43 @@ def run_ours(args, rank, world, local_rank):
               "admm_iters_per_s": La / (dms / 1000.0), "ms_per_solve": dms}
         s2.close()
 
+    # single-instance lines of the other configs (latency-bound; CUDA-graph replay of
+    # the fixed-iteration loop): c1 unicycle (both engines), c3 Franka FullADMM
+    singles = None
+    if not args.no_dr and rank == 0:
+        from gen import make_instance
+        from gen.problems import stack_instances
+        singles = {}
+        for cfg, eng, name in (("c1", nrto.NRTO_FULLADMM, "c1_fulladmm"), ("c1", nrto.NRTO_DR, "c1_dr"),
+                               ("c3", nrto.NRTO_FULLADMM, "c3_fulladmm")):
+            shp3, d3 = make_instance(cfg)
+            dd3 = nrto.to_tensors(stack_instances([(shp3, d3)])[1], device=dev)
+            s3 = nrto.InnerSolver(shp3, dd3, fixed_iters=1)
+            o3 = nrto.alloc_out(shp3, 1, s3.E, device=dev, full=False)
+            for _ in range(2):
+                s3.solve(eng, out=o3)
+            torch.cuda.synchronize()
+            e6, e7 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e6.record(stream)
+            for _ in range(3):
+                s3.solve(eng, out=o3)
+            e7.record(stream)
+            torch.cuda.synchronize()
+            sms = e6.elapsed_time(e7) / 3
+            if eng == nrto.NRTO_FULLADMM:
+                it = s3.params.max_iter
+                singles[name] = {"workload": "%s, 1 instance (n_x=%d, n_u=%d, T=%d, n_g=%d), FullADMM, %d iterations, fixed"
+                                 % (cfg, shp3.n_x, shp3.n_u, shp3.T, shp3.n_g, it),
+                                 "inner_iters_per_s": it / (sms / 1000.0), "us_per_iteration": 1000 * sms / it,
+                                 "ms_per_solve": sms}
+            else:
+                La, Ld = s3.params.max_admm_iter, s3.params.max_dr_iter
+                singles[name] = {"workload": "%s, 1 instance (n_x=%d, n_u=%d, T=%d, n_g=%d), NRTO-DR, %d x %d, fixed"
+                                 % (cfg, shp3.n_x, shp3.n_u, shp3.T, shp3.n_g, La, Ld),
+                                 "dr_iters_per_s": La * Ld / (sms / 1000.0), "us_per_dr_iteration": 1000 * sms / (La * Ld),
+                                 "ms_per_solve": sms}
+            s3.close()
+
     # batch-wide residual statistics over NVLink (the only collective)
     max_rp, n_unconv, any_div = batch_stats(out["r_p"], out["status"], device=dev)
 
@@ -330,6 +367,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "dr_engine": dr,
+        "single_instance": singles,
         "residuals": {"max_r_p": max_rp, "unconverged_instances": n_unconv,
                       "any_diverged": any_div},
     }

@@ -451,6 +451,61 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
       if (h->prof) { cudaEventRecord(b, s2); h->recs.push_back({cls, a, b}); }
       return e;
     };
+    // in-order (small batch) fixed-iteration solves: the loop is device-only, so it is
+    // captured once into a CUDA graph (keyed by the device-state descriptor before
+    // the loop) and replayed -- the per-iteration kernels are short, launch gaps matter
+    static const int use_graph_fa = [] { const char* e = getenv("NRTO_GRAPH"); return e ? atoi(e) : 1; }();
+    if (!overlap && prm.fixed_iters && !h->prof && use_graph_fa) {
+      if (!h->gst) CK(cudaStreamCreateWithFlags(&h->gst, cudaStreamNonBlocking));
+      if (!h->ev_in) CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+      if (!h->ev_out) CK(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
+      v.iter = 0; v.ylazy = 0;             // loop-set fields: normalised for the key
+      if (!h->fa_exec || std::memcmp(&h->fa_key, &v, sizeof(Dev)) != 0) {
+        if (h->fa_exec) { cudaGraphExecDestroy(h->fa_exec); h->fa_exec = nullptr; }
+        Dev key;
+        std::memcpy(&key, &v, sizeof(Dev));
+        const int64_t l0 = h->launches;
+        cudaStream_t gs = h->gst;
+        CK(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = cudaSuccess;
+        for (int l = 1; l <= prm.max_iter && e == cudaSuccess; ++l) {
+          v.iter = l;
+          v.ylazy = (v.fused == 2 && l < prm.max_iter) ? 1 : 0;
+          if (v.fused == 0) {
+            e = launch_fa_pass(h, gs);
+            if (e == cudaSuccess) e = launch_adjoint(h, v.Y, v.s, v.active, gs);
+            if (e == cudaSuccess) e = launch_fa_gain(h, gs);
+            if (e == cudaSuccess) e = launch_qp(h, NRTO_FULLADMM, l, gs);
+          } else {
+            e = v.fused == 2 ? launch_fa_tma(h, gs) : launch_fa_fused(h, gs);
+            if (e == cudaSuccess && v.fused == 2) e = launch_fa_ctrl(h, gs);
+            if (e == cudaSuccess) e = launch_project(h, gs);
+            if (e == cudaSuccess)
+              e = launch_zlist(h, v.Y, v.clist, v.cw, nullptr, v.ncorr, 0, v.active, v.Zc, gs, v.ylazy,
+                               v.fused == 2 ? 1 : 0, v.dG, v.dH);
+            if (e == cudaSuccess) e = launch_fa_gain(h, gs);
+            if (e == cudaSuccess) e = wide ? launch_qp_lite(h, NRTO_FULLADMM, l, gs) : launch_qp(h, NRTO_FULLADMM, l, gs);
+          }
+        }
+        cudaGraph_t g = nullptr;
+        const cudaError_t ee = cudaStreamEndCapture(gs, &g);
+        if (e == cudaSuccess) e = ee;
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&h->fa_exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        v.ylazy = 0;
+        if (e != cudaSuccess) { h->fa_exec = nullptr; return cuda_fail(e, "FullADMM loop graph capture"); }
+        h->fa_graph_launches = h->launches - l0;
+        h->launches = l0;
+        std::memcpy(&h->fa_key, &key, sizeof(Dev));
+      }
+      v.iter = prm.max_iter;
+      CK(cudaEventRecord(h->ev_in, st));
+      CK(cudaStreamWaitEvent(h->gst, h->ev_in, 0));
+      CK(cudaGraphLaunch(h->fa_exec, h->gst));
+      CK(cudaEventRecord(h->ev_out, h->gst));
+      CK(cudaStreamWaitEvent(st, h->ev_out, 0));
+      h->launches += h->fa_graph_launches;
+    } else
     for (int l = 1; l <= prm.max_iter; ++l) {
       v.iter = l;
       // lazy y storage needs a known last iteration (it stores every y^L)
@@ -620,6 +675,7 @@ extern "C" nrto_err nrto_destroy(nrto_handle h) {
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->dr_exec) cudaGraphExecDestroy(h->dr_exec);
+  if (h->fa_exec) cudaGraphExecDestroy(h->fa_exec);
   if (h->gst) cudaStreamDestroy(h->gst);
   if (h->dcount) cudaFree(h->dcount);
   if (h->hist_buf) cudaFree(h->hist_buf);

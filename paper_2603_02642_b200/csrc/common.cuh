@@ -146,6 +146,9 @@ struct nrto_handle_s {
   cudaGraphExec_t dr_exec = nullptr;
   nrto::Dev dr_key;
   int64_t dr_graph_launches = 0;
+  cudaGraphExec_t fa_exec = nullptr;   // same for the in-order fixed-iteration FullADMM loop
+  nrto::Dev fa_key;
+  int64_t fa_graph_launches = 0;
   // persistent staging for host-memory outputs and the active-count poll
   double* stage_ng2 = nullptr;   // [2][B][ng]  margins
   double* stage_b = nullptr;     // [B]         objective

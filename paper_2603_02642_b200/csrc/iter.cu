@@ -854,8 +854,12 @@ cudaError_t launch_finish(nrto_handle_s* h, int engine, const nrto_out* o, cudaS
         v, engine, o->nu, o->lam_nu, o->margin_cone, pre);
     h->launches++;
   }
-  k_finish_inst<<<d.B, 128, (d.T + 1) * d.nx * sizeof(double), st>>>(v, o->margin_lin,
-                                                                      o->objective);
+  const size_t fsm = (size_t)(d.T + 1) * d.nx * sizeof(double);   // rollout dx (long horizons > 48 KB)
+  if (fsm > 48 * 1024) {
+    if (fsm > 227 * 1024) return cudaErrorInvalidValue;
+    cudaFuncSetAttribute(k_finish_inst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+  }
+  k_finish_inst<<<d.B, 128, fsm, st>>>(v, o->margin_lin, o->objective);
   h->launches++;
   return cudaGetLastError();
 }

@@ -367,3 +367,31 @@ def test_dr_graph_replay_matches_stream_path():
     g, e = outs
     for k in ("kv", "du", "p", "p_tilde", "lam_p"):
         assert close(g[k], e[k], tol=1e-12), k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["c1", "c3s"])
+def test_fulladmm_graph_replay_matches_stream_path(case):
+    """Small-batch fixed-iteration FullADMM solves run as a captured CUDA graph
+    (replayed from the second solve on); with the profiler on they run launch by
+    launch.  The same solve must give the same result either way, and match the
+    oracle."""
+    _require_gpu()
+    shape, data = CASES[case]()
+    kw = dict(max_iter=6, fixed_iters=1)
+    outs = []
+    for prof in (False, True):
+        s = nrto.InnerSolver(shape, nrto.to_tensors(single(shape, data), device="cuda"), **kw)
+        o = nrto.alloc_out(shape, 1, s.E, device="cuda")
+        s.solve(nrto.NRTO_FULLADMM, out=o)
+        s.solve(nrto.NRTO_FULLADMM, out=o)        # graph replay (prof off)
+        if prof:
+            s.profile(True)
+        s.solve(nrto.NRTO_FULLADMM, out=o)
+        torch.cuda.synchronize()
+        outs.append({k: v.cpu().numpy() for k, v in o.items()})
+        s.close()
+    g, e = outs
+    for k in ("kv", "du", "p", "p_tilde", "lam_p"):
+        assert close(g[k], e[k], tol=1e-12), k
+    assert_parity({k: v for k, v in g.items()}, oracle_run(shape, data, nrto.NRTO_FULLADMM, **kw))
