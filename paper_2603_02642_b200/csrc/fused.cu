@@ -922,8 +922,14 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
     // device-sized lists (TMA path): a fixed split so that long lists (early
     // iterations: most cones in case 3) are walked by nsp warps per step; splits
     // past the list end exit at once, empty splits add nothing
-    static const int lsp = [] { const char* e = getenv("NRTO_ZLIST_SPLIT"); return e ? atoi(e) : 1; }();
+    static const int lsp = [] { const char* e = getenv("NRTO_ZLIST_SPLIT"); return e ? atoi(e) : 0; }();
     if (ncnt && ghmode && lsp > 1) nsp = lsp;
+    if (ncnt && ghmode && lsp == 0) {
+      // small batches (latency bound, e.g. one c3 instance): split the list until the
+      // grid has ~32 warps per SM; the bench batch (B T >= 32 x 148 warps) stays unsplit
+      const int64_t warps = (int64_t)v.d.B * v.d.T;
+      while (nsp < 32 && warps * nsp * 2 <= 32 * 148) nsp *= 2;
+    }
     if (nsp > 1 && !prezeroed) {   // zero the slices of the instances that will be accumulated
       const int64_t per = (int64_t)v.d.T * v.d.nu * v.d.nx;
       k_zero_active<<<(unsigned)(((int64_t)v.d.B * per + 255) / 256), 256, 0, st>>>(Zout, per, v.d.B, act);
@@ -937,7 +943,7 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
     }
     // warps (steps) per CTA: small CTAs fit beside the co-resident QP CTAs
     static const int zw0 = [] { const char* e = getenv("NRTO_ZLIST_WARPS"); return e ? atoi(e) : 4; }();
-    const int zw = (!ncnt && nsp > 1) ? 2 : zw0;     // split fixed lists: 2-warp CTAs spread wider
+    const int zw = (nsp > 1) ? 2 : zw0;              // split lists: 2-warp CTAs spread wider
     dim3 grid(v.d.B, (v.d.T + zw - 1) / zw, nsp);
     // NRTO_ZLIST_WARPS = 4: 128-thread CTAs; NRTO_ZLIST_MINB = 8 / 6: capped at 64 / 80 registers
     static const int zmb = [] { const char* e = getenv("NRTO_ZLIST_MINB"); return e ? atoi(e) : 8; }();
