@@ -560,7 +560,9 @@ size_t tma_smem_bytes(const Dims& d) {
 }
 
 bool tma_supported(const Dims& d) {
-  return (d.nx % 2 == 0) && d.nx <= 16 && d.nu <= 8 && d.T <= 111 && tma_stages(d) >= 3;
+  // T <= 415: the pass keeps D_k of the whole horizon in shared memory (tma_stages
+  // checks that it fits with >= 3 stages) and unrolls up to 26 chunks per tile
+  return (d.nx % 2 == 0) && d.nx <= 16 && d.nu <= 8 && d.T <= 415 && tma_stages(d) >= 3;
 }
 
 template <int NTI, int NKS, int KK, int NXE = 0, int NUE = 0, int NW = 16>
@@ -587,11 +589,14 @@ cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st) {
   const int nti = (d.nx + 7) / 8, nks = (d.nu + 3) / 4;
   cudaError_t e = cudaSuccess;
   if (h->dev.nwitems > 0) {
-    if (d.nx == 14 && d.nu == 7 && d.T >= 64) e = launch_tma_t<2, 2, 7, 14, 7, TMA_NW>(h, st);
+    // KK = chunks of 16 blocks per tile: covers K <= 16 KK - 1
+    if (d.nx == 14 && d.nu == 7 && d.T >= 64 && d.T < 112) e = launch_tma_t<2, 2, 7, 14, 7, TMA_NW>(h, st);
     else if (d.nx == 12 && d.nu == 4 && d.T >= 32 && d.T < 64) e = launch_tma_t<2, 1, 4, 12, 4>(h, st);
     else if (d.T < 32) e = launch_tma_k<2>(h, nti, nks, st);
     else if (d.T < 64) e = launch_tma_k<4>(h, nti, nks, st);
-    else e = launch_tma_k<7>(h, nti, nks, st);
+    else if (d.T < 112) e = launch_tma_k<7>(h, nti, nks, st);
+    else if (d.T < 208) e = launch_tma_k<13>(h, nti, nks, st);
+    else e = launch_tma_k<26>(h, nti, nks, st);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
