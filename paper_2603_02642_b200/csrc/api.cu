@@ -442,6 +442,9 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
       CK(cudaEventCreateWithFlags(&h->ev_qp, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));
+      CK(cudaStreamCreateWithPriority(&h->hi2, cudaStreamNonBlocking, hp));
+      CK(cudaEventCreateWithFlags(&h->ev_g, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_c, cudaEventDisableTiming));
     }
     cudaStream_t st2 = h->aux;
     const cudaStream_t user_st = st;
@@ -523,8 +526,18 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
         CK(timed(NRTO_K_GAIN, launch_fa_gain));
         CK(timed_qp(NRTO_FULLADMM, l));
       } else {
+        // overlapped mode: the control-cone kernel (needs D from gain(l-1) only) runs on
+        // a second high-priority stream beside the state-cone pass
+        const bool ctrl_side = overlap && v.fused == 2;
+        if (ctrl_side) {
+          CK(cudaEventRecord(h->ev_g, st));
+          CK(cudaStreamWaitEvent(h->hi2, h->ev_g, 0));
+          CK(timed2(h->hi2, NRTO_K_CTRL, [&](cudaStream_t s2) { return launch_fa_ctrl(h, s2); }));
+          CK(cudaEventRecord(h->ev_c, h->hi2));
+        }
         CK(timed(NRTO_K_PASS, v.fused == 2 ? launch_fa_tma : launch_fa_fused));
-        if (v.fused == 2) CK(timed(NRTO_K_CTRL, launch_fa_ctrl));
+        if (v.fused == 2 && !ctrl_side) CK(timed(NRTO_K_CTRL, launch_fa_ctrl));
+        if (ctrl_side) CK(cudaStreamWaitEvent(st, h->ev_c, 0));
         if (overlap && l > 1) CK(cudaStreamWaitEvent(st, h->ev_qp, 0));
         CK(timed(NRTO_K_OTHER, launch_project));
         if (overlap) {
@@ -682,6 +695,9 @@ extern "C" nrto_err nrto_destroy(nrto_handle h) {
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->dr_exec) cudaGraphExecDestroy(h->dr_exec);
+  if (h->hi2) cudaStreamDestroy(h->hi2);
+  if (h->ev_g) cudaEventDestroy(h->ev_g);
+  if (h->ev_c) cudaEventDestroy(h->ev_c);
   if (h->fa_exec) cudaGraphExecDestroy(h->fa_exec);
   if (h->gst) cudaStreamDestroy(h->gst);
   if (h->dcount) cudaFree(h->dcount);

@@ -139,6 +139,8 @@ struct nrto_handle_s {
   // second stream for the QP(l) || pass(l+1) overlap (fixed-iteration mode)
   cudaStream_t aux = nullptr;     // low priority: QP
   cudaStream_t hi = nullptr;      // high priority: cone pass chain
+  cudaStream_t hi2 = nullptr;     // high priority: control cones beside the pass
+  cudaEvent_t ev_g = nullptr, ev_c = nullptr;
   cudaEvent_t ev_proj = nullptr, ev_qp = nullptr, ev_in = nullptr, ev_out = nullptr;
   // CUDA graph of the fixed-iteration DR loop (api.cu): replayed while the device
   // state descriptor it was captured with (Dev, by value) is unchanged
