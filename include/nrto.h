@@ -40,6 +40,11 @@
  *   - Every call is asynchronous on the stream it is given (a cudaStream_t
  *     passed as void*, NULL = legacy default stream) unless a HOST memory
  *     flag forces staging copies; results are valid after the stream syncs.
+ *     Internally nrto_inner_solve may run work on handle-owned streams (the
+ *     overlapped QP, the control-cone kernel) and, for fixed-iteration solves
+ *     without profiling, replay a CUDA graph of the whole iteration loop that
+ *     it captured on an earlier call with the same device state; all of it is
+ *     joined back to `stream` by events before the call's outputs are written.
  *
  * Errors: functions return nrto_err; no C++ exception crosses the ABI.  On a
  * non-OK return nrto_last_error() gives a thread-local message.  Per-instance
