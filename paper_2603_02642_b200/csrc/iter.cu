@@ -195,42 +195,55 @@ __global__ void k_fa_gain(Dev v, int mode, const double* kin, double* kout) {
 // Warp-level versions: one warp per (instance, step), 8 per CTA (the 7x14
 // chain has 98 outputs, so a CTA per step mostly idles and the tiny CTAs
 // crowd the SMs the concurrently running QP needs).
-__device__ void chain_solve_w(const double* V, const double* U, const double* den,
-                              double* sR, double* sX, int nu, int nx, int lane) {
+// NXC, NUC > 0: sizes fixed at compile time (bench shapes; loops fully unrolled,
+// same summation order as the runtime-size version).
+template <int NXC = 0, int NUC = 0>
+__device__ __forceinline__ void chain_solve_w(const double* V, const double* U, const double* den,
+                                              double* sR, double* sX, int nu_rt, int nx_rt, int lane) {
+  const int nx = NXC > 0 ? NXC : nx_rt, nu = NUC > 0 ? NUC : nu_rt;
+#pragma unroll
   for (int r = lane; r < nu * nx; r += 32) {
     const int a = r / nx, c = r % nx;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nu; ++q) acc += V[q * nu + a] * sR[q * nx + c];
     sX[r] = acc;
   }
   __syncwarp();
+#pragma unroll
   for (int r = lane; r < nu * nx; r += 32) {
     const int a = r / nx, c = r % nx;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[q * nx + c];
     sR[r] = acc * den[r];
   }
   __syncwarp();
+#pragma unroll
   for (int r = lane; r < nu * nx; r += 32) {
     const int a = r / nx, c = r % nx;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nu; ++q) acc += V[a * nu + q] * sR[q * nx + c];
     sX[r] = acc;
   }
   __syncwarp();
+#pragma unroll
   for (int r = lane; r < nu * nx; r += 32) {
     const int a = r / nx, c = r % nx;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[c * nx + q];
     sR[r] = acc;
   }
   __syncwarp();
 }
 
+template <int NXC = 0, int NUC = 0>
 __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
   extern __shared__ double sm[];
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu;
+  const int nx = NXC > 0 ? NXC : d.nx, nu = NUC > 0 ? NUC : d.nu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (gw >= (int64_t)d.B * d.T) return;
@@ -255,9 +268,12 @@ __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
     const double cl = (v.iter == 1) ? 0.5 : 1.0;
     const double* Gk = v.G + bk * nu * nu;
     const double* Dk = v.D + bk * nx * nu;
-    for (int r = lane; r < nu * nx; r += 32) {
+#pragma unroll
+  #pragma unroll
+  for (int r = lane; r < nu * nx; r += 32) {
       const int m = r / nx, i = r % nx;
       double pr = v.H[bk * nu * nx + r];
+#pragma unroll
       for (int q = 0; q < nu; ++q) pr += Gk[m * nu + q] * Dk[i * nu + q];
       sX[r] = cl * pr + v.Zc[bk * nu * nx + r] + v.Zctrl[bk * nu * nx + r] - v.Zb[bk * nu * nx + r];
       sK[r] = Kb[i * nu + m];
@@ -272,7 +288,9 @@ __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
       for (int r = lane; r < nu * nu; r += 32) v.G[bk * nu * nu + r] += v.dG[bk * nu * nu + r];
     }
   } else {
-    for (int r = lane; r < nu * nx; r += 32) {
+#pragma unroll
+  #pragma unroll
+  for (int r = lane; r < nu * nx; r += 32) {
       double z = v.Zc[bk * nu * nx + r];
       const double* zp = v.Zpart + ((int64_t)b * v.nsplit * d.T + k) * nu * nx + r;
       for (int sp = 0; sp < v.nsplit; ++sp) z += zp[(int64_t)sp * d.T * nu * nx];
@@ -284,23 +302,29 @@ __global__ void __launch_bounds__(256) k_fa_gain_w(Dev v) {
   if (k == 0 && lane == 0) v.ncorr[b] = 0;      // correction list consumed
   __syncwarp();
   const double rho = v.prm.rho;
+#pragma unroll
   for (int r = lane; r < nu * nx; r += 32) {
     const int m = r / nx, i = r % nx;
     double gp = 0.0, wk = 0.0;
+#pragma unroll
     for (int q = 0; q < nx; ++q) gp += sX[m * nx + q] * Pk[q * nx + i];
+#pragma unroll
     for (int q = 0; q < nu; ++q) wk += Wk[m * nu + q] * sK[q * nx + i];
     sR[r] = 2.0 * wk + rho * st * gp;
   }
   __syncwarp();
-  chain_solve_w(v.fa.V + bk * nu * nu, v.U + ((int64_t)b * d.T + kr) * nx * nx, v.fa.den + bk * nu * nx, sR, sX,
+  chain_solve_w<NXC, NUC>(v.fa.V + bk * nu * nu, v.U + ((int64_t)b * d.T + kr) * nx * nx, v.fa.den + bk * nu * nx, sR, sX,
                 nu, nx, lane);
+#pragma unroll
   for (int r = lane; r < nu * nx; r += 32) {
     const int m = r / nx, i = r % nx;
     Kb[i * nu + m] = sR[r];
   }
+#pragma unroll
   for (int r = lane; r < nx * nu; r += 32) {    // C = sqrt(tau) Psi K^T ; D = 2C - Cold
     const int i = r / nu, m = r % nu;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nx; ++q) acc += Pk[i * nx + q] * sR[m * nx + q];
     const double c = st * acc;
     const int64_t idx = bk * nx * nu + r;
@@ -773,7 +797,11 @@ cudaError_t launch_fa_gain(nrto_handle_s* h, cudaStream_t st) {
     const int64_t nw = (int64_t)d.B * d.T;
     // small CTAs (NRTO_GAIN_WARPS, default 4) fit beside the co-resident QP CTAs
     static const int gwp = [] { const char* e = getenv("NRTO_GAIN_WARPS"); return e ? atoi(e) : 4; }();
-    k_fa_gain_w<<<(unsigned)((nw + gwp - 1) / gwp), 32 * gwp, gwp * 3 * d.nu * d.nx * sizeof(double), st>>>(v);
+    const unsigned gg = (unsigned)((nw + gwp - 1) / gwp);
+    const size_t gsm = gwp * 3 * d.nu * d.nx * sizeof(double);
+    if (d.nx == 14 && d.nu == 7) k_fa_gain_w<14, 7><<<gg, 32 * gwp, gsm, st>>>(v);
+    else if (d.nx == 12 && d.nu == 4) k_fa_gain_w<12, 4><<<gg, 32 * gwp, gsm, st>>>(v);
+    else k_fa_gain_w<><<<gg, 32 * gwp, gsm, st>>>(v);
     h->launches++;
     return cudaGetLastError();
   }

@@ -379,7 +379,8 @@ k_fa_ctrl(Dev v) {
       for (int m = 0; m < 8; ++m) bm[m] = (m < nu) ? bj[m] : 0.0;
       double y = 0.0;
       if (lane < nx) {
-        y = (sj != 1.0) ? (1.0 - sj) * Y[off + lane] : 0.0;
+        // history term (1 - s^{l-1}) y^{l-1}; at l = 1 it is lam_nu^0 = 0 by definition
+        y = (v.iter > 1 && sj != 1.0) ? (1.0 - sj) * Y[off + lane] : 0.0;
 #pragma unroll
         for (int m = 0; m < 8; ++m) y += drow[m] * bm[m];
         Y[off + lane] = y;
