@@ -93,11 +93,14 @@ __global__ void k_adjoint(Dev v, const double* __restrict__ y, const double* __r
 
 // Gain chain solve for one (instance, step): K = V [(V^T R U) ./ den] U^T,
 // R given in sR (nu x nx).  Uses scratch sX (nu x nx); nt threads cooperate.
-__device__ void chain_solve(const double* V, const double* U, const double* den,
-                            double* sR, double* sX, int nu, int nx, int tid, int nt) {
+template <int NXC = 0, int NUC = 0>
+__device__ __forceinline__ void chain_solve(const double* V, const double* U, const double* den,
+                                            double* sR, double* sX, int nu_rt, int nx_rt, int tid, int nt) {
+  const int nx = NXC > 0 ? NXC : nx_rt, nu = NUC > 0 ? NUC : nu_rt;
   for (int r = tid; r < nu * nx; r += nt) {        // sX = V^T R
     const int a = r / nx, c = r % nx;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nu; ++q) acc += V[q * nu + a] * sR[q * nx + c];
     sX[r] = acc;
   }
@@ -105,6 +108,7 @@ __device__ void chain_solve(const double* V, const double* U, const double* den,
   for (int r = tid; r < nu * nx; r += nt) {        // sR = (sX U) ./ den
     const int a = r / nx, c = r % nx;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[q * nx + c];
     sR[r] = acc * den[r];
   }
@@ -112,6 +116,7 @@ __device__ void chain_solve(const double* V, const double* U, const double* den,
   for (int r = tid; r < nu * nx; r += nt) {        // sX = V sR
     const int a = r / nx, c = r % nx;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nu; ++q) acc += V[a * nu + q] * sR[q * nx + c];
     sX[r] = acc;
   }
@@ -119,6 +124,7 @@ __device__ void chain_solve(const double* V, const double* U, const double* den,
   for (int r = tid; r < nu * nx; r += nt) {        // sR = sX U^T  (= K)
     const int a = r / nx, c = r % nx;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[c * nx + q];
     sR[r] = acc;
   }
@@ -348,10 +354,11 @@ __device__ __forceinline__ void cpa8_g(double* dst, const double* src) {
 // staged into shared memory with cp.async first -- one global round trip
 // instead of one per small-matrix loop step (single-instance DR is latency
 // bound); Psi_k / U_k come from the first step of their identical-Psi run.
+template <int NXC = 0, int NUC = 0>
 __global__ void k_dr_gain(Dev v) {
   extern __shared__ double sm[];
   const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu;
+  const int nx = NXC > 0 ? NXC : d.nx, nu = NUC > 0 ? NUC : d.nu;
   const int NA = nu * nx, NN = nx * nx, NG = nu * nu;
   const int b = blockIdx.x / d.T, k = blockIdx.x % d.T;
   if (!v.active[b] || !v.dr_active[b]) return;
@@ -387,11 +394,12 @@ __global__ void k_dr_gain(Dev v) {
   for (int r = tid; r < NA; r += nt) {
     const int m = r / nx, i = r % nx;
     double gp = 0.0;
+#pragma unroll
     for (int q = 0; q < nx; ++q) gp += sX[m * nx + q] * sP[q * nx + i];
     sR[r] = sg * sKt[i * nu + m] + rs * st * gp;
   }
   __syncthreads();
-  chain_solve(sV, sU, sden, sR, sX, nu, nx, tid, nt);
+  chain_solve<NXC, NUC>(sV, sU, sden, sR, sX, nu, nx, tid, nt);
   double* Ko = v.K + (int64_t)b * d.NK + (int64_t)k * nu * nx;
   for (int r = tid; r < NA; r += nt) {
     const int m = r / nx, i = r % nx;
@@ -401,6 +409,7 @@ __global__ void k_dr_gain(Dev v) {
   for (int r = tid; r < NA; r += nt) {
     const int i = r / nu, m = r % nu;
     double acc = 0.0;
+#pragma unroll
     for (int q = 0; q < nx; ++q) acc += sP[i * nx + q] * sR[m * nx + q];
     v.Ccur[bk * NA + r] = st * acc;
   }
@@ -814,8 +823,10 @@ cudaError_t launch_dr_gain(nrto_handle_s* h, cudaStream_t st) {
   Dev& v = h->dev;
   const Dims& d = v.d;
   const size_t smem = (5 * (size_t)d.nu * d.nx + 2 * (size_t)d.nx * d.nx + (size_t)d.nu * d.nu) * sizeof(double);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_dr_gain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_dr_gain<<<d.B * d.T, 128, smem, st>>>(v);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_dr_gain<>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (d.nx == 12 && d.nu == 4) k_dr_gain<12, 4><<<d.B * d.T, 128, smem, st>>>(v);
+  else if (d.nx == 14 && d.nu == 7) k_dr_gain<14, 7><<<d.B * d.T, 128, smem, st>>>(v);
+  else k_dr_gain<><<<d.B * d.T, 128, smem, st>>>(v);
   h->launches++;
   return cudaGetLastError();
 }
