@@ -233,6 +233,18 @@ def test_batch_parity_c5_shape():
         assert_parity(g, o, i=i)
 
 
+def test_dr_batch_parity_graph():
+    """A small batch through the DR engine (fixed iterations: CUDA-graph replay,
+    split fixed-list adjoint, CTA-per-cone pass) matches the oracle per instance."""
+    items = [make_quad(2, i, T=12, n_obs=3) for i in range(3)]
+    shape, batch = stack_instances(items)
+    kw = dict(max_admm_iter=2, max_dr_iter=8, fixed_iters=1)
+    g = gpu_solve(shape, batch, nrto.NRTO_DR, **kw)
+    for i, (_, d) in enumerate(items):
+        o = oracle_run(shape, d, nrto.NRTO_DR, **kw)
+        assert_parity(g, o, i=i, engine=1)
+
+
 def test_batch_per_instance_freeze():
     """Instances converge at different iterations and are frozen (R12)."""
     items = [make_unicycle(1, i) for i in range(5)]
