@@ -235,7 +235,6 @@ cudaError_t launch_count_active(nrto_handle_s* h, int32_t* d_count, int dr, cuda
 int read_setup_error(cudaStream_t st);
 cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st);
 cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st);
-cudaError_t launch_relayout(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_gram_tiles(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_ctrl(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_fused(nrto_handle_s* h, cudaStream_t st);

@@ -446,38 +446,6 @@ cudaError_t launch_project(nrto_handle_s* h, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Tile-interleaved copies of b_hat and b (state tiles), one CTA per (instance, tile):
-//   bhat_t[b][ttb0 + (k nc + c) n_x + i] = bhat[b][off_c + k n_x + i],   k = 0..K
-//   Bd_t[b][ttb1 + (k nc + c) nup + m]   = Bd[b][offB_c + k nup + m],    k = 0..K-1
-__global__ void k_relayout(Dev v) {
-  const int t = blockIdx.x, b = blockIdx.y;
-  const int* tl = v.tiles + (int64_t)t * kTI;
-  const int K = tl[1], nc = tl[2];
-  const int nx = v.d.nx, nup = v.d.nup;
-  const double* bh = v.bhat + (int64_t)b * v.d.E;
-  const double* bd = v.Bd + (int64_t)b * v.d.EB;
-  double* oh = v.bhat_t + (int64_t)b * v.Est + v.ttb[2 * t];
-  double* ob = v.Bd_t + (int64_t)b * v.EBst + v.ttb[2 * t + 1];
-  const int nh = (K + 1) * nc * nx, nbb = K * nc * nup;
-  for (int r = threadIdx.x; r < nh; r += blockDim.x) {
-    const int i = r % nx, c = (r / nx) % nc, k = r / (nx * nc);
-    oh[r] = bh[v.off[tl[4 + c]] + (int64_t)k * nx + i];
-  }
-  for (int r = threadIdx.x; r < nbb; r += blockDim.x) {
-    const int m = r % nup, c = (r / nup) % nc, k = r / (nup * nc);
-    ob[r] = bd[v.offB[tl[4 + c]] + (int64_t)k * nup + m];
-  }
-}
-
-cudaError_t launch_relayout(nrto_handle_s* h, cudaStream_t st) {
-  const Dev& v = h->dev;
-  if (v.nstate_tiles > 0 && v.d.B > 0) {
-    k_relayout<<<dim3(v.nstate_tiles, v.d.B), 256, 0, st>>>(v);
-    h->launches++;
-  }
-  return cudaGetLastError();
-}
-
 // G0_k = sum_{state c, K_c > k} b_{c,k} b_{c,k}^T, H0_k = sum b_{c,k} b_hat_{c,k}^T (= Zb_k,
 // control rows have b_hat = 0), one warp per (instance, k), from the tile layout: the
 // 8 cones of a tile at block k are one contiguous slab; DMMA over the cone index.
