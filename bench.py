@@ -356,6 +356,9 @@ def run_ours(args, rank, world, local_rank):
         "cone_elements_per_s": value * E,
         "sl_iteration_wall_clock_ms": (e2e or {}).get("sl_iteration_wall_clock_ms"),
         "kernel_ms_per_step": kernel_ms,
+        "kernel_ms_note": ("CUDA-event time per kernel class on its own stream; qp (low-priority "
+                           "stream) and ctrl (second high-priority stream) run concurrently with "
+                           "pass / adjoint / gain, so the classes overlap and do not add up to the step"),
         "roofline": {"bound": "hbm", "kernel": "k_fa_tma: fused state-cone pass (S3 forward map + "
                                                 "S4 SOC norms + S5 state update)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
