@@ -2,6 +2,7 @@
 // fused with the dual update and the residual / termination test of the outer
 // iteration: FullADMM (16) + P:505-507, or NRTO-ADMM (5c).
 #include "common.cuh"
+#include <algorithm>
 
 namespace nrto {
 
@@ -1228,7 +1229,11 @@ cudaError_t launch_qp(nrto_handle_s* h, int engine, int l, cudaStream_t st) {
   if (stageA || qp_smem(d, 0) <= lim) {
     const size_t smem = qp_smem(d, stageA);
     cudaFuncSetAttribute(k_qp_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_qp_staged<<<d.B, 1024, smem, st>>>(h->dev, engine, l, stageA);
+    // threads: enough for the widest phase (rows, (T+1) n_x state entries), at most
+    // 1024 -- tiny instances (c1) synchronise 2 warps instead of 32 per phase
+    int nth = std::max(d.ng, (d.T + 1) * d.nx);
+    nth = std::min(1024, std::max(64, (nth + 31) / 32 * 32));
+    k_qp_staged<<<d.B, nth, smem, st>>>(h->dev, engine, l, stageA);
   } else {
     k_qp<<<d.B, 128, 0, st>>>(h->dev, engine, l);
   }
