@@ -257,28 +257,52 @@ def panda_ee(q: np.ndarray) -> np.ndarray:
 
 
 def make_franka(cfg: int, i: int, T: int = 100, dt: float = 0.05, tau: float = 0.01,
-                sigma0: float = 0.2, sigmad: float = 0.2, r_obs: float = 0.1,
-                r_trust: float = 2.0, r_goal: float = 0.02, jitter: bool = False):
+                sigma0: float = 0.1, sigmad: float = 0.1, r_obs: float = 0.1,
+                r_trust: float = 2.0, r_goal: float = 0.3, jitter: bool = False,
+                near: float = 0.97, sway: float = 0.3, jit_q: float = 0.05,
+                nnear: int = 4, t_hold: float = 0.5, ru: float = 0.01,
+                vfrac: float = 0.985, n_cyc: float = 2.0):
     rng = _rng(cfg, i)
     base = _rng(cfg, 0) if jitter else rng  # c5: shared scene, per-instance jitter
     n_x, n_u = 14, 7
     mid, half = 0.5 * (_FQMIN + _FQMAX), 0.5 * (_FQMAX - _FQMIN)
     qa = mid + 0.8 * half * base.uniform(-1, 1, 7)
     qb = mid + 0.8 * half * base.uniform(-1, 1, 7)
-    # two joints are driven close to a limit so that limit rows become active
-    for jj in base.choice(7, 2, replace=False):
-        qb[jj] = mid[jj] + 0.97 * half[jj] * (1 if base.uniform() < 0.5 else -1)
+    qa[[0, 2]] = mid[[0, 2]] + 0.2 * half[[0, 2]] * base.uniform(-1, 1, 2)
+    # nnear of the joints {2,4,5,6,7} are driven close to a limit (held there from
+    # t_hold on) so that their robust position rows bind; joints 1 and 3 sweep
+    # back and forth at vfrac of their velocity limit (clipped-sine velocity
+    # profile with flat cruise phases) so that robust velocity rows bind; any
+    # remaining joint sways on top of its transfer
+    near_js = base.choice(np.array([1, 3, 4, 5, 6]), nnear, replace=False)
+    cruise_js = np.array([0, 2])
+    for jj in near_js:
+        qb[jj] = mid[jj] + near * half[jj] * (1 if base.uniform() < 0.5 else -1)
     obs_dir = base.standard_normal(3)
-    clear = base.uniform(0.05, 0.25) * 0.2
+    clear = base.uniform(0.03, 0.08)
+    ph = base.uniform(0, 1)
     if jitter:  # c5: x_bar_0 ~ N(0, 0.05^2), endpoint jitter, obstacle +-5 cm
-        qa = np.clip(qa + rng.normal(0, 0.05, 7), _FQMIN + 0.02 * half, _FQMAX - 0.02 * half)
-        qb = np.clip(qb + rng.normal(0, 0.05, 7), _FQMIN + 0.02 * half, _FQMAX - 0.02 * half)
+        qa = np.clip(qa + rng.normal(0, jit_q, 7), _FQMIN + 0.02 * half, _FQMAX - 0.02 * half)
+        qb = np.clip(qb + rng.normal(0, jit_q, 7), _FQMIN + 0.02 * half, _FQMAX - 0.02 * half)
+        # the held joints never end closer to their limit than `near`
+        qb[near_js] = np.clip(qb[near_js], mid[near_js] - near * half[near_js],
+                              mid[near_js] + near * half[near_js])
     t = np.arange(T + 1) / T
-    s = 0.5 * (1 - np.cos(math.pi * t))
-    q = qa[None, :] + s[:, None] * (qb - qa)[None, :]
-    # a 4-period sway on top of the transfer so that velocity / torque rows bind
-    amp = np.array([0.15, 0.15, 0.15, 0.15, 0.35, 0.35, 0.35])
+    th = np.full(7, 1.0)
+    th[near_js] = t_hold
+    s = 0.5 * (1 - np.cos(math.pi * np.minimum(t[:, None] / th[None, :], 1.0)))
+    q = qa[None, :] + s * (qb - qa)[None, :]
+    # a 4-period sway on the free joints so that velocity / torque rows vary
+    amp = sway * np.array([0.15, 0.15, 0.15, 0.15, 0.35, 0.35, 0.35])
+    amp[near_js] = 0.0
+    amp[cruise_js] = 0.0
     q = q + np.sin(8 * math.pi * t)[:, None] * np.sin(math.pi * t)[:, None] * amp[None, :]
+    # cruise joints: dq = vfrac * dq_max * clip(1.6 sin(2 pi (n_cyc t + ph)), -1, 1),
+    # position = running sum (semi-implicit Euler), centred on the joint's mid-range
+    vel = np.clip(1.6 * np.sin(2 * math.pi * (n_cyc * t[1:] + ph)), -1.0, 1.0)
+    for jj in cruise_js:
+        qc = np.concatenate([[0.0], np.cumsum(vfrac * _FDQMAX[jj] * vel * dt)])
+        q[:, jj] = qa[jj] - 0.5 * (qc.max() + qc.min()) + qc
     dq = np.zeros((T + 1, 7))
     dq[1:] = (q[1:] - q[:-1]) / dt          # semi-implicit Euler
     tauu = _FI * (dq[1:] - dq[:-1]) / dt + _FD * dq[:-1]
@@ -294,6 +318,15 @@ def make_franka(cfg: int, i: int, T: int = 100, dt: float = 0.05, tau: float = 0
     center = ee[kc] + od * (r_obs + clear)
     if jitter:
         center = center + rng.uniform(-0.05, 0.05, 3)
+    # the nominal keeps its clearance at EVERY knot (no row violated at the nominal)
+    # (and a wider berth away from the encounter knot kc)
+    need = r_obs + clear + 0.1 * np.minimum(1.0, np.abs(np.arange(T + 1) - kc) / 20.0)
+    for _ in range(2000):
+        dist = np.linalg.norm(ee - center[None, :], axis=1)
+        kmin = int(np.argmin(dist - need))
+        if dist[kmin] >= need[kmin]:
+            break
+        center = center + 0.002 * (center - ee[kmin]) / max(dist[kmin], 1e-9)
     h = 1e-6
     Jp = np.empty((T + 1, 3, 7))
     for c in range(7):
@@ -328,7 +361,7 @@ def make_franka(cfg: int, i: int, T: int = 100, dt: float = 0.05, tau: float = 0
     shape = Shape(n_x, n_u, T, np.array(knot, np.int32), np.array(kind, np.int8))
     data = dict(A=A, B=B, grad=np.array(grad), g0=np.array(g0),
                 Psi=_psi_blocks(base, n_x, T, sigma0, sigmad), tau=float(tau),
-                W_K=np.tile(np.eye(n_u), (T, 1, 1)), R_u=np.tile(0.1 * np.eye(n_u), (T, 1, 1)),
+                W_K=np.tile(np.eye(n_u), (T, 1, 1)), R_u=np.tile(ru * np.eye(n_u), (T, 1, 1)),
                 u_hat=tauu, r_trust=float(r_trust))
     return shape, data
 

@@ -202,6 +202,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
     }
   }
   v.fused = use_tma ? 2 : ((fused_supported(d) && ntiles > 0) ? 1 : 0);
+  v.nsm = nsm;
   v.nctrl = nctrl;
   v.ntiles = ntiles; v.nsplit = nsplit; v.nwitems = (int)(witems.size() / 4);
   v.nstate_tiles = nstate_tiles;
@@ -244,7 +245,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   }
   AL(v.Y, B * d.E); AL(v.s, B * ng); AL(v.tin, B * ng); AL(v.pt, B * ng); AL(v.ptprev, B * ng);
   AL(v.p, B * ng); AL(v.lamp, B * ng); AL(v.K, B * d.NK); AL(v.Ccur, B * T * nx * nu);
-  AL(v.Cprev, B * T * nx * nu); AL(v.D, B * T * nx * nu); AL(v.Z, B * T * nu * nx);
+  AL(v.Cprev, B * T * nx * nu); AL(v.D, B * T * nx * nu); AL(v.Z, B * T * nu * nx); AL(v.Zg, B * T * nu * nx);
   AL(v.du, B * T * nu); AL(v.zl, B * ng); AL(v.yl, B * ng); AL(v.zb, B * (T + 1) * nx);
   AL(v.yb, B * (T + 1) * nx); AL(v.rp, B * ng); AL(v.wq, B * ng); AL(v.rx, B * (T + 1) * nx);
   AL(v.ru, B * T * nu); AL(v.kff, B * T * nu); AL(v.dxt, B * (T + 1) * nx); AL(v.dut, B * T * nu);
@@ -405,7 +406,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
   auto timed_qp = [&](int eng, int l) -> cudaError_t {
     cudaEvent_t a = nullptr, b = nullptr;
     if (h->prof) { a = prof_event(h); b = prof_event(h); cudaEventRecord(a, st); }
-    cudaError_t e = (d.ng >= kQpSparseRows) ? launch_qp_lite(h, eng, l, st) : launch_qp(h, eng, l, st);
+    cudaError_t e = (d.ng >= kQpSparseRows) ? launch_qp_sparse(h, eng, l, st) : launch_qp(h, eng, l, st);
     if (h->prof) { cudaEventRecord(b, st); h->recs.push_back({NRTO_K_QP, a, b}); }
     return e;
   };
@@ -416,8 +417,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     // overlap needs enough instances to keep the SMs busy with the pass while the
     // QP runs; for small batches the QP is on the critical path and the wide
     // staged variant (Acl in shared memory, 1024 threads) is used in order.
-    int nsm = 148;
-    { int dev = 0; if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev); }
+    const int nsm = v.nsm;
 #ifndef QP_OVERLAP_CTAS_PER_SM
 #define QP_OVERLAP_CTAS_PER_SM 2
 #endif
@@ -493,7 +493,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
               e = launch_zlist(h, v.Y, v.clist, v.cw, nullptr, v.ncorr, 0, v.active, v.Zc, gs, v.ylazy,
                                v.fused == 2 ? 1 : 0, v.dG, v.dH);
             if (e == cudaSuccess) e = launch_fa_gain(h, gs);
-            if (e == cudaSuccess) e = wide ? launch_qp_lite(h, NRTO_FULLADMM, l, gs) : launch_qp(h, NRTO_FULLADMM, l, gs);
+            if (e == cudaSuccess) e = wide ? launch_qp_sparse(h, NRTO_FULLADMM, l, gs) : launch_qp(h, NRTO_FULLADMM, l, gs);
           }
         }
         cudaGraph_t g = nullptr;
@@ -543,7 +543,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
         if (overlap) {
           CK(cudaEventRecord(h->ev_proj, st));
           CK(cudaStreamWaitEvent(st2, h->ev_proj, 0));
-          CK(timed2(st2, NRTO_K_QP, [&](cudaStream_t s2) { return launch_qp_lite(h, NRTO_FULLADMM, l, s2, QP_OVERLAP_CTAS_PER_SM * nsm); }));
+          CK(timed2(st2, NRTO_K_QP, [&](cudaStream_t s2) { return launch_qp_sparse(h, NRTO_FULLADMM, l, s2, QP_OVERLAP_CTAS_PER_SM * nsm); }));
           CK(cudaEventRecord(h->ev_qp, st2));
         }
         CK(timed(NRTO_K_ADJOINT, [](nrto_handle_s* hh, cudaStream_t s2) {
@@ -552,7 +552,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
                               w.fused == 2 ? 1 : 0, w.dG, w.dH); }));
         CK(timed(NRTO_K_GAIN, launch_fa_gain));
         if (!overlap) {
-          if (wide) CK(timed2(st, NRTO_K_QP, [&](cudaStream_t s2) { return launch_qp_lite(h, NRTO_FULLADMM, l, s2); }));
+          if (wide) CK(timed2(st, NRTO_K_QP, [&](cudaStream_t s2) { return launch_qp_sparse(h, NRTO_FULLADMM, l, s2); }));
           else CK(timed_qp(NRTO_FULLADMM, l));
         }
       }
@@ -600,7 +600,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
             if (e == cudaSuccess) e = launch_dr_reduce(h, h->gst);
           }
           if (e == cudaSuccess)
-            e = (d.ng >= kQpSparseRows) ? launch_qp_lite(h, NRTO_DR, l, h->gst) : launch_qp(h, NRTO_DR, l, h->gst);
+            e = (d.ng >= kQpSparseRows) ? launch_qp_sparse(h, NRTO_DR, l, h->gst) : launch_qp(h, NRTO_DR, l, h->gst);
         }
         cudaGraph_t g = nullptr;
         const cudaError_t ee = cudaStreamEndCapture(h->gst, &g);

@@ -67,6 +67,7 @@ struct Dev {
   double* Cprev;  // [B][T][nx][nu]  for the previous k_v
   double* D;      // [B][T][nx][nu]  2 Ccur - Cprev (FullADMM forward map)
   double* Z;      // [B][T][nu][nx]  adjoint accumulator sum_j b (s y)^T
+  double* Zg;     // [B][T][nu][nx]  nrto_gain_update's own accumulator (keeps the DR warm Z)
   // QP state
   double *du, *zl, *yl, *zb, *yb;     // [B][T][nu], [B][ng] x2, [B][T+1][nx] x2
   double *rp, *wq, *rx, *ru, *kff, *dxt, *dut;  // scratch
@@ -99,6 +100,7 @@ struct Dev {
   double* gval;            // [B][ng][8] its nonzero values
   double* Zctrl;           // [B][T][nu][nx] exact adjoint of the control cones (fused == 2)
   int ntiles, nsplit, nwitems;
+  int nsm;                 // multiprocessor count of the device (queried once at setup)
   int nstate_tiles;        // state tiles come first in `tiles`
   // TMA path: tile-interleaved copies of b_hat and b for the state tiles,
   // block-major [k][cone of tile][i] so a chunk of a tile is one bulk copy.
@@ -248,6 +250,6 @@ bool tma_supported(const Dims& d);
 cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_project(nrto_handle_s* h, cudaStream_t st);
-cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid = 0);
+cudaError_t launch_qp_sparse(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid = 0);
 
 }  // namespace nrto

@@ -915,7 +915,7 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
       // (measured on c2: 8 -> 32 splits, adjoint 29 -> 16 us per DR iteration)
       const int64_t warps = (int64_t)v.d.B * v.d.T;
       const int64_t navg = std::max<int64_t>(1, nfixed / 2);
-      while (nsp < 64 && warps * nsp * 2 <= 32 * 148 && navg / (nsp * 2) >= 8) nsp *= 2;
+      while (nsp < 64 && warps * nsp * 2 <= 32 * v.nsm && navg / (nsp * 2) >= 8) nsp *= 2;
       static const int dsp = [] { const char* e = getenv("NRTO_ZLIST_DSPLIT"); return e ? atoi(e) : 0; }();
       if (dsp > 0) nsp = dsp;
     }
@@ -928,7 +928,7 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
       // small batches (latency bound, e.g. one c3 instance): split the list until the
       // grid has ~32 warps per SM; the bench batch (B T >= 32 x 148 warps) stays unsplit
       const int64_t warps = (int64_t)v.d.B * v.d.T;
-      while (nsp < 32 && warps * nsp * 2 <= 32 * 148) nsp *= 2;
+      while (nsp < 32 && warps * nsp * 2 <= 32 * v.nsm) nsp *= 2;
     }
     if (nsp > 1 && !prezeroed) {   // zero the slices of the instances that will be accumulated
       const int64_t per = (int64_t)v.d.T * v.d.nu * v.d.nx;

@@ -907,11 +907,18 @@ cudaError_t launch_gain_update(nrto_handle_s* h, const double* nu, const double*
                                double* kv_next, cudaStream_t st) {
   Dev& v = h->dev;
   const Dims& d = v.d;
+  // accumulate into the handle's own Zg, not Z: Z carries the DR engine's warm
+  // adjoint of eta~ between solves, which a standalone gain update must keep
+  double* const zkeep = v.Z;
+  v.Z = v.Zg;
   cudaError_t e = launch_adjoint(h, nu, nullptr, nullptr, st);
-  if (e != cudaSuccess) return e;
-  k_fa_gain<<<d.B * d.T, 128, 3 * d.nu * d.nx * sizeof(double), st>>>(v, 1, kv_prev, kv_next);
-  h->launches++;
-  return cudaGetLastError();
+  if (e == cudaSuccess) {
+    k_fa_gain<<<d.B * d.T, 128, 3 * d.nu * d.nx * sizeof(double), st>>>(v, 1, kv_prev, kv_next);
+    h->launches++;
+    e = cudaGetLastError();
+  }
+  v.Z = zkeep;
+  return e;
 }
 
 cudaError_t launch_soc_project(const double* t, const double* y, const int64_t* off, int64_t n,

@@ -423,11 +423,7 @@ __global__ void __launch_bounds__(1024) k_qp_staged(Dev v, int engine, int l, in
 }
 
 // ---------------------------------------------------------------------------
-// Light variant sized to co-reside with the TMA cone pass on every SM (256
-// threads, <= 48 registers, ~18 KB shared memory), so that QP(l) runs
-// concurrently with pass(l+1) on a second stream.  Same arithmetic
-// as k_qp_staged; Acl_k streams through a 4-slot cp.async ring owned by the
-// sweep warp, a_k / e_k / kff / r_u / du~ live in global scratch.
+// cp.async helpers of the sparse-row QP below.
 __device__ __forceinline__ void cpa8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src) : "memory");
@@ -444,250 +440,9 @@ constexpr int kQPRing = QP_RING;   // power of two (common.cuh)
 #define QP_THREADS 256
 #endif
 
-__global__ void __launch_bounds__(256, 5) k_qp_lite(Dev v, int engine, int l) {
-  extern __shared__ double sm[];
-  __shared__ double red[32];
-  const Dims d = v.d;
-  const int nx = d.nx, nu = d.nu, T = d.T, ng = d.ng;
-  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-  if (!v.active[b]) return;
-  const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
-  const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
-  const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp, aq = v.prm.alpha_qp;
-  const double den = rho + sq + rq, beta = rq / den;
-  const int64_t bg = (int64_t)b * ng;
-  const double* __restrict__ grad = v.grad + bg * nx;
-  const double* __restrict__ g0 = v.g0 + bg;
-  double* p = v.p + bg; double* zl = v.zl + bg; double* yl = v.yl + bg;
-  double* rp = v.rp + bg; double* wq = v.wq + bg;
-  const double* pt = v.pt + bg; double* lam = v.lamp + bg;
-  double* zb = v.zb + (int64_t)b * (T + 1) * nx; double* yb = v.yb + (int64_t)b * (T + 1) * nx;
-  double* du = v.du + (int64_t)b * T * nu;
-  double* gA = v.dxt + (int64_t)b * (T + 1) * nx;    // a_k, then e_k
-  double* gK = v.kff + (int64_t)b * T * nu;           // kff_k
-  double* gR = v.ru + (int64_t)b * T * nu;            // r_u,k, then du~_k
-  const double* __restrict__ Ru = v.Ru + (int64_t)b * T * nu * nu;
-  const double* __restrict__ uh = v.uhat + (int64_t)b * T * nu;
-  const double* __restrict__ Bm = v.Bm + (int64_t)b * T * nx * nu;
-  const double* __restrict__ Kf = F.Kf + (int64_t)b * T * nu * nx;
-  const double* __restrict__ AclG = F.Acl + (int64_t)b * T * nx * nx;
-  const double* __restrict__ Hi = F.Hinv + (int64_t)b * T * nu * nu;
-  const double* __restrict__ HB = F.HB + (int64_t)b * T * nu * nx;
-  const double rtr = v.rtrust[b];
-  const double rinv = (engine == NRTO_FULLADMM) ? 1.0 : 1.0 / rho;
-  double* sS = sm;                                    // [(T+1) nx]
-  double* ring = sS + (T + 1) * nx;                   // [kQPRing][nx nx]
-  const int nn = nx * nx;
-
-  const int nits = v.prm.qp_iters;
-  for (int it = 0; it < nits; ++it) {
-    if (it == 0) {           // later iterations get rhs_p / w from the fused row update below
-      for (int j = tid; j < ng; j += nt) {
-        const double vj = pt[j] - lam[j] * rinv;
-        const double r = sq * p[j] + rho * vj + rq * zl[j] - yl[j];
-        rp[j] = r;
-        wq[j] = rq * zl[j] - yl[j] - beta * r;
-      }
-      __syncthreads();
-    }
-    for (int r = tid; r < T * nu; r += nt) {
-      const int k = r / nu, m = r % nu;
-      double acc = sq * du[r];
-      for (int q = 0; q < nu; ++q) acc -= 2.0 * Ru[(k * nu + m) * nu + q] * uh[k * nu + q];
-      for (int q = __ldg(v.cptr + k); q < __ldg(v.cptr + k + 1); ++q) {
-        const int j = __ldg(v.crow + q);
-        acc += grad[j * nx + m] * wq[j];
-      }
-      gR[r] = acc;
-    }
-    __syncthreads();
-    for (int r = tid; r < (T + 1) * nx; r += nt) {
-      const int k = r / nx, i = r % nx;
-      double acc = 0.0;
-      if (k > 0) {
-        acc = rq * zb[r] - yb[r];
-#pragma unroll 4
-        for (int q = __ldg(v.sptr + k); q < __ldg(v.sptr + k + 1); ++q) {
-          const int j = __ldg(v.srow + q);
-          acc += grad[j * nx + i] * wq[j];
-        }
-      }
-      if (k < T) {
-        const double* Kk = Kf + (int64_t)k * nu * nx;
-        for (int m = 0; m < nu; ++m) acc -= Kk[m * nx + i] * gR[k * nu + m];
-        gA[r] = acc;
-      } else {
-        sS[r] = acc;
-      }
-    }
-    __syncthreads();
-    if (tid < 32) {                                   // backward recurrence, Acl ring
-      for (int pf = 0; pf < kQPRing; ++pf) {
-        const int k = T - 1 - pf;
-        if (k >= 0) for (int e = tid; e < nn; e += 32) cpa8(ring + pf * nn + e, AclG + (int64_t)k * nn + e);
-        cpa_commit();
-      }
-      double s = (tid < nx) ? sS[T * nx + tid] : 0.0;
-      const int ic = tid < nx ? tid : 0;
-      for (int k = T - 1, slot = 0; k >= 0; --k, slot = (slot + 1) % kQPRing) {
-        cpa_wait<kQPRing - 1>();
-        __syncwarp();
-        const double* Ak = ring + slot * nn + ic;
-        double a0 = gA[k * nx + ic], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int r = 0;
-        for (; r + 4 <= nx; r += 4) {
-          a0 += Ak[(r + 0) * nx] * __shfl_sync(0xffffffffu, s, r + 0);
-          a1 += Ak[(r + 1) * nx] * __shfl_sync(0xffffffffu, s, r + 1);
-          a2 += Ak[(r + 2) * nx] * __shfl_sync(0xffffffffu, s, r + 2);
-          a3 += Ak[(r + 3) * nx] * __shfl_sync(0xffffffffu, s, r + 3);
-        }
-        for (; r < nx; ++r) a0 += Ak[r * nx] * __shfl_sync(0xffffffffu, s, r);
-        s = (a0 + a1) + (a2 + a3);
-        if (tid < nx) sS[k * nx + tid] = s;
-        __syncwarp();
-        const int kn = k - kQPRing;                   // refill this slot
-        if (kn >= 0) for (int e = tid; e < nn; e += 32) cpa8(ring + slot * nn + e, AclG + (int64_t)kn * nn + e);
-        cpa_commit();
-      }
-      cpa_wait<0>();
-    }
-    __syncthreads();
-    for (int r = tid; r < T * nu; r += nt) {
-      const int k = r / nu, m = r % nu;
-      const double* H = Hi + (int64_t)k * nu * nu;
-      const double* hb = HB + (int64_t)k * nu * nx;
-      double acc = 0.0;
-      for (int q = 0; q < nu; ++q) acc += H[m * nu + q] * gR[k * nu + q];
-      for (int i = 0; i < nx; ++i) acc += hb[m * nx + i] * sS[(k + 1) * nx + i];
-      gK[r] = acc;
-    }
-    __syncthreads();
-    for (int r = tid; r < T * nx; r += nt) {
-      const int k = r / nx, i = r % nx;
-      const double* Bk = Bm + (int64_t)k * nx * nu;
-      double acc = 0.0;
-      for (int m = 0; m < nu; ++m) acc += Bk[i * nu + m] * gK[k * nu + m];
-      gA[r] = acc;
-    }
-    __syncthreads();
-    if (tid < 32) {                                   // forward recurrence, Acl ring
-      for (int pf = 0; pf < kQPRing; ++pf) {
-        if (pf < T) for (int e = tid; e < nn; e += 32) cpa8(ring + pf * nn + e, AclG + (int64_t)pf * nn + e);
-        cpa_commit();
-      }
-      double x = 0.0;
-      const int ic = tid < nx ? tid : 0;
-      if (tid < nx) sS[tid] = 0.0;
-      for (int k = 0, slot = 0; k < T; ++k, slot = (slot + 1) % kQPRing) {
-        cpa_wait<kQPRing - 1>();
-        __syncwarp();
-        const double* Ak = ring + slot * nn + ic * nx;
-        double a0 = gA[k * nx + ic], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int r = 0;
-        for (; r + 4 <= nx; r += 4) {
-          a0 += Ak[r + 0] * __shfl_sync(0xffffffffu, x, r + 0);
-          a1 += Ak[r + 1] * __shfl_sync(0xffffffffu, x, r + 1);
-          a2 += Ak[r + 2] * __shfl_sync(0xffffffffu, x, r + 2);
-          a3 += Ak[r + 3] * __shfl_sync(0xffffffffu, x, r + 3);
-        }
-        for (; r < nx; ++r) a0 += Ak[r] * __shfl_sync(0xffffffffu, x, r);
-        x = (a0 + a1) + (a2 + a3);
-        if (tid < nx) sS[(k + 1) * nx + tid] = x;
-        __syncwarp();
-        const int kn = k + kQPRing;
-        if (kn < T) for (int e = tid; e < nn; e += 32) cpa8(ring + slot * nn + e, AclG + (int64_t)kn * nn + e);
-        cpa_commit();
-      }
-      cpa_wait<0>();
-    }
-    __syncthreads();
-    for (int r = tid; r < T * nu; r += nt) {
-      const int k = r / nu, m = r % nu;
-      const double* Kk = Kf + (int64_t)k * nu * nx;
-      double acc = gK[r];
-      for (int q = 0; q < nx; ++q) acc -= Kk[m * nx + q] * sS[k * nx + q];
-      gR[r] = acc;
-    }
-    __syncthreads();
-    for (int j = tid; j < ng; j += nt) {
-      const int k = v.knot[j];
-      double bd = 0.0;
-      if (v.kind[j] == 0) {
-        for (int q = 0; q < nx; ++q) bd += grad[j * nx + q] * sS[k * nx + q];
-      } else {
-        for (int q = 0; q < nu; ++q) bd += grad[j * nx + q] * gR[k * nu + q];
-      }
-      const double ptl = (rp[j] - rq * bd) / den;
-      const double ztl = bd + ptl;
-      const double pn = aq * ptl + (1.0 - aq) * p[j];
-      const double zl0 = zl[j], yl0 = yl[j];
-      const double zh = aq * ztl + (1.0 - aq) * zl0;
-      const double zn = fmin(zh + yl0 / rq, -g0[j]);
-      const double yn = yl0 + rq * (zh - zn);
-      p[j] = pn; zl[j] = zn; yl[j] = yn;
-      if (it + 1 < nits) {   // rhs_p and w of the next QP iteration
-        const double vj = pt[j] - lam[j] * rinv;
-        const double r = sq * pn + rho * vj + rq * zn - yn;
-        rp[j] = r;
-        wq[j] = rq * zn - yn - beta * r;
-      }
-    }
-    for (int r = tid; r < T * nu; r += nt) du[r] = aq * gR[r] + (1.0 - aq) * du[r];
-    __syncthreads();
-    double nb = 0.0;
-    for (int r = tid; r < (T + 1) * nx; r += nt) {
-      const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
-      sS[r] = zh;
-      const double w = zh + yb[r] / rq;
-      nb += w * w;
-    }
-    nb = sqrt(block_sum(nb, red));
-    const double scl = (nb > rtr) ? rtr / nb : 1.0;
-    for (int r = tid; r < (T + 1) * nx; r += nt) {
-      const double zh = sS[r];
-      const double zn = scl * (zh + yb[r] / rq);
-      yb[r] += rq * (zh - zn);
-      zb[r] = zn;
-    }
-    __syncthreads();
-  }
-  double ap = 0.0, ad = 0.0;
-  double* tin = v.tin + bg;
-  double* ptp = v.ptprev + bg;
-  for (int j = tid; j < ng; j += nt) {
-    const double dp = p[j] - pt[j];
-    if (engine == NRTO_FULLADMM) {
-      lam[j] += dp;
-      tin[j] = p[j] + lam[j];
-    } else {
-      lam[j] += rho * dp;
-    }
-    ap += dp * dp;
-    const double dd = pt[j] - ptp[j];
-    ad += dd * dd;
-    ptp[j] = pt[j];
-  }
-  ap = block_sum(ap, red);
-  ad = block_sum(ad, red);
-  if (tid == 0) {
-    const double rpv = sqrt(ap), rdv = rho * sqrt(ad);
-    v.r_p[b] = rpv;
-    v.r_d[b] = rdv;
-    record_hist(v, b, l, rpv, rdv, engine);
-    v.iters[b] = l;
-    if (!isfinite(rpv) || !isfinite(rdv)) {
-      v.status[b] = NRTO_DIVERGED;
-      v.active[b] = 0;
-    } else if (!v.prm.fixed_iters && (l % v.prm.check_every) == 0 && rpv <= v.prm.eps_p &&
-               rdv <= v.prm.eps_d) {
-      v.status[b] = NRTO_CONVERGED;
-      v.active[b] = 0;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
-// Sparse-row variant of k_qp_lite.  The constraint gradients are kept in a
+// Sparse-row QP, sized to co-reside with the TMA cone pass (256 threads, <= 48
+// registers, ~24 KB shared memory).  The constraint gradients are kept in a
 // compressed row form built at setup (<= 8 nonzeros per row, else dense), and
 // the row phase of QP iteration m gathers (B du~)_j, updates (p, z, y)_j and
 // immediately scatters the NEXT iteration's w_j grad_j into the knot
@@ -1200,7 +955,7 @@ cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid) {
+cudaError_t launch_qp_sparse(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid) {
   const Dims& d = h->dev.d;
   const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx + kQPRing) * sizeof(double);
   if (smem > 48 * 1024) return launch_qp(h, engine, l, st);
@@ -1212,9 +967,7 @@ cudaError_t launch_qp_lite(nrto_handle_s* h, int engine, int l, cudaStream_t st,
     h->launches++;
     return cudaGetLastError();
   }
-  k_qp_lite<<<d.B, 256, smem, st>>>(h->dev, engine, l);
-  h->launches++;
-  return cudaGetLastError();
+  return launch_qp(h, engine, l, st);
 }
 
 static size_t qp_smem(const Dims& d, int stageA) {
@@ -1268,7 +1021,8 @@ cudaError_t launch_fa_reset(nrto_handle_s* h, cudaStream_t st) {
   const int64_t B = d.B;
   // TMA path: every y^1 block is written before it is read (no history at l = 1),
   // so the B E-double state array is not cleared (8.7 GB at the bench batch)
-  if (v.fused != 2) zero(h, v.Y, B * d.E, st);
+  // (max_iter = 0 runs no pass: the outputs nu / lam_nu are then built from Y = 0)
+  if (v.fused != 2 || v.prm.max_iter == 0) zero(h, v.Y, B * d.E, st);
   zero(h, v.s, B * d.ng, st); zero(h, v.tin, B * d.ng, st); zero(h, v.pt, B * d.ng, st);
   zero(h, v.ptprev, B * d.ng, st); zero(h, v.p, B * d.ng, st); zero(h, v.lamp, B * d.ng, st);
   zero(h, v.K, B * d.NK, st);
