@@ -222,6 +222,42 @@ nrto_err nrto_profile_read(nrto_handle h, int32_t kclass, double* total_ms, int6
  * lazy y).  0 when the TMA pass is not in use.  Synchronises the device. */
 nrto_err nrto_pass_bytes(nrto_handle h, int64_t* bytes);
 
+/* Incremental driving of the inner solve, for callers that interleave their
+ * own work between outer iterations -- e.g. the batch-wide allreduce(MAX) of
+ * the residual flags across ranks (one process per GPU, instances sharded;
+ * SURVEY §8e), the multi-GPU form of the termination test of Algorithm 1
+ * line 9 / P:505-507.  Same kernels and arithmetic as the in-order
+ * schedule of nrto_inner_solve (termination mode); every call is asynchronous
+ * on `stream` (no host synchronisation):
+ *   nrto_solve_begin    reset for `engine` (FullADMM cold start R10; DR keeps
+ *                       its warm state); no residual trace / case stats
+ *   nrto_solve_iterate  run up to n_iters more outer iterations (capped at
+ *                       max_iter / max_admm_iter); *done (host, may be NULL)
+ *                       receives the outer iterations run so far.  Converged /
+ *                       diverged instances stay frozen (R12).
+ *   nrto_solve_flags    flags[4] (DEVICE doubles) = [max_b r_p/eps_p,
+ *                       max_b r_d/eps_d, #active instances, any diverged]
+ *                       (NaN propagates through the maxima)
+ *   nrto_solve_end      finish (nu, lam_nu, margins, objective) and write `out`
+ *                       exactly as nrto_inner_solve does.
+ * NRTO_ESTATE if called out of order. */
+nrto_err nrto_solve_begin(nrto_handle h, int32_t engine, void* stream);
+nrto_err nrto_solve_iterate(nrto_handle h, int32_t n_iters, int32_t* done, void* stream);
+nrto_err nrto_solve_flags(nrto_handle h, double* flags, void* stream);
+nrto_err nrto_solve_end(nrto_handle h, const nrto_out* out, void* stream);
+
+/* Projection-case statistics of the FullADMM engine (SM Eq.(18), P:992-1002;
+ * the three cases of Fig. 3).  enable != 0: every later FullADMM
+ * solve counts, per outer iteration l = 1..max_iter, the cones (over the whole
+ * batch) whose Block-1 projection (13) fell in case 1 (||y|| <= t: kept),
+ * case 2 (||y|| <= -t: origin) or case 3 (boundary).  Counting costs a few
+ * warp-aggregated atomics per projection kernel.  nrto_case_stats_read copies
+ * the counts of the LAST FullADMM solve into counts[L][3] (host int64, row l-1
+ * = iteration l; rows the solve did not reach are 0) and synchronises the
+ * device.  NRTO_EINVAL for counts == NULL or L < 0. */
+nrto_err nrto_case_stats_enable(nrto_handle h, int32_t enable);
+nrto_err nrto_case_stats_read(nrto_handle h, int64_t* counts, int32_t L);
+
 nrto_err nrto_destroy(nrto_handle h);
 
 /* Thread-local message for the last non-OK return (never NULL). */

@@ -152,7 +152,9 @@ class DenseQP:
             out[pb.ng:] = zb * (pb.r_trust / nb)
         return out
 
-    def solve(self, v, iters):
+    def solve(self, v, iters, trace=None):
+        """`trace` (a list) receives per iteration the step-1 solution x~, z~ = C x~
+        and the new (x, z, y) -- read only by the iterate pins in the tests."""
         pb = self.pb
         NU = pb.NU
         q = np.concatenate([2.0 * pb.Ru @ pb.u_hat, -self.rho * v])
@@ -166,6 +168,9 @@ class DenseQP:
             znew = self.proj(zh + self.y / rq)
             self.y = self.y + rq * (zh - znew)
             self.z = znew
+            if trace is not None:
+                trace.append(dict(xt=xt.copy(), zt=zt.copy(), x=self.x.copy(),
+                                  z=self.z.copy(), y=self.y.copy()))
         return self.x[:NU].copy(), self.x[NU:].copy()
 
 

@@ -236,7 +236,10 @@ class RiccatiQP:
             dx[k + 1] = sp.A[k] @ dx[k] + sp.B[k] @ du[k]
         return du, dx
 
-    def solve(self, v, iters):
+    def solve(self, v, iters, trace=None):
+        """`trace` (a list) receives per iteration x~ = (du~, p~'), z~ = (B du~ + p~',
+        dx~) and the new (x, z, y), flattened in DenseQP's order (x = (du, p),
+        z = (z_lin, z_ball)) -- read only by the iterate pins in the tests."""
         sp = self.sp
         T = sp.T
         st = sp.kind == 0
@@ -264,6 +267,12 @@ class RiccatiQP:
             self.yl = self.yl + rq * (zhl - znl)
             self.yb = self.yb + rq * (zhb - znb)
             self.zl, self.zb = znl, znb
+            if trace is not None:
+                trace.append(dict(xt=np.concatenate([dut.reshape(-1), pt]),
+                                  zt=np.concatenate([ztl, dxt.reshape(-1)]),
+                                  x=np.concatenate([self.du.reshape(-1), self.p]),
+                                  z=np.concatenate([self.zl, self.zb.reshape(-1)]),
+                                  y=np.concatenate([self.yl, self.yb.reshape(-1)])))
         return self.du.reshape(-1).copy(), self.p.copy()
 
 

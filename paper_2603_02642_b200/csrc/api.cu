@@ -347,6 +347,64 @@ static int poll_active(nrto_handle_s* h, int32_t* dcount, int dr, cudaStream_t s
   return c;
 }
 
+
+// finish kernels (nu, lam_nu, margins, objective) and the copies of every output
+static nrto_err write_outputs(nrto_handle_s* h, int engine, const nrto_out* o, cudaStream_t st,
+                              double* nu_d, double* lam_d, double* obj_d, double* mc_d, double* ml_d) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  const bool host = o->memory == NRTO_MEM_HOST;
+  const int64_t B = d.B;
+  const size_t D8 = sizeof(double);
+  nrto_out od = *o;
+  od.nu = nu_d; od.lam_nu = lam_d; od.objective = obj_d; od.margin_cone = mc_d; od.margin_lin = ml_d;
+  CK(launch_finish(h, engine, &od, st));
+  CK(copy_out(o->kv, v.K, B * d.NK * D8, host, st));
+  CK(copy_out(o->du, v.du, B * d.T * d.nu * D8, host, st));
+  CK(copy_out(o->p, v.p, B * d.ng * D8, host, st));
+  CK(copy_out(o->p_tilde, v.pt, B * d.ng * D8, host, st));
+  CK(copy_out(o->lam_p, v.lamp, B * d.ng * D8, host, st));
+  CK(copy_out(o->iters, v.iters, B * 4, host, st));
+  CK(copy_out(o->status, v.status, B * 4, host, st));
+  CK(copy_out(o->r_p, v.r_p, B * D8, host, st));
+  CK(copy_out(o->r_d, v.r_d, B * D8, host, st));
+  if (v.hist) CK(copy_out(o->hist, v.hist, (size_t)B * v.hist_L * 3 * D8, host, st));
+  v.hist = nullptr;
+  if (host) {
+    CK(copy_out(o->nu, nu_d, B * d.E * D8, true, st));
+    CK(copy_out(o->lam_nu, lam_d, B * d.E * D8, true, st));
+    CK(copy_out(o->objective, obj_d, B * D8, true, st));
+    CK(copy_out(o->margin_cone, mc_d, B * d.ng * D8, true, st));
+    CK(copy_out(o->margin_lin, ml_d, B * d.ng * D8, true, st));
+  }
+  if (host) CK(cudaStreamSynchronize(st));
+  return NRTO_OK;
+}
+
+// handle-owned staging of the kernel-written optional outputs in host mode
+static nrto_err out_staging(nrto_handle_s* h, const nrto_out* o, double** nu_d, double** lam_d,
+                            double** obj_d, double** mc_d, double** ml_d) {
+  const Dims& d = h->dev.d;
+  const int64_t B = d.B;
+  const size_t D8 = sizeof(double);
+  *nu_d = o->nu; *lam_d = o->lam_nu; *obj_d = o->objective; *mc_d = o->margin_cone; *ml_d = o->margin_lin;
+  if (!h->dcount) {
+    CK(cudaMalloc((void**)&h->dcount, 4));
+    CK(cudaMalloc((void**)&h->stage_ng2, (size_t)std::max<int64_t>(2 * B * d.ng, 1) * D8));
+    CK(cudaMalloc((void**)&h->stage_b, (size_t)B * D8));
+  }
+  if (o->memory == NRTO_MEM_HOST) {
+    if ((o->nu || o->lam_nu) && !h->stage_e2)
+      CK(cudaMalloc((void**)&h->stage_e2, (size_t)std::max<int64_t>(2 * B * d.E, 1) * D8));
+    if (o->nu) *nu_d = h->stage_e2;
+    if (o->lam_nu) *lam_d = h->stage_e2 + B * d.E;
+    if (o->objective) *obj_d = h->stage_b;
+    if (o->margin_cone) *mc_d = h->stage_ng2;
+    if (o->margin_lin) *ml_d = h->stage_ng2 + B * d.ng;
+  }
+  return NRTO_OK;
+}
+
 constexpr int kQpSparseRows = 512;   // rows from which the sparse-row QP is used for any batch
 
 extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_out* o,
@@ -358,25 +416,11 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
   Dev& v = h->dev;
   const Dims& d = v.d;
   const nrto_params& prm = v.prm;
-  const bool host = o->memory == NRTO_MEM_HOST;
   const int64_t B = d.B;
-  const size_t D8 = sizeof(double);
-  // handle-owned staging for kernel-written optional outputs in host mode
-  double *nu_d = o->nu, *lam_d = o->lam_nu, *obj_d = o->objective, *mc_d = o->margin_cone,
-         *ml_d = o->margin_lin;
-  if (!h->dcount) {
-    CK(cudaMalloc((void**)&h->dcount, 4));
-    CK(cudaMalloc((void**)&h->stage_ng2, (size_t)std::max<int64_t>(2 * B * d.ng, 1) * D8));
-    CK(cudaMalloc((void**)&h->stage_b, (size_t)B * D8));
-  }
-  if (host) {
-    if ((o->nu || o->lam_nu) && !h->stage_e2)
-      CK(cudaMalloc((void**)&h->stage_e2, (size_t)std::max<int64_t>(2 * B * d.E, 1) * D8));
-    if (o->nu) nu_d = h->stage_e2;
-    if (o->lam_nu) lam_d = h->stage_e2 + B * d.E;
-    if (o->objective) obj_d = h->stage_b;
-    if (o->margin_cone) mc_d = h->stage_ng2;
-    if (o->margin_lin) ml_d = h->stage_ng2 + B * d.ng;
+  double *nu_d, *lam_d, *obj_d, *mc_d, *ml_d;
+  {
+    const nrto_err se = out_staging(h, o, &nu_d, &lam_d, &obj_d, &mc_d, &ml_d);
+    if (se != NRTO_OK) return se;
   }
   int32_t* dcount = h->dcount;
   // optional residual trace: handle-owned device buffer, zeroed per solve
@@ -393,6 +437,21 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     }
     CK(cudaMemsetAsync(h->hist_buf, 0, need * sizeof(double), st));
     v.hist = h->hist_buf;
+  }
+
+  // optional projection-case statistics (FullADMM): handle-owned counters, zeroed per solve
+  v.case_cnt = nullptr;
+  if (h->case_stats && engine == NRTO_FULLADMM && prm.max_iter > 0) {
+    const int64_t need = 3LL * prm.max_iter;
+    if (h->case_cap < need) {
+      if (h->case_buf) cudaFree(h->case_buf);
+      h->case_buf = nullptr; h->case_cap = 0;
+      CK(cudaMalloc((void**)&h->case_buf, need * sizeof(unsigned long long)));
+      h->case_cap = need;
+    }
+    CK(cudaMemsetAsync(h->case_buf, 0, need * sizeof(unsigned long long), st));
+    v.case_cnt = h->case_buf;
+    h->case_L = prm.max_iter;
   }
 
   cudaError_t ce = cudaSuccess;
@@ -640,29 +699,8 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
       }
     }
   }
-  nrto_out od = *o;
-  od.nu = nu_d; od.lam_nu = lam_d; od.objective = obj_d; od.margin_cone = mc_d; od.margin_lin = ml_d;
-  CK(launch_finish(h, engine, &od, st));
-  CK(copy_out(o->kv, v.K, B * d.NK * D8, host, st));
-  CK(copy_out(o->du, v.du, B * d.T * d.nu * D8, host, st));
-  CK(copy_out(o->p, v.p, B * d.ng * D8, host, st));
-  CK(copy_out(o->p_tilde, v.pt, B * d.ng * D8, host, st));
-  CK(copy_out(o->lam_p, v.lamp, B * d.ng * D8, host, st));
-  CK(copy_out(o->iters, v.iters, B * 4, host, st));
-  CK(copy_out(o->status, v.status, B * 4, host, st));
-  CK(copy_out(o->r_p, v.r_p, B * D8, host, st));
-  CK(copy_out(o->r_d, v.r_d, B * D8, host, st));
-  if (v.hist) CK(copy_out(o->hist, v.hist, (size_t)B * v.hist_L * 3 * D8, host, st));
-  v.hist = nullptr;
-  if (host) {
-    CK(copy_out(o->nu, nu_d, B * d.E * D8, true, st));
-    CK(copy_out(o->lam_nu, lam_d, B * d.E * D8, true, st));
-    CK(copy_out(o->objective, obj_d, B * D8, true, st));
-    CK(copy_out(o->margin_cone, mc_d, B * d.ng * D8, true, st));
-    CK(copy_out(o->margin_lin, ml_d, B * d.ng * D8, true, st));
-  }
-  if (host) CK(cudaStreamSynchronize(st));
-  return NRTO_OK;
+  v.case_cnt = nullptr;
+  return write_outputs(h, engine, o, st, nu_d, lam_d, obj_d, mc_d, ml_d);
 }
 
 extern "C" nrto_err nrto_gain_update(nrto_handle h, const double* nu, const double* kv_prev,
@@ -705,6 +743,7 @@ extern "C" nrto_err nrto_destroy(nrto_handle h) {
   if (h->stage_ng2) cudaFree(h->stage_ng2);
   if (h->stage_b) cudaFree(h->stage_b);
   if (h->stage_e2) cudaFree(h->stage_e2);
+  if (h->case_buf) cudaFree(h->case_buf);
   free_all(h);
   delete h;
   return NRTO_OK;
@@ -750,4 +789,128 @@ extern "C" nrto_err nrto_pass_bytes(nrto_handle h, int64_t* bytes) {
   if (e != cudaSuccess) return cuda_fail(e, "nrto_pass_bytes");
   *bytes = (int64_t)v;
   return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_case_stats_enable(nrto_handle h, int32_t enable) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  h->case_stats = enable != 0;
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_case_stats_read(nrto_handle h, int64_t* counts, int32_t L) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (!counts || L < 0) return fail(NRTO_EINVAL, "counts is NULL or L < 0");
+  std::memset(counts, 0, sizeof(int64_t) * 3 * (size_t)L);
+  const int n = std::min<int>(L, h->case_L);
+  if (n <= 0 || !h->case_buf) return NRTO_OK;
+  std::vector<unsigned long long> tmp((size_t)3 * n);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(tmp.data(), h->case_buf, tmp.size() * sizeof(unsigned long long),
+                                       cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "nrto_case_stats_read");
+  for (size_t i = 0; i < tmp.size(); ++i) counts[i] = (int64_t)tmp[i];
+  return NRTO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Incremental driving (nrto_solve_begin / _iterate / _flags / _end): the same
+// kernels as the in-order schedule of nrto_inner_solve, in chunks of outer
+// iterations, so that a multi-rank caller can interleave a batch-wide collective
+// of the residual flags between chunks.
+static cudaError_t fa_iteration_inorder(nrto_handle_s* h, int l, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  v.iter = l;
+  v.ylazy = 0;
+  cudaError_t e;
+  if (v.fused == 0) {
+    e = launch_fa_pass(h, st);
+    if (e == cudaSuccess) e = launch_adjoint(h, v.Y, v.s, v.active, st);
+    if (e == cudaSuccess) e = launch_fa_gain(h, st);
+    if (e == cudaSuccess) e = launch_qp(h, NRTO_FULLADMM, l, st);
+    return e;
+  }
+  e = v.fused == 2 ? launch_fa_tma(h, st) : launch_fa_fused(h, st);
+  if (e == cudaSuccess && v.fused == 2) e = launch_fa_ctrl(h, st);
+  if (e == cudaSuccess) e = launch_project(h, st);
+  if (e == cudaSuccess)
+    e = launch_zlist(h, v.Y, v.clist, v.cw, nullptr, v.ncorr, 0, v.active, v.Zc, st, 0,
+                     v.fused == 2 ? 1 : 0, v.dG, v.dH);
+  if (e == cudaSuccess) e = launch_fa_gain(h, st);
+  const bool wide = d.B >= v.nsm || d.ng >= kQpSparseRows;
+  if (e == cudaSuccess) e = wide ? launch_qp_sparse(h, NRTO_FULLADMM, l, st) : launch_qp(h, NRTO_FULLADMM, l, st);
+  return e;
+}
+
+static cudaError_t dr_iteration(nrto_handle_s* h, int l, cudaStream_t st) {
+  Dev& v = h->dev;
+  cudaError_t e = launch_dr_arm(h, st);
+  for (int m = 1; m <= v.prm.max_dr_iter && e == cudaSuccess; ++m) {
+    e = launch_dr_gain(h, st);
+    if (e == cudaSuccess) e = launch_dr_pass(h, st);
+    if (e == cudaSuccess) e = launch_dr_adjoint(h, st);
+    if (e == cudaSuccess) e = launch_dr_reduce(h, st);
+  }
+  if (e == cudaSuccess)
+    e = (v.d.ng >= kQpSparseRows) ? launch_qp_sparse(h, NRTO_DR, l, st) : launch_qp(h, NRTO_DR, l, st);
+  return e;
+}
+
+extern "C" nrto_err nrto_solve_begin(nrto_handle h, int32_t engine, void* stream) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (engine != NRTO_FULLADMM && engine != NRTO_DR) return fail(NRTO_EINVAL, "unknown engine");
+  cudaStream_t st = (cudaStream_t)stream;
+  Dev& v = h->dev;
+  v.hist = nullptr;
+  v.hist_L = engine == NRTO_FULLADMM ? v.prm.max_iter : v.prm.max_admm_iter;
+  v.case_cnt = nullptr;
+  if (engine == NRTO_FULLADMM) {
+    CK(launch_fa_reset(h, st));
+  } else {
+    if (!h->dr_ready) {
+      CK(launch_engine_factors(h, NRTO_DR, st));
+      const int se = read_setup_error(st);
+      if (se) return fail(NRTO_ENOTSPD, se == 1 ? "W_K + sigma_dr/2 is not SPD" : "Riccati H_uu is not SPD");
+      h->dr_ready = 1;
+    }
+    CK(launch_dr_reset(h, h->dr_fresh, st));
+    h->dr_fresh = 0;
+  }
+  h->inc_engine = engine;
+  h->inc_l = 0;
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_solve_iterate(nrto_handle h, int32_t n_iters, int32_t* done, void* stream) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (h->inc_engine < 0) return fail(NRTO_ESTATE, "nrto_solve_iterate before nrto_solve_begin");
+  if (n_iters < 0) return fail(NRTO_EINVAL, "n_iters < 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int Lmax = h->inc_engine == NRTO_FULLADMM ? h->dev.prm.max_iter : h->dev.prm.max_admm_iter;
+  const int l1 = std::min(Lmax, h->inc_l + n_iters);
+  for (int l = h->inc_l + 1; l <= l1; ++l) {
+    CK(h->inc_engine == NRTO_FULLADMM ? fa_iteration_inorder(h, l, st) : dr_iteration(h, l, st));
+    h->inc_l = l;
+  }
+  if (done) *done = h->inc_l;
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_solve_flags(nrto_handle h, double* flags, void* stream) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (!flags) return fail(NRTO_EINVAL, "flags is NULL");
+  CK(launch_solve_flags(h, flags, (cudaStream_t)stream));
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_solve_end(nrto_handle h, const nrto_out* o, void* stream) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (!o) return fail(NRTO_EINVAL, "out is NULL");
+  if (h->inc_engine < 0) return fail(NRTO_ESTATE, "nrto_solve_end before nrto_solve_begin");
+  const int engine = h->inc_engine;
+  h->inc_engine = -1;
+  double *nu_d, *lam_d, *obj_d, *mc_d, *ml_d;
+  const nrto_err se = out_staging(h, o, &nu_d, &lam_d, &obj_d, &mc_d, &ml_d);
+  if (se != NRTO_OK) return se;
+  return write_outputs(h, engine, o, (cudaStream_t)stream, nu_d, lam_d, obj_d, mc_d, ml_d);
 }

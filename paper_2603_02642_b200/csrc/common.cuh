@@ -84,6 +84,7 @@ struct Dev {
   int iter;                // outer iteration l of the launch (set by the host loop)
   double* hist;            // [B][hist_L][3] residual trace (nullptr: not requested)
   int hist_L;
+  unsigned long long* case_cnt;   // [hist_L][3] projection cases 1/2/3 per iteration (nullptr: off)
   int ylazy;               // 1: lazy y storage in this iteration
   unsigned long long* pass_bytes;  // algorithmic bytes moved by k_fa_tma (device counter)
   double* nrm2;            // [B][ng] ||y^l||^2 written by the fused pass
@@ -158,6 +159,12 @@ struct nrto_handle_s {
   double* stage_b = nullptr;     // [B]         objective
   double* stage_e2 = nullptr;    // [2][B][E]   nu, lam_nu (allocated on first host request)
   int32_t* dcount = nullptr;
+  int case_stats = 0;                       // nrto_case_stats_enable
+  unsigned long long* case_buf = nullptr;   // [case_cap][3]
+  int64_t case_cap = 0;
+  int case_L = 0;                           // rows written by the last FullADMM solve
+  int inc_engine = -1;                      // incremental solve in progress (nrto_solve_begin)
+  int inc_l = 0;                            // outer iterations run by it
 };
 
 namespace nrto {
@@ -210,6 +217,24 @@ __device__ __forceinline__ void record_hist(const Dev& v, int b, int l, double r
   }
 }
 
+// Projection-case statistics (nrto_case_stats_enable): s = 1 <=> case 1 (kept),
+// s = 0 <=> case 2 (origin), else case 3 (boundary) -- soc_case never returns
+// 0 or 1 in case 3 since |t| < a there.  Warp-aggregated counters per iteration.
+__device__ __forceinline__ void count_case(const Dev& v, double s) {
+  if (!v.case_cnt || v.iter < 1 || v.iter > v.hist_L) return;
+  const unsigned m = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  const int c1 = __popc(__ballot_sync(m, s == 1.0));
+  const int c2 = __popc(__ballot_sync(m, s == 0.0));
+  const int c3 = __popc(m) - c1 - c2;
+  if (lane == leader) {
+    unsigned long long* c = v.case_cnt + (int64_t)(v.iter - 1) * 3;
+    if (c1) atomicAdd(c + 0, (unsigned long long)c1);
+    if (c2) atomicAdd(c + 1, (unsigned long long)c2);
+    if (c3) atomicAdd(c + 2, (unsigned long long)c3);
+  }
+}
+
 __device__ __forceinline__ double shat_of(const Dev& v, double sprev) {
   if (v.iter == 1) return 0.5;
   return (sprev == 1.0) ? 1.0 : 0.0;
@@ -234,6 +259,7 @@ cudaError_t launch_gain_update(nrto_handle_s* h, const double* nu, const double*
 cudaError_t launch_soc_project(const double* t, const double* y, const int64_t* off,
                                int64_t n, double* to, double* yo, cudaStream_t st);
 cudaError_t launch_count_active(nrto_handle_s* h, int32_t* d_count, int dr, cudaStream_t st);
+cudaError_t launch_solve_flags(nrto_handle_s* h, double* flags, cudaStream_t st);
 int read_setup_error(cudaStream_t st);
 cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st);
 cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st);

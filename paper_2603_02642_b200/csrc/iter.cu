@@ -63,6 +63,7 @@ __global__ void k_fa_pass(Dev v) {
     const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
     v.s[ij] = s;
     v.pt[ij] = tp;
+    count_case(v, s);
   }
 }
 
@@ -758,6 +759,43 @@ __global__ void k_count_active(Dev v, int32_t* out, int dr) {
   if (threadIdx.x == 0) *out = (int32_t)c;
 }
 
+// Batch residual flags (nrto_solve_flags): [max_b r_p/eps_p, max_b r_d/eps_d,
+// #active instances, any instance diverged] -- the operand of the batch-wide
+// allreduce(MAX) of the multi-rank termination test.
+__global__ void k_solve_flags(Dev v, double* out) {
+  __shared__ double sh[4][32];
+  double rp = 0.0, rd = 0.0, act = 0.0, dv = 0.0;
+  const double ep = v.prm.eps_p > 0 ? v.prm.eps_p : 1.0, ed = v.prm.eps_d > 0 ? v.prm.eps_d : 1.0;
+  for (int b = threadIdx.x; b < v.d.B; b += blockDim.x) {
+    const double a = v.r_p[b] / ep, c = v.r_d[b] / ed;
+    rp = (a > rp || a != a) ? a : rp;      // NaN propagates (diverged)
+    rd = (c > rd || c != c) ? c : rd;
+    act += v.active[b] ? 1.0 : 0.0;
+    dv = (v.status[b] == NRTO_DIVERGED) ? 1.0 : dv;
+  }
+  double r[4] = {rp, rd, act, dv};
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    double x = r[q];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, x, o);
+      x = (q == 2) ? x + y : ((y > x || y != y) ? y : x);
+    }
+    if (lane == 0) sh[q][w] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const int q = threadIdx.x;
+    double x = (q == 2) ? 0.0 : sh[q][0];
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      const double y = sh[q][i];
+      x = (q == 2) ? x + y : ((y > x || y != y) ? y : x);
+    }
+    out[q] = x;
+  }
+}
+
 // Standalone batched SOC projection (nrto_soc_project).
 __global__ void k_soc_project(const double* t, const double* y, const int64_t* off, int64_t n,
                               double* to, double* yo) {
@@ -924,6 +962,12 @@ cudaError_t launch_gain_update(nrto_handle_s* h, const double* nu, const double*
 cudaError_t launch_soc_project(const double* t, const double* y, const int64_t* off, int64_t n,
                                double* to, double* yo, cudaStream_t st) {
   if (n > 0) k_soc_project<<<warp_grid(n, 8), 256, 0, st>>>(t, y, off, n, to, yo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solve_flags(nrto_handle_s* h, double* flags, cudaStream_t st) {
+  k_solve_flags<<<1, 256, 0, st>>>(h->dev, flags);
+  h->launches++;
   return cudaGetLastError();
 }
 

@@ -6,6 +6,12 @@
 
 namespace nrto {
 
+// min(a, b) of the row projection z_l = min(., -g_l) that PROPAGATES NaN (IEEE fmin
+// returns the non-NaN operand): a non-finite input must end as NRTO_DIVERGED
+__device__ __forceinline__ double nan_min(double a, double b) {
+  return (a != a || b != b) ? a + b : fmin(a, b);
+}
+
 // One CTA per instance.  x = (du, p), z = (z_lin, z_ball), y dual.
 //   rhs_p = sigma p + rho v + rho_q z_lin - y_lin
 //   w     = rho_q z_lin - y_lin - beta rhs_p,           beta = rho_q/(rho+sigma+rho_q)
@@ -132,7 +138,7 @@ __global__ void __launch_bounds__(128) k_qp(Dev v, int engine, int l) {
       const double ztl = bd + ptl;
       p[j] = aq * ptl + (1.0 - aq) * p[j];
       const double zh = aq * ztl + (1.0 - aq) * zl[j];
-      const double zn = fmin(zh + yl[j] / rq, -g0[j]);
+      const double zn = nan_min(zh + yl[j] / rq, -g0[j]);
       yl[j] += rq * (zh - zn);
       zl[j] = zn;
     }
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(1024) k_qp_staged(Dev v, int engine, int l, in
       const double ztl = bd + ptl;
       p[j] = aq * ptl + (1.0 - aq) * p[j];
       const double zh = aq * ztl + (1.0 - aq) * zl[j];
-      const double zn = fmin(zh + yl[j] / rq, -g0[j]);
+      const double zn = nan_min(zh + yl[j] / rq, -g0[j]);
       yl[j] += rq * (zh - zn);
       zl[j] = zn;
     }
@@ -515,7 +521,7 @@ __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int ti
         const double ptl = (r0 - rq * bd) / den;
         pn = aq * ptl + (1.0 - aq) * pj[u];
         const double zh = aq * (bd + ptl) + (1.0 - aq) * zlj[u];
-        zn = fmin(zh + ylj[u] / rq, -g0j[u]);
+        zn = nan_min(zh + ylj[u] / rq, -g0j[u]);
         yn = ylj[u] + rq * (zh - zn);
         p[j] = pn; zl[j] = zn; yl[j] = yn;
       }

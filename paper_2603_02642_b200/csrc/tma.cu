@@ -413,6 +413,7 @@ __global__ void k_project(Dev v) {
   const double tp = soc_case(v.tin[id], sqrt(v.nrm2[id]), &s);
   v.s[id] = s;
   v.pt[id] = tp;
+  count_case(v, s);
   // TMA path: state cones leaving / entering the interior set {s = 1} update
   // the Gram sums G, H of the predicted adjoint.
   // At l = 1 the interior set restarts from empty (the gain kernel replaces G, H by

@@ -84,9 +84,17 @@ def lib():
         L.nrto_profile_read.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_double),
                                         C.POINTER(C.c_int64)]
         L.nrto_pass_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+        L.nrto_case_stats_enable.argtypes = [C.c_void_p, C.c_int32]
+        L.nrto_case_stats_read.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]
+        L.nrto_solve_begin.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+        L.nrto_solve_iterate.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p]
+        L.nrto_solve_flags.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.nrto_solve_end.argtypes = [C.c_void_p, C.POINTER(nrto_out), C.c_void_p]
         for f in ("nrto_layout", "nrto_setup", "nrto_inner_solve", "nrto_gain_update",
                   "nrto_soc_project", "nrto_destroy", "nrto_refresh", "nrto_profile_enable",
-                  "nrto_profile_read", "nrto_pass_bytes"):
+                  "nrto_profile_read", "nrto_pass_bytes", "nrto_case_stats_enable",
+                  "nrto_case_stats_read", "nrto_solve_begin", "nrto_solve_iterate",
+                  "nrto_solve_flags", "nrto_solve_end"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -198,6 +206,38 @@ def nrto_pass_bytes(handle) -> int:
     return int(n.value)
 
 
+def nrto_case_stats_enable(handle, enable=True):
+    _check(lib().nrto_case_stats_enable(C.c_void_p(handle), int(bool(enable))))
+
+
+def nrto_case_stats_read(handle, L) -> np.ndarray:
+    """[L, 3] int64 counts of projection cases 1/2/3 per iteration of the last FullADMM solve."""
+    out = np.zeros((int(L), 3), np.int64)
+    _check(lib().nrto_case_stats_read(C.c_void_p(handle), out.ctypes.data_as(C.POINTER(C.c_int64)),
+                                      int(L)))
+    return out
+
+
+def nrto_solve_begin(handle, engine, stream=None):
+    _check(lib().nrto_solve_begin(C.c_void_p(handle), int(engine), _stream_ptr(stream)))
+
+
+def nrto_solve_iterate(handle, n_iters, stream=None) -> int:
+    done = C.c_int32()
+    _check(lib().nrto_solve_iterate(C.c_void_p(handle), int(n_iters), C.byref(done), _stream_ptr(stream)))
+    return int(done.value)
+
+
+def nrto_solve_flags(handle, flags, stream=None):
+    """flags: device float64 tensor [4] <- [max r_p/eps_p, max r_d/eps_d, #active, any diverged]."""
+    _check(lib().nrto_solve_flags(C.c_void_p(handle), _ptr(flags), _stream_ptr(stream)))
+
+
+def nrto_solve_end(handle, out: dict, stream=None, memory=NRTO_MEM_DEVICE):
+    o = nrto_out(memory, *[_ptr(out.get(k)) for k in OUT_FIELDS])
+    _check(lib().nrto_solve_end(C.c_void_p(handle), C.byref(o), _stream_ptr(stream)))
+
+
 def nrto_inner_solve(handle, engine, out: dict, stream=None, memory=NRTO_MEM_DEVICE):
     o = nrto_out(memory, *[_ptr(out.get(k)) for k in OUT_FIELDS])
     _check(lib().nrto_inner_solve(C.c_void_p(handle), int(engine), C.byref(o), _stream_ptr(stream)))
@@ -276,6 +316,39 @@ class InnerSolver:
 
     def pass_bytes(self):
         return nrto_pass_bytes(self.handle)
+
+    def case_stats(self, enable=True):
+        nrto_case_stats_enable(self.handle, enable)
+
+    def case_stats_read(self, L=None):
+        return nrto_case_stats_read(self.handle, self.params.max_iter if L is None else L)
+
+    def solve_collective(self, engine=NRTO_FULLADMM, out=None, check_every=None, allreduce=None,
+                         full=True):
+        """Termination-mode solve driven in chunks of `check_every` outer iterations
+        with a batch-wide test between chunks: `allreduce(flags)`
+        reduces the device flags [max r_p/eps_p, max r_d/eps_d, #active, diverged]
+        in place with MAX (e.g. torch.distributed.all_reduce over NCCL); the
+        loop stops once no instance on any rank is active.  Returns (out,
+        number of collectives)."""
+        import torch
+        if out is None:
+            out = alloc_out(self.shape, self.batch, self.E, device="cuda", full=full)
+        ce = int(check_every or self.params.check_every)
+        L = self.params.max_iter if engine == NRTO_FULLADMM else self.params.max_admm_iter
+        flags = torch.zeros(4, dtype=torch.float64, device="cuda")
+        nrto_solve_begin(self.handle, engine, self.stream)
+        done, ncoll = 0, 0
+        while done < L:
+            done = nrto_solve_iterate(self.handle, ce, self.stream)
+            nrto_solve_flags(self.handle, flags, self.stream)
+            if allreduce is not None:
+                allreduce(flags)
+                ncoll += 1
+            if float(flags[2].item()) == 0.0:      # #active (MAX over ranks: anyone active)
+                break
+        nrto_solve_end(self.handle, out, self.stream)
+        return out, ncoll
 
     def gain_update(self, nu, kv_prev, kv_next):
         nrto_gain_update(self.handle, nu, kv_prev, kv_next, self.stream)

@@ -66,3 +66,17 @@ def close(x, ref, scale=0.0, tol=1e-9):
     round-off into a relative failure (SURVEY §8c parity protocol)."""
     x = np.asarray(x, float); ref = np.asarray(ref, float)
     return np.linalg.norm(x - ref) <= tol * (np.linalg.norm(ref) + scale) + 1e-300
+
+
+def elementwise(x, ref, floor_frac=1e-3):
+    """Element-wise parity metric: max_i |x_i - ref_i| / (|ref_i| + f ||ref||_inf).
+
+    Complements `close` (normwise): an error confined to a small subset of the
+    entries (e.g. the control-cone part of nu) is visible here even when it is
+    invisible in the norm of the whole array.  The floor f ||ref||_inf keeps
+    entries that are zero up to round-off (cancellation) from dividing by ~0."""
+    x = np.asarray(x, float).ravel(); ref = np.asarray(ref, float).ravel()
+    if ref.size == 0:
+        return 0.0
+    den = np.abs(ref) + floor_frac * max(np.max(np.abs(ref)), 1e-300)
+    return float(np.max(np.abs(x - ref) / den))

@@ -1,0 +1,260 @@
+"""GPU parity of the exact bench path and of the configurations round 1 left untested.
+
+* the bench workload itself: c5, B = 512, T = 100, L = 50 fixed iterations, in
+  the overlapped schedule bench.py times (B >= #SMs: QP(l) on the low-priority
+  stream beside pass(l+1), persistent QP grid looping over > 1 instance per CTA,
+  control cones on the second high-priority stream, lazy y) -- instances
+  {0, 137, 300, 511} against the oracle normwise AND element-wise, and the
+  stationarity invariant sum_j rho A_hat_j^T lam_nu,j + Q_v k_v = 0
+  on EVERY instance, evaluated by an independent torch checker (test-side code,
+  plain batched matmuls, no libnrto kernel);
+* the same workload with termination on (eps_p = eps_d = 1e-3): the iteration at
+  which each sampled instance stops equals the oracle's, recorded by
+  scripts/workload_check.py (oracle only) in tests/golden/workload_c3_c5.json;
+* c2 NRTO-DR at the bench's 40 x 100 warm-started configuration;
+* c4 at T = 800 (generic pass, dense list adjoint, 128-thread QP, DR long-cone pass);
+* random SPD W_K, non-diagonal R_u and a distinct Psi_k per step;
+* a NaN input gives status NRTO_DIVERGED for that instance only;
+* nrto_gain_update between two DR solves leaves the DR warm start intact.
+
+Element-wise parity (tests.helpers.elementwise): max_i |x_i - ref_i| /
+(|ref_i| + f ||ref||_inf) <= tol, f = 1e-3 -- an error confined to a small subset
+of entries (e.g. the control-cone entries of nu) cannot hide in a norm.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from gen import make_instance, make_batch, stack_instances
+from gen.problems import make_franka, make_quad, make_unicycle
+from oracle import structured as st
+from oracle.params import make_params
+from tests.helpers import close, elementwise, golden
+
+from paper_2603_02642_b200 import nrto
+
+from tests.test_gpu_parity import assert_parity, gpu_solve, oracle_run, single, _require_gpu
+
+
+def _inst(batch, i):
+    d = {k: np.array(v[i]) for k, v in batch.items()}
+    d["tau"] = float(d["tau"]); d["r_trust"] = float(d["r_trust"])
+    return d
+
+
+def assert_elementwise(g, o, i=0, tol=1e-9, engine=0):
+    keys = ["kv", "du", "p", "p_tilde"] + (["nu"] if engine == 0 else [])
+    for k in keys:
+        err = elementwise(g[k][i], o[k])
+        assert err <= tol, f"{k}: element-wise {err:.3e} > {tol:.1e}"
+
+
+# ------------------------------------------------ independent stationarity checker
+def stationarity_torch(shape, batch, kv, lam_nu, rho, dev):
+    """|| sum_j rho A_hat_j^T lam_nu,j + Q_v k_v || per instance, relative to
+    1 + ||Q_v k_v||, from the definitions of P:846-869 (costate sweeps
+    c_{j,k} = A_k^T c_{j,k+1}, b_{j,k} = B_k^T c_{j,k+1}; block k of A_hat_j^T e_j =
+    sqrt(tau) vec(b_{j,k} (Psi_k^T e_{j,k})^T); Q_v = 2 blkdiag(I (x) W_k)).
+    Plain batched torch matmuls on the GPU (test-side; shares no code with libnrto)."""
+    B = kv.shape[0]
+    nx, nu, T = shape.n_x, shape.n_u, shape.T
+    knot = np.asarray(shape.cone_knot); kind = np.asarray(shape.cone_kind)
+    off = st.ragged_layout(shape)
+    t = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float64, device=dev)
+    A, Bm, grad, Psi = t(batch["A"]), t(batch["B"]), t(batch["grad"]), t(batch["Psi"])
+    W = t(batch["W_K"]); sq = torch.sqrt(t(batch["tau"])).view(B, 1, 1)
+    lam = torch.as_tensor(lam_nu, device=dev)
+    G = torch.zeros(B, T, nu, nx, dtype=torch.float64, device=dev)
+    for kj in range(1, T + 1):                        # state cones, grouped by knot
+        rows = np.nonzero((kind == 0) & (knot == kj))[0]
+        if len(rows) == 0:
+            continue
+        c = grad[:, rows, :]                           # c_{j,k_j} = grad g_j
+        for k in range(kj - 1, -1, -1):
+            b = torch.einsum("brx,bxu->bru", c, Bm[:, k])          # B_k^T c_{j,k+1}
+            idx = torch.as_tensor((off[rows][:, None] + k * nx + np.arange(nx)[None, :]), device=dev)
+            e = lam[:, idx]                                         # [B, r, nx]
+            pe = torch.einsum("brx,bxy->bry", e, Psi[:, k])        # (Psi_k^T e)^T
+            G[:, k] += torch.einsum("bru,bry->buy", b, pe)
+            c = torch.einsum("brx,bxy->bry", c, A[:, k])           # A_k^T c_{j,k+1}
+    for k in range(T):                                 # control cones: b = h'_j at block k
+        rows = np.nonzero((kind == 1) & (knot == k))[0]
+        if len(rows) == 0:
+            continue
+        b = grad[:, rows, :nu]
+        idx = torch.as_tensor(off[rows][:, None] + np.arange(nx)[None, :], device=dev)
+        pe = torch.einsum("brx,bxy->bry", lam[:, idx], Psi[:, k])
+        G[:, k] += torch.einsum("bru,bry->buy", b, pe)
+    K = torch.as_tensor(kv, device=dev).view(B, T, nx, nu).transpose(-1, -2)   # column-major vec
+    QK = 2.0 * torch.einsum("bkuv,bkvx->bkux", W, K)
+    R = QK + rho * sq.view(B, 1, 1, 1) * G
+    res = torch.linalg.vector_norm(R.reshape(B, -1), dim=1)
+    ref = 1.0 + torch.linalg.vector_norm(QK.reshape(B, -1), dim=1)
+    return (res / ref).cpu().numpy()
+
+
+# --------------------------------------------------------------- the bench path
+@pytest.fixture(scope="module")
+def bench_batch():
+    return make_batch("c5", 512)
+
+
+def test_bench_path_overlapped_b512(bench_batch):
+    """The exact bench configuration (bench.py: c5, 512 instances, L = 50,
+    fixed_iters, overlapped schedule) against the oracle, element-wise."""
+    _require_gpu()
+    shape, batch = bench_batch
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    assert 512 >= 2 * nsm, "the persistent QP grid must loop over > 1 instance per CTA"
+    L = 50
+    data = nrto.to_tensors(batch, device="cuda")
+    s = nrto.InnerSolver(shape, data, max_iter=L, fixed_iters=1)
+    out = nrto.alloc_out(shape, 512, s.E, device="cuda", full=True)
+    s.solve(nrto.NRTO_FULLADMM, out=out)          # first solve (state of a fresh handle)
+    s.solve(nrto.NRTO_FULLADMM, out=out)          # second solve: the bench's steady state
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    for k in ("kv", "du", "p", "p_tilde", "lam_p", "nu", "lam_nu", "objective", "margin_cone",
+              "margin_lin", "r_p", "r_d"):
+        assert np.all(np.isfinite(g[k])), k
+    assert np.all(g["iters"] == L) and np.all(g["status"] == nrto.NRTO_MAX_ITERS)
+    for i in (0, 137, 300, 511):
+        o = oracle_run(shape, _inst(batch, i), nrto.NRTO_FULLADMM, max_iter=L, fixed_iters=1)
+        assert_parity(g, o, i=i)
+        assert_elementwise(g, o, i=i)
+    inv = stationarity_torch(shape, batch, out["kv"], out["lam_nu"], 10.0, "cuda")
+    assert np.all(inv <= 1e-10), f"stationarity invariant max {inv.max():.3e}"
+    s.close()
+
+
+def test_bench_workload_converges_like_the_oracle(bench_batch):
+    """Termination on (eps_p = eps_d = 1e-3, checked every iteration, L_max = 600):
+    the sampled instances stop at the oracle's iteration (golden record written
+    by scripts/workload_check.py, oracle only) and every instance converges."""
+    _require_gpu()
+    shape, batch = bench_batch
+    ref = {(c["cfg"], c["instance"]): c for c in golden("workload_c3_c5.json")["cases"]}
+    g = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, max_iter=600, eps_p=1e-3, eps_d=1e-3)
+    assert np.all(g["status"] == nrto.NRTO_CONVERGED), \
+        f"{int(np.sum(g['status'] != 0))} instances did not converge in 600 iterations"
+    for i in (0, 137, 300, 511):
+        assert int(g["iters"][i]) == ref[("c5", i)]["iters"], i
+    # c3 (the single-instance Franka config) converges at the oracle's iteration too
+    sh3, d3 = make_instance("c3")
+    g3 = gpu_solve(sh3, single(sh3, d3), nrto.NRTO_FULLADMM, max_iter=600, eps_p=1e-3, eps_d=1e-3)
+    assert int(g3["status"][0]) == 0 and int(g3["iters"][0]) == ref[("c3", 0)]["iters"]
+
+
+# --------------------------------------------------------------- other configs
+def test_c2_dr_bench_configuration():
+    """c2 quadcopter NRTO-DR at the bench's 40 x 100 (fixed, warm-started DR)."""
+    shape, data = make_instance("c2")
+    kw = dict(max_admm_iter=40, max_dr_iter=100, fixed_iters=1)
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_DR, **kw)
+    o = oracle_run(shape, data, nrto.NRTO_DR, **kw)
+    assert_parity(g, o, engine=1)
+    assert_elementwise(g, o, engine=1, tol=1e-8)
+
+
+def test_c4_t800_fulladmm_and_dr():
+    """T = 800 (beyond the TMA pass's shared-memory horizon): the generic pass,
+    dense list adjoint, 128-thread QP and the DR long-cone pass."""
+    shape, data = make_quad(4, 11, T=800, n_obs=2)
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_FULLADMM, max_iter=2, fixed_iters=1)
+    o = oracle_run(shape, data, nrto.NRTO_FULLADMM, max_iter=2, fixed_iters=1)
+    assert_parity(g, o)
+    kw = dict(max_admm_iter=2, max_dr_iter=2, fixed_iters=1)
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_DR, **kw)
+    o = oracle_run(shape, data, nrto.NRTO_DR, **kw)
+    assert_parity(g, o, engine=1)
+
+
+def _random_weights(shape, data, seed):
+    """Random SPD W_K and R_u per step (non-diagonal) and a distinct upper-triangular
+    Psi_k (positive diagonal) per step -- exercises the generalised eigen chain with
+    W != I, non-diagonal R_u in the Riccati / QP, and per-step Psi / U."""
+    rng = np.random.default_rng(seed)
+    T, nu, nx = shape.T, shape.n_u, shape.n_x
+    d = dict(data)
+
+    def spd(n, lo, hi):
+        Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        return (Q * rng.uniform(lo, hi, n)) @ Q.T
+
+    d["W_K"] = np.stack([spd(nu, 0.3, 3.0) for _ in range(T)])
+    d["R_u"] = np.stack([spd(nu, 0.02, 0.5) for _ in range(T)])
+    P = np.array(data["Psi"], float)
+    for k in range(T + 1):
+        U = np.triu(rng.standard_normal((nx, nx))) * 0.3 * np.abs(np.diag(P[k])).mean()
+        U[np.diag_indices(nx)] = np.abs(np.diag(P[k])) * rng.uniform(0.5, 2.0, nx)
+        P[k] = U
+    d["Psi"] = P
+    return d
+
+
+@pytest.mark.parametrize("case", ["c1", "c3s"])
+def test_random_weights_and_psi(case):
+    shape, data = make_instance("c1") if case == "c1" else make_franka(3, 0, T=12)
+    d = _random_weights(shape, data, 7)
+    for L in (2, 20):
+        g = gpu_solve(shape, single(shape, d), nrto.NRTO_FULLADMM, max_iter=L, fixed_iters=1)
+        o = oracle_run(shape, d, nrto.NRTO_FULLADMM, max_iter=L, fixed_iters=1)
+        assert_parity(g, o)
+        assert_elementwise(g, o, tol=1e-8)
+    kw = dict(max_admm_iter=3, max_dr_iter=10, fixed_iters=1)
+    g = gpu_solve(shape, single(shape, d), nrto.NRTO_DR, **kw)
+    o = oracle_run(shape, d, nrto.NRTO_DR, **kw)
+    assert_parity(g, o, engine=1)
+
+
+def test_random_weights_batch_tma_path():
+    """Random W_K / R_u / Psi_k through the batched TMA pass and sparse QP."""
+    items = []
+    for i in range(4):
+        sh, d = make_franka(5, i, T=12, jitter=True)
+        items.append((sh, _random_weights(sh, d, 100 + i)))
+    shape, batch = stack_instances(items)
+    g = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, max_iter=10, fixed_iters=1)
+    for i, (_, d) in enumerate(items):
+        o = oracle_run(shape, d, nrto.NRTO_FULLADMM, max_iter=10, fixed_iters=1)
+        assert_parity(g, o, i=i)
+
+
+def test_nan_input_diverges_that_instance_only():
+    """Non-finite iterates are reported as NRTO_DIVERGED per instance, not
+    as an error; the other instances of the batch are unaffected."""
+    items = [make_unicycle(1, i) for i in range(3)]
+    bad = dict(items[1][1]); g0 = np.array(bad["g0"], float); g0[5] = np.nan; bad["g0"] = g0
+    items[1] = (items[1][0], bad)
+    shape, batch = stack_instances(items)
+    g = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, max_iter=40)
+    assert g["status"][1] == nrto.NRTO_DIVERGED
+    for i in (0, 2):
+        o = oracle_run(shape, items[i][1], nrto.NRTO_FULLADMM, max_iter=40)
+        assert g["status"][i] == o["status"] and g["iters"][i] == o["iters"]
+        assert_parity(g, o, i=i)
+
+
+def test_gain_update_keeps_dr_warm_start():
+    """DR solve -> nrto_gain_update -> DR solve equals DR solve -> DR solve (the DR
+    warm state persists across calls)."""
+    _require_gpu()
+    shape, data = make_instance("c1")
+    kw = dict(max_admm_iter=3, max_dr_iter=10, fixed_iters=1)
+    res = []
+    for between in (False, True):
+        s = nrto.InnerSolver(shape, nrto.to_tensors(single(shape, data), device="cuda"), **kw)
+        o = nrto.alloc_out(shape, 1, s.E, device="cuda")
+        s.solve(nrto.NRTO_DR, out=o)
+        if between:
+            nu = torch.randn(1, s.E, dtype=torch.float64, device="cuda")
+            kp = torch.randn(1, shape.T * shape.n_u * shape.n_x, dtype=torch.float64, device="cuda")
+            s.gain_update(nu, kp, torch.empty_like(kp))
+        s.solve(nrto.NRTO_DR, out=o)
+        torch.cuda.synchronize()
+        res.append({k: v.cpu().numpy() for k, v in o.items()})
+        s.close()
+    for k in ("kv", "du", "p", "p_tilde", "lam_p"):
+        assert close(res[1][k], res[0][k], tol=1e-13), k
