@@ -1,22 +1,28 @@
 #!/usr/bin/env python
 """Benchmark of the NRTO inner solve (one JSON line on rank 0).
 
-Workload: c5 -- a batch of Franka-shaped SOCP subproblems
-(n_x=14, n_u=7, T=100, n_g=4306 cones, E=2.12M ragged cone elements each),
-FullADMM engine, L_max=50 iterations with fixed_iters, per-GPU batch
-fixed (weak scaling; N=8 x 512 = 4096 = c5).  One step = one SL-iteration
-subproblem for the whole batch: nrto_refresh (setup S0-S2 from
-device-resident primitives) + nrto_inner_solve (S3-S10).  Working set per GPU
-is ~22 GB >> 126 MB L2, so no L2 flush is needed between steps.
+Workload: config c5 of BASELINE.json -- a batch of 4096
+independent Franka-shaped SOCP subproblems (n_x=14, n_u=7, T=100, n_g=4306
+cones, E=2.12M ragged cone elements each), FullADMM engine, L=50 iterations
+with fixed_iters, STRONG scaling: rank r of N owns 4096/N instances
+and runs them in waves of <= 512 resident instances (one handle; the 4096
+instances' primitives stay resident in HBM, ~1 MB each).  One step = one
+SL-iteration subproblem for the whole batch: per wave nrto_refresh (setup
+S0-S2 from the device-resident primitives) + nrto_inner_solve (S3-S10).
+The working set (~35 GB per wave) is >> the 126 MB L2: no flush is needed.
 
 `--impl reference` times the CPU oracle (oracle/, as it stands) on a bounded
-sample of the same workload (one instance per step).
+sample of the same workload, one instance per host core per step.
+`--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N processes (one per GPU).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
+import socket
 import subprocess
 import sys
 import threading
@@ -29,6 +35,7 @@ import numpy as np
 
 METRIC = "inner DR/ADMM iters/sec and SOC projections/sec per GPU; SL-iteration wall-clock"
 UNIT = "instance-iterations/s"
+NOMINAL_HBM_GBS = 8000.0       # B200 HBM3e nominal (north_star's "~8 TB/s")
 
 
 def parse():
@@ -37,11 +44,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch-per-gpu", type=int, default=512)
+    ap.add_argument("--instances", type=int, default=4096, help="total instances (strong scaling)")
+    ap.add_argument("--wave", type=int, default=512, help="max resident instances per wave")
     ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--conv-max-iter", type=int, default=600)
     ap.add_argument("--workload", default="c5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-conv", action="store_true")
     ap.add_argument("--no-dr", action="store_true")
     return ap.parse_args()
 
@@ -90,41 +100,83 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def workload_shape_stats(shape):
+def shape_stats(shape):
+    """E, E_s, E_B (state rows), n_ctrl -- SURVEY §8(d) notation."""
     nx, nu = shape.n_x, shape.n_u
     knot = np.asarray(shape.cone_knot, np.int64)
-    kind = np.asarray(shape.cone_kind)
-    st = kind == 0
+    st = np.asarray(shape.cone_kind) == 0
     E_s = int(((knot[st] + 1) * nx).sum())
-    E = E_s + int((~st).sum()) * nx
-    E_B = int((knot[st] * nu).sum()) + int((~st).sum()) * nu
-    return E, E_s, E_B
+    n_ctrl = int((~st).sum())
+    E = E_s + n_ctrl * nx
+    E_B = int((knot[st] * nu).sum())
+    return E, E_s, E_B, n_ctrl
 
 
-def cpu_oracle_sample(cfg, L, n_inst=1, seed0=0):
-    """Time the oracle (as it stands) on n_inst instances x L iterations, 1 thread."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
+def _gen_chunk(args):
+    cfg, first, n = args
+    from gen import make_batch
+    return make_batch(cfg, n, start=first)
+
+
+def make_shard(cfg, first, count, procs=None):
+    """The rank's instances (gen/, seeded per instance), generated in a process pool."""
+    from gen import stack_instances  # noqa: F401  (import check)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    procs = procs or max(1, min(16, (os.cpu_count() or 1) // world))
+    chunks = []
+    step = max(1, (count + procs - 1) // procs)
+    for a in range(first, first + count, step):
+        chunks.append((cfg, a, min(step, first + count - a)))
+    if len(chunks) == 1:
+        return _gen_chunk(chunks[0])
+    import multiprocessing as mp
+    with mp.get_context("spawn").Pool(min(procs, len(chunks))) as pool:
+        parts = pool.map(_gen_chunk, chunks)
+    shape = parts[0][0]
+    batch = {k: np.concatenate([p[1][k] for p in parts]) for k in parts[0][1]}
+    return shape, batch
+
+
+def _oracle_worker(args):
+    cfg, i, L = args
     from threadpoolctl import threadpool_limits
     from gen import make_instance
     from oracle import structured as st
     from oracle.params import make_params
-    items = [make_instance(cfg, seed0 + i) for i in range(n_inst)]
     with threadpool_limits(limits=1):
+        shape, data = make_instance(cfg, i)
         t0 = time.perf_counter()
-        for shape, data in items:
-            sp = st.StructuredProblem(shape, data)
-            st.fulladmm(sp, make_params(max_iter=L, fixed_iters=1))
-        dt = time.perf_counter() - t0
-    return n_inst * L / dt, dt
+        sp = st.StructuredProblem(shape, data)
+        st.fulladmm(sp, make_params(max_iter=L, fixed_iters=1))
+        return time.perf_counter() - t0
 
 
-def workload_config(args, world, shape, E, E_B):
-    """The `config` of both arms (ours and --impl reference)."""
-    B, L = args.batch_per_gpu, args.iters
-    return {"workload": f"{args.workload}: batch of Franka-shaped SOCP subproblems "
-                        f"(n_x=14, n_u=7, T=100, n_g={shape.n_g}, E={E}), FullADMM, "
-                        f"L={L} fixed iterations, {B} instances/GPU",
-            "global_batch": world * B, "parallelism": f"instances sharded dp{world}",
-            "l2": "inputs larger than L2 (working set ~%.0f GB/GPU)" % (B * 8 * (2 * E + E_B) / 1e9)}
+def cpu_oracle_sample(cfg, L, seed0=0, cores=None):
+    """The oracle as it stands, one single-threaded process per host core, each
+    solving one instance x L FullADMM iterations (setup included).  Returns
+    (instance-iterations/s over the wall time, wall s, cores used, 1-core rate)."""
+    cores = cores or max(1, min(32, os.cpu_count() or 1))
+    jobs = [(cfg, seed0 + i, L) for i in range(cores)]
+    import multiprocessing as mp
+    t0 = time.perf_counter()
+    if cores == 1:
+        per = [_oracle_worker(jobs[0])]
+    else:
+        with mp.get_context("spawn").Pool(cores) as pool:
+            per = pool.map(_oracle_worker, jobs)
+    wall = time.perf_counter() - t0
+    return cores * L / wall, wall, cores, L / float(np.mean(per))
 
 
 def load_peaks():
@@ -132,8 +184,18 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             j = json.load(f)
-        return float(j["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def workload_config(args, world, shape, E, per_rank, wave):
+    return {"workload": f"{args.workload}: {args.instances} Franka-shaped SOCP subproblems "
+                        f"(n_x=14, n_u=7, T=100, n_g={shape.n_g}, E={E}) sharded over "
+                        f"{world} GPU(s), FullADMM, L={args.iters} fixed iterations; "
+                        f"{per_rank} instances/GPU in waves of {wave}",
+            "global_batch": args.instances, "parallelism": f"instances sharded dp{world}",
+            "l2": "inputs larger than L2 (working set ~%.0f GB per wave)"
+                  % (wave * 8 * (3 * E + E) / 1e9)}
 
 
 # -------------------------------------------------------------- reference
@@ -141,29 +203,31 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     L = args.iters
-    cfg = "c5" if args.workload == "c5" else args.workload
-    for _ in range(args.warmup):
-        cpu_oracle_sample(cfg, L, 1, seed0=0)
-    times = []
+    cfg = args.workload
+    cpu_oracle_sample(cfg, L, seed0=0, cores=1)          # warm the interpreter / imports
+    walls, rates, cores = [], [], 1
     for s in range(args.steps):
-        v, dt = cpu_oracle_sample(cfg, L, 1, seed0=s + 1)
-        times.append(dt)
-    ms = 1000.0 * float(np.mean(times))
-    value = L / (ms / 1000.0)
-    sample = (f"bounded sample: 1 {cfg} instance x {L} FullADMM iterations (+ setup) per step "
-              f"(of the {args.batch_per_gpu} instances/GPU of the workload), 1 host thread")
+        v, wall, cores, _ = cpu_oracle_sample(cfg, L, seed0=1000 + s * 64)
+        walls.append(wall)
+        rates.append(v)
+    ms = 1000.0 * float(np.mean(walls))
+    value = cores * L / (ms / 1000.0)
+    sample = (f"bounded sample: {cores} {cfg} instances x {L} FullADMM iterations (+ setup) per "
+              f"step, one single-threaded oracle process per host core ({cores} of "
+              f"{os.cpu_count()} cores, {cpu_model()})")
     from gen import make_instance
     shape, _ = make_instance(cfg, 0)
-    E, _, E_B = workload_shape_stats(shape)
-    config = workload_config(args, world, shape, E, E_B)
+    E = shape_stats(shape)[0]
+    per_rank = args.instances // max(1, world)
+    config = workload_config(args, world, shape, E, per_rank, min(args.wave, per_rank))
     config["sample"] = sample
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen/, seeded PCG64)",
             "config": config,
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -179,38 +243,47 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
     from paper_2603_02642_b200 import nrto
-    from paper_2603_02642_b200.dist import instance_range, max_over_ranks, batch_stats
-    from gen import make_batch
+    from paper_2603_02642_b200.dist import (strong_range, max_over_ranks, batch_stats,
+                                            solve_collective, nccl_max)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    B, L = args.batch_per_gpu, args.iters
-    first, count = instance_range(rank, world, B)
-    shape, batch = make_batch(args.workload, count, start=first)
-    E, E_s, E_B = workload_shape_stats(shape)
-    data_dev = nrto.to_tensors(batch, device=dev)
-    solver = nrto.InnerSolver(shape, data_dev, max_iter=L, fixed_iters=1)
-    out = nrto.alloc_out(shape, B, solver.E, device=dev, full=True)
-    out.pop("nu"); out.pop("lam_nu")          # optional ragged outputs not requested
+    L = args.iters
+    first, count = strong_range(rank, world, args.instances)
+    nw = max(1, -(-count // args.wave))
+    wave = -(-count // nw)
+    waves = [(a, min(wave, count - a)) for a in range(0, count, wave)]
+    shape, batch = make_shard(args.workload, first, count)
+    E, E_s, E_B, n_ctrl = shape_stats(shape)
+    data_dev = nrto.to_tensors(batch, device=dev)            # primitives of every instance, resident
+    sl = lambda d, a, n: {k: v[a:a + n] for k, v in d.items()}
+    solvers = {}
+    for a, n in waves:                                        # one handle per distinct wave size
+        if n not in solvers:
+            solvers[n] = nrto.InnerSolver(shape, sl(data_dev, a, n), max_iter=L, fixed_iters=1)
+    out = nrto.alloc_out(shape, count, solvers[wave].E, device=dev, full=True, ragged=False)
     stream = torch.cuda.current_stream()
 
     def step():
-        solver.refresh(data_dev)
-        solver.solve(nrto.NRTO_FULLADMM, out=out)
+        for a, n in waves:
+            s = solvers[n]
+            s.refresh(sl(data_dev, a, n))
+            s.solve(nrto.NRTO_FULLADMM, out=sl(out, a, n))
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    def launches():
+        return sum(s.launches() for s in solvers.values())
+
+    # ---- headline: device-resident inputs, profiler OFF (production launch path)
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    solver.profile(True)
-    solver.profile_read()                      # clear
-    solver.pass_bytes()                        # clear the pass byte counter
-    l0 = solver.launches()
+    l0 = launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
@@ -219,26 +292,49 @@ def run_ours(args, rank, world, local_rank):
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    launches = solver.launches() - l0
-    prof = solver.profile_read()
-    moved = solver.pass_bytes()                # algorithmic bytes of k_fa_tma in the timed steps
-    solver.profile(False)
+    n_launch = launches() - l0
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_max = max_over_ranks(ms, device=dev)
-    value = world * B * L / (ms_max / 1000.0)
+    value = args.instances * L / (ms_max / 1000.0)
+
+    # ---- profiled pass (separate, 1 step): per-kernel-class device time (CUDA events on
+    # each launching stream), the pass kernel's own byte counter, projection-case mix
+    for s in solvers.values():
+        s.profile(True); s.profile_read(); s.pass_bytes(); s.case_stats(True)
+    torch.cuda.synchronize()
+    case_tot = np.zeros((L, 3), np.int64)
+    for a, n in waves:
+        s = solvers[n]
+        s.refresh(sl(data_dev, a, n))
+        s.solve(nrto.NRTO_FULLADMM, out=sl(out, a, n))
+        case_tot += s.case_stats_read(L)
+    torch.cuda.synchronize()
+    prof = {}
+    moved = 0
+    for s in solvers.values():
+        for k, (t_ms, n_l) in s.profile_read().items():
+            a0, b0 = prof.get(k, (0.0, 0))
+            prof[k] = (a0 + t_ms, b0 + n_l)
+        moved += s.pass_bytes()
+        s.profile(False); s.case_stats(False)
+
+    # batch-wide residual statistics of the fixed-L solve (allreduce over ranks)
+    max_rp, n_unconv, any_div = batch_stats(out["r_p"], out["status"], device=dev)
 
     # ---- end to end through the C ABI with HOST buffers (H2D + D2H inside)
     e2e = None
     if not args.no_e2e:
         data_host = nrto.to_tensors(batch, device="cpu", pinned=True)
-        out_h = nrto.alloc_out(shape, B, solver.E, device="cpu", pinned=True, full=True)
-        out_h.pop("nu"); out_h.pop("lam_nu")
+        out_h = nrto.alloc_out(shape, count, solvers[wave].E, device="cpu", pinned=True, full=True,
+                               ragged=False)
         h2d = sum(v.numel() * v.element_size() for v in data_host.values())
         d2h = sum(v.numel() * v.element_size() for v in out_h.values())
 
         def step_e2e():
-            solver.refresh(data_host, memory=nrto.NRTO_MEM_HOST)
-            solver.solve(nrto.NRTO_FULLADMM, out=out_h, memory=nrto.NRTO_MEM_HOST)
+            for a, n in waves:
+                s = solvers[n]
+                s.refresh(sl(data_host, a, n), memory=nrto.NRTO_MEM_HOST)
+                s.solve(nrto.NRTO_FULLADMM, out=sl(out_h, a, n), memory=nrto.NRTO_MEM_HOST)
 
         step_e2e()
         torch.cuda.synchronize()
@@ -251,16 +347,76 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         barrier()
         ems = max_over_ranks(ev2.elapsed_time(ev3) / args.steps, device=dev)
-        e2e = {"value": world * B * L / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "sl_iteration_wall_clock_ms": ems}
+        e2e = {"value": args.instances * L / (ems / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d) * world, "d2h_bytes_per_step": int(d2h) * world,
+               "ms_per_step": ems,
+               "note": "refresh from pinned host primitives + fixed-L solve + D2H of every "
+                       "output, per wave, all ranks; bytes summed over ranks"}
 
-    # secondary line: the NRTO-DR engine on its own config (c2 quadcopter, one
-    # instance, 40 NRTO-ADMM x 100 DR iterations, fixed) -- latency-bound, reported
-    # as DR iterations/s (S3-S8 per DR iteration) and NRTO-ADMM iterations/s
-    dr = None
+    # ---- SL-iteration wall-clock to CONVERGENCE (termination on, eps_p = eps_d = 1e-3,
+    # L_max = conv-max-iter): host pinned inputs -> refresh -> solve to convergence with
+    # the batch-wide allreduce(MAX) of the residual flags every iteration (SURVEY §8e,
+    # nrto_solve_* incremental ABI) -> D2H of the outputs; device events, max over ranks
+    conv = None
+    if not args.no_conv:
+        for sv in solvers.values():           # free the fixed-L handles (HBM) first
+            sv.close()
+        csol = {}
+        for a, n in waves:
+            if n not in csol:
+                csol[n] = nrto.InnerSolver(shape, sl(data_dev, a, n), max_iter=args.conv_max_iter,
+                                           eps_p=1e-3, eps_d=1e-3, check_every=1)
+        data_host = data_host if e2e else nrto.to_tensors(batch, device="cpu", pinned=True)
+        Ew = nrto.nrto_layout(shape, 1)[0]
+        out_c = nrto.alloc_out(shape, count, Ew, device="cpu", pinned=True, full=True, ragged=False)
+        out_cd = nrto.alloc_out(shape, count, Ew, device=dev, full=True, ragged=False)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ev4, ev5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev4.record(stream)
+        ncoll, iters_run = 0, 0
+        for a, n in waves:
+            s = csol[n]
+            s.refresh(sl(data_host, a, n), memory=nrto.NRTO_MEM_HOST)
+            o, done, nc = solve_collective(s, nrto.NRTO_FULLADMM, out=sl(out_cd, a, n),
+                                           allreduce=nccl_max if world > 1 else None)
+            ncoll += nc
+            iters_run += done
+            for k in out_c:
+                out_c[k][a:a + n].copy_(o[k], non_blocking=True)
+        ev5.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        cms = max_over_ranks(ev4.elapsed_time(ev5), device=dev)
+        wall = max_over_ranks(wall * 1000.0, device=dev)
+        its = out_c["iters"].numpy().astype(np.float64)
+        stt = out_c["status"].numpy()
+        if world > 1:
+            g_its = [None] * world
+            dist.all_gather_object(g_its, (its.tolist(), stt.tolist()))
+            its = np.concatenate([np.asarray(x[0]) for x in g_its])
+            stt = np.concatenate([np.asarray(x[1]) for x in g_its])
+        inst_its = float(its.sum())
+        conv = {"eps_p": 1e-3, "eps_d": 1e-3, "max_iter": args.conv_max_iter, "check_every": 1,
+                "iters_to_converge": {"p50": float(np.median(its)), "max": float(its.max()),
+                                      "min": float(its.min()), "mean": float(its.mean())},
+                "converged": int((stt == 0).sum()), "instances": int(len(stt)),
+                "diverged": int((stt == 2).sum()),
+                "sl_iteration_wall_clock_ms": cms, "host_wall_ms": wall,
+                "instance_iterations_per_s": inst_its / (cms / 1000.0),
+                "collectives_per_rank": ncoll,
+                "note": "one SL iteration for the whole batch: H2D of the primitives, setup, "
+                        "inner solve to convergence (per-instance freeze, batch-wide "
+                        "termination allreduce every iteration), D2H of the outputs"}
+        for s in csol.values():
+            s.close()
+
+    # secondary lines (rank 0): NRTO-DR engine on c2 (configs[1]) and single-instance
+    # latency of c1 (both engines) and c3 -- CUDA-graph replay of the fixed loop
+    dr, singles = None, None
     if not args.no_dr and rank == 0:
-        from gen import make_instance
-        from gen.problems import stack_instances
+        from gen import make_instance, stack_instances
         shp2, d2 = make_instance("c2")
         dd2 = nrto.to_tensors(stack_instances([(shp2, d2)])[1], device=dev)
         s2 = nrto.InnerSolver(shp2, dd2, fixed_iters=1)
@@ -280,13 +436,6 @@ def run_ours(args, rank, world, local_rank):
               "dr_iters_per_s": La * Ld / (dms / 1000.0),
               "admm_iters_per_s": La / (dms / 1000.0), "ms_per_solve": dms}
         s2.close()
-
-    # single-instance lines of the other configs (latency-bound; CUDA-graph replay of
-    # the fixed-iteration loop): c1 unicycle (both engines), c3 Franka FullADMM
-    singles = None
-    if not args.no_dr and rank == 0:
-        from gen import make_instance
-        from gen.problems import stack_instances
         singles = {}
         for cfg, eng, name in (("c1", nrto.NRTO_FULLADMM, "c1_fulladmm"), ("c1", nrto.NRTO_DR, "c1_dr"),
                                ("c3", nrto.NRTO_FULLADMM, "c3_fulladmm")):
@@ -318,67 +467,112 @@ def run_ours(args, rank, world, local_rank):
                                  "ms_per_solve": sms}
             s3.close()
 
-    # batch-wide residual statistics over NVLink (the only collective)
-    max_rp, n_unconv, any_div = batch_stats(out["r_p"], out["status"], device=dev)
-
+    # case mix over all ranks (SURVEY §8d representativeness rule: case 3 >= 5 % after l = 5)
+    ct = torch.as_tensor(case_tot, dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ct)
+    case_tot = ct.cpu().numpy()
     if rank != 0:
         return
+    after = case_tot[5:].sum(0)
+    share = after / max(after.sum(), 1.0)
+    first5 = case_tot[:5].sum(0) / max(case_tot[:5].sum(), 1.0)
+    case_mix = {"after_iter5": {"case1": float(share[0]), "case2": float(share[1]), "case3": float(share[2])},
+                "iters_1_to_5": {"case1": float(first5[0]), "case2": float(first5[1]), "case3": float(first5[2])},
+                "representative": bool(share[2] >= 0.05),
+                "rule": "case 3 >= 5 % of projections after iteration 5 (SURVEY §8d)"}
+
     peak, peak_kind = load_peaks()
-    # roofline of k_fa_tma: algorithmic bytes = b_hat + b of every state-cone
-    # block, y^{l-1} of cones with s^{l-1} != 1, y^l where stored -- counted by the
-    # kernel itself (nrto_pass_bytes) -- over its event-timed device time in the steps
+    # roofline of the dominant kernel k_fa_tma (state cones):
+    #   achieved (§8d) = SURVEY §8(d) algorithmic bytes of the state-cone stream per
+    #     instance-iteration, 8 (2 E_s + E_s + E_B), x the instances of a launch, / its
+    #     event-timed average duration in the profiled step (same launch path as the headline)
+    #   dram = the bytes the kernel itself counts (lazy y: b_hat + b + y where read /
+    #     stored), same time -- what HBM actually carries (ncu agrees, `traffic`)
     pms, pn = prof["pass"]
-    bytes_per_launch = moved / pn if pn else None
-    achieved = moved / (pms / 1000.0) / 1e9 if pms else None
+    bytes8d = 8 * (3 * E_s + E_B)
+    inst_per_launch = float(count) / max(1, len(waves))
+    t_launch = (pms / pn) / 1000.0 if pn else None
+    achieved = bytes8d * inst_per_launch / t_launch / 1e9 if t_launch else None
+    dram_gbs = (moved / pn) / t_launch / 1e9 if t_launch else None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "pass_traffic.json")
     if os.path.exists(tf):
         try:
             tj = json.load(open(tf))
-            if tj.get("batch") == B and tj.get("iters") == L:
+            if tj.get("wave") == wave and tj.get("iters") == L:
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             pass
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v1, dt = cpu_oracle_sample(args.workload, L, 1, seed0=0)
-        cpu = {"value": v1, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"1 {args.workload} instance x {L} FullADMM iterations incl. setup "
-                         f"({dt:.1f} s, 1 host thread)"}
-    kernel_ms = {k: (v[0] / args.steps) for k, v in prof.items()}
+        v_all, wall, cores, v1 = cpu_oracle_sample(args.workload, L, seed0=0)
+        cpu = {"value": v_all, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{cores} {args.workload} instances x {L} FullADMM iterations incl. setup, "
+                         f"one single-threaded oracle process per core ({wall:.1f} s wall)",
+               "value_1core": v1, "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    kernel_ms = {k: (v[0]) for k, v in prof.items()}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (gen/, seeded PCG64; no datasets or trained weights)",
-        "config": workload_config(args, world, shape, E, E_B),
+        "config": workload_config(args, world, shape, E, count, wave),
+        "value_per_gpu": value / world,
         "soc_projections_per_s": value * shape.n_g,
         "cone_elements_per_s": value * E,
-        "sl_iteration_wall_clock_ms": (e2e or {}).get("sl_iteration_wall_clock_ms"),
+        "sl_iteration_wall_clock_ms": (conv or {}).get("sl_iteration_wall_clock_ms"),
+        "convergence": conv,
+        "case_mix": case_mix,
         "kernel_ms_per_step": kernel_ms,
-        "kernel_ms_note": ("CUDA-event time per kernel class on its own stream; qp (low-priority "
-                           "stream) and ctrl (second high-priority stream) run concurrently with "
-                           "pass / adjoint / gain, so the classes overlap and do not add up to the step"),
-        "roofline": {"bound": "hbm", "kernel": "k_fa_tma: fused state-cone pass (S3 forward map + "
-                                                "S4 SOC norms + S5 state update)",
+        "kernel_ms_note": ("one separate profiled step (CUDA events per kernel class on its launching "
+                           "stream); qp (low-priority stream) and ctrl (second high-priority stream) "
+                           "run concurrently with pass / adjoint / gain, so classes overlap and do not "
+                           "add up to the step; the headline steps run with the profiler off"),
+        "roofline": {"bound": "hbm",
+                     "kernel": "k_fa_tma: fused state-cone pass (S3 forward map + S4 SOC norms + "
+                               "S5 state update)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": bytes_per_launch},
+                     "frac_vs_nominal_8tbs": (achieved / NOMINAL_HBM_GBS) if achieved else None,
+                     "algorithmic_bytes_per_launch": bytes8d * inst_per_launch,
+                     "algorithmic_bytes_def": "SURVEY 8(d): 8 (2 E_s + E_s + E_B) per instance-iteration "
+                                              "(state-cone row read+write, b_hat, b) x instances per launch",
+                     "dram_achieved": dram_gbs,
+                     "dram_frac": (dram_gbs / peak) if dram_gbs else None,
+                     "dram_bytes_per_launch": (moved / pn) if pn else None,
+                     "dram_def": "bytes the kernel moves (lazy y: b_hat + b of every block, y^{l-1} "
+                                 "read / y^l stored only where needed), counted by the kernel",
+                     "avg_launch_ms": (pms / pn) if pn else None, "launches": pn},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": int(launches),
+        "gpu_launches": int(n_launch),
         "clocks": clk.summary(),
         "dr_engine": dr,
         "single_instance": singles,
-        "residuals": {"max_r_p": max_rp, "unconverged_instances": n_unconv,
+        "residuals": {"max_r_p_at_L": max_rp, "unconverged_at_L": n_unconv,
                       "any_diverged": any_div},
     }
     print(json.dumps(line), flush=True)
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -388,6 +582,7 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:

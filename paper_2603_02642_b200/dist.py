@@ -2,9 +2,11 @@
 
 Instances are independent: rank r of N owns a contiguous range
 of instances and its own nrto handle; no data-path collective exists.  The
-only collectives are the max-over-ranks step time and the batch-wide
-residual statistics (max r_p, #unconverged, any diverged), done through
-torch.distributed (NCCL over NVLink on the GPU box, gloo in CPU tests).
+collectives are the batch-wide termination test inside the loop (allreduce MAX
+of the 4 residual flags every check_every outer iterations, `solve_collective`),
+the max-over-ranks step time and the final residual statistics (max r_p,
+#unconverged, any diverged), done through torch.distributed (NCCL over NVLink
+on the GPU box, gloo in CPU tests).
 """
 from __future__ import annotations
 
@@ -46,3 +48,56 @@ def batch_stats(r_p, status, device=None):
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
     return float(mx.item()), int(cnt[0].item()), bool(cnt[1].item() > 0)
+
+
+def collective_loop(iterate, read_flags, allreduce, L: int, check_every: int):
+    """Host loop of the multi-rank termination test (Algorithm 1 line 9, P:522;
+    SURVEY §8e).  `iterate(n)` runs up to n more outer iterations and returns the
+    number run so far; `read_flags()` returns the 4-vector [max r_p/eps_p,
+    max r_d/eps_d, #active, any diverged] of this rank; `allreduce(flags)`
+    reduces it in place with MAX over ranks (None: single rank).  Stops once no
+    instance on any rank is active or after L iterations.  Returns (iterations
+    run, collectives issued)."""
+    if check_every < 1:
+        raise ValueError("check_every must be >= 1")
+    done, ncoll = 0, 0
+    while done < L:
+        done = iterate(check_every)
+        flags = read_flags()
+        if allreduce is not None:
+            allreduce(flags)
+            ncoll += 1
+        if float(flags[2]) == 0.0:
+            break
+    return done, ncoll
+
+
+def nccl_max(flags):
+    """allreduce(MAX) of a flags tensor over the default process group."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX)
+
+
+def solve_collective(solver, engine, out=None, check_every=None, allreduce=nccl_max):
+    """Termination-mode inner solve of this rank's shard through the incremental
+    C ABI (nrto_solve_begin / _iterate / _flags / _end), with the batch-wide
+    allreduce(MAX) of the residual flags between chunks of check_every outer
+    iterations.  Returns (out, iterations run, collectives issued)."""
+    import torch
+    from . import nrto
+    if out is None:
+        out = nrto.alloc_out(solver.shape, solver.batch, solver.E, device="cuda")
+    ce = int(check_every or solver.params.check_every)
+    L = solver.params.max_iter if engine == nrto.NRTO_FULLADMM else solver.params.max_admm_iter
+    flags = torch.zeros(4, dtype=torch.float64, device="cuda")
+
+    def read_flags():
+        nrto.nrto_solve_flags(solver.handle, flags, solver.stream)
+        return flags
+
+    nrto.nrto_solve_begin(solver.handle, engine, solver.stream)
+    done, ncoll = collective_loop(lambda n: nrto.nrto_solve_iterate(solver.handle, n, solver.stream),
+                                  read_flags, allreduce, L, ce)
+    nrto.nrto_solve_end(solver.handle, out, solver.stream)
+    return out, done, ncoll

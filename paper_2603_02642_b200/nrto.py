@@ -263,8 +263,9 @@ def nrto_destroy(handle):
 
 
 # ------------------------------------------------------------------ convenience
-def alloc_out(shape, batch, E, device="cuda", pinned=False, full=True):
-    """Output tensors for nrto_inner_solve (all fields when full=True)."""
+def alloc_out(shape, batch, E, device="cuda", pinned=False, full=True, ragged=True):
+    """Output tensors for nrto_inner_solve (all fields when full=True; the ragged
+    [batch][E] nu / lam_nu only when ragged=True as well)."""
     import torch
     f64, i32 = torch.float64, torch.int32
     kw = dict(device=device)
@@ -280,9 +281,10 @@ def alloc_out(shape, batch, E, device="cuda", pinned=False, full=True):
              r_p=torch.empty(batch, dtype=f64, **kw), r_d=torch.empty(batch, dtype=f64, **kw),
              objective=torch.empty(batch, dtype=f64, **kw))
     if full:
-        o.update(nu=torch.empty(batch, E, dtype=f64, **kw), lam_nu=torch.empty(batch, E, dtype=f64, **kw),
-                 margin_cone=torch.empty(batch, shape.n_g, dtype=f64, **kw),
+        o.update(margin_cone=torch.empty(batch, shape.n_g, dtype=f64, **kw),
                  margin_lin=torch.empty(batch, shape.n_g, dtype=f64, **kw))
+        if ragged:
+            o.update(nu=torch.empty(batch, E, dtype=f64, **kw), lam_nu=torch.empty(batch, E, dtype=f64, **kw))
     return o
 
 
@@ -322,33 +324,6 @@ class InnerSolver:
 
     def case_stats_read(self, L=None):
         return nrto_case_stats_read(self.handle, self.params.max_iter if L is None else L)
-
-    def solve_collective(self, engine=NRTO_FULLADMM, out=None, check_every=None, allreduce=None,
-                         full=True):
-        """Termination-mode solve driven in chunks of `check_every` outer iterations
-        with a batch-wide test between chunks: `allreduce(flags)`
-        reduces the device flags [max r_p/eps_p, max r_d/eps_d, #active, diverged]
-        in place with MAX (e.g. torch.distributed.all_reduce over NCCL); the
-        loop stops once no instance on any rank is active.  Returns (out,
-        number of collectives)."""
-        import torch
-        if out is None:
-            out = alloc_out(self.shape, self.batch, self.E, device="cuda", full=full)
-        ce = int(check_every or self.params.check_every)
-        L = self.params.max_iter if engine == NRTO_FULLADMM else self.params.max_admm_iter
-        flags = torch.zeros(4, dtype=torch.float64, device="cuda")
-        nrto_solve_begin(self.handle, engine, self.stream)
-        done, ncoll = 0, 0
-        while done < L:
-            done = nrto_solve_iterate(self.handle, ce, self.stream)
-            nrto_solve_flags(self.handle, flags, self.stream)
-            if allreduce is not None:
-                allreduce(flags)
-                ncoll += 1
-            if float(flags[2].item()) == 0.0:      # #active (MAX over ranks: anyone active)
-                break
-        nrto_solve_end(self.handle, out, self.stream)
-        return out, ncoll
 
     def gain_update(self, nu, kv_prev, kv_next):
         nrto_gain_update(self.handle, nu, kv_prev, kv_next, self.stream)

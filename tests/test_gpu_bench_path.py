@@ -258,3 +258,99 @@ def test_gain_update_keeps_dr_warm_start():
         s.close()
     for k in ("kv", "du", "p", "p_tilde", "lam_p"):
         assert close(res[1][k], res[0][k], tol=1e-13), k
+
+
+# ------------------------------------------------ incremental ABI, case stats, collective
+@pytest.mark.parametrize("case", ["c1", "c3s", "batch"])
+def test_incremental_solve_matches_inner_solve(case):
+    """nrto_solve_begin/_iterate/_flags/_end (chunks of check_every, the host-side
+    termination test of the multi-rank loop) give the same per-instance
+    iterations, status and iterates as nrto_inner_solve in termination mode."""
+    _require_gpu()
+    from paper_2603_02642_b200.dist import solve_collective
+    if case == "batch":
+        items = [make_franka(5, i, T=12, jitter=True) for i in range(6)]
+        shape, batch = stack_instances(items)
+    else:
+        shape, data = make_instance("c1") if case == "c1" else make_franka(3, 0, T=12)
+        batch = single(shape, data)
+    kw = dict(max_iter=300, eps_p=1e-4, eps_d=1e-4, check_every=3)
+    ref = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, **kw)
+    s = nrto.InnerSolver(shape, nrto.to_tensors(batch, device="cuda"), **kw)
+    out, done, ncoll = solve_collective(s, nrto.NRTO_FULLADMM, allreduce=None)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    s.close()
+    assert ncoll == 0 and done == int(ref["iters"].max()) and done % 3 == 0
+    np.testing.assert_array_equal(g["iters"], ref["iters"])
+    np.testing.assert_array_equal(g["status"], ref["status"])
+    for k in ("kv", "du", "p", "p_tilde", "lam_p", "nu", "lam_nu"):
+        assert close(g[k], ref[k], tol=1e-12), k
+
+
+def test_case_stats_match_oracle():
+    """Per-iteration projection-case histogram (nrto_case_stats_*) equals the
+    oracle's case counts of SM Eq.(18), iteration by iteration."""
+    _require_gpu()
+    for shape, data in (make_instance("c1"), make_franka(3, 0, T=12)):
+        L = 30
+        s = nrto.InnerSolver(shape, nrto.to_tensors(single(shape, data), device="cuda"),
+                             max_iter=L, fixed_iters=1)
+        s.case_stats(True)
+        s.solve(nrto.NRTO_FULLADMM)
+        cnt = s.case_stats_read()
+        s.close()
+        o = oracle_run(shape, data, nrto.NRTO_FULLADMM, max_iter=L, fixed_iters=1)
+        assert np.all(cnt.sum(1) == shape.n_g)
+        np.testing.assert_array_equal(cnt, np.asarray(o["cases"]))
+
+
+def _mp_worker(rank, world, port, out):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_02642_b200 import nrto
+    from paper_2603_02642_b200.dist import solve_collective, instance_range
+    from gen.problems import make_unicycle
+    from gen import stack_instances
+    first, count = instance_range(rank, world, 2)
+    shape, batch = stack_instances([make_unicycle(1, i) for i in range(first, first + count)])
+    s = nrto.InnerSolver(shape, nrto.to_tensors(batch, device="cuda"), max_iter=300, eps_p=1e-5,
+                         eps_d=1e-5, check_every=2)
+
+    def allreduce(f):                 # gloo on one GPU: reduce a host copy of the device flags
+        c = f.cpu()
+        dist.all_reduce(c, op=dist.ReduceOp.MAX)
+        f.copy_(c)
+
+    o, done, ncoll = solve_collective(s, nrto.NRTO_FULLADMM, allreduce=allreduce)
+    torch.cuda.synchronize()
+    out[rank] = (first, o["iters"].cpu().numpy().tolist(), o["kv"].cpu().numpy(), done, ncoll)
+    s.close()
+    dist.destroy_process_group()
+
+
+def test_two_process_collective_loop_on_one_gpu():
+    """Two ranks (processes) on one GPU, instances sharded, the termination test
+    allreduced every check_every iterations: both ranks run until the slowest
+    instance of EITHER shard has converged, and every instance's result equals
+    its single-process solve."""
+    _require_gpu()
+    import socket
+    import torch.multiprocessing as mp
+    s_ = socket.socket(); s_.bind(("127.0.0.1", 0)); port = s_.getsockname()[1]; s_.close()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_mp_worker, args=(2, port, out), nprocs=2, join=True)
+    items = [make_unicycle(1, i) for i in range(4)]
+    shape, batch = stack_instances(items)
+    ref = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, max_iter=300, eps_p=1e-5, eps_d=1e-5, check_every=2)
+    last = int(ref["iters"].max())
+    for r in range(2):
+        first, iters, kv, done, ncoll = out[r]
+        assert done == last and ncoll == last // 2          # global stop, one collective per chunk
+        np.testing.assert_array_equal(iters, ref["iters"][first:first + 2])
+        assert close(kv, ref["kv"][first:first + 2], tol=1e-12)

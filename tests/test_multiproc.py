@@ -74,3 +74,61 @@ def test_ranges():
     assert cover == [(0, 4), (4, 3), (7, 3)]
     with pytest.raises(ValueError):
         instance_range(2, 2, 4)
+
+
+def _loop_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_02642_b200.dist import collective_loop, nccl_max
+    stop_at = [7, 12][rank]          # this rank's last active instance stops here
+    state = {"l": 0}
+
+    def iterate(n):
+        state["l"] = min(40, state["l"] + n)
+        return state["l"]
+
+    def read_flags():
+        active = 1.0 if state["l"] < stop_at else 0.0
+        return torch.tensor([10.0 / (rank + 1), 1.0 * rank, active, 0.0], dtype=torch.float64)
+
+    box = {}
+
+    def allreduce(f):
+        nccl_max(f)
+        box["f"] = f.clone()
+
+    done, ncoll = collective_loop(iterate, read_flags, allreduce, 40, 5)
+    out[rank] = (done, ncoll, box["f"].tolist())
+    dist.destroy_process_group()
+
+
+def test_two_rank_collective_termination_loop():
+    """The in-loop batch-wide termination test: both ranks keep
+    iterating until the LAST active instance on ANY rank has stopped (rank 1
+    at 12 -> both stop after the chunk ending at 15), with one allreduce(MAX)
+    of the flags per chunk of check_every = 5 iterations."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_loop_worker, args=(world, port, out), nprocs=world, join=True)
+    for r in range(world):
+        done, ncoll, f = out[r]
+        assert done == 15 and ncoll == 3
+        assert f == [10.0, 1.0, 0.0, 0.0]       # MAX over ranks of the last flags
+
+
+def test_collective_loop_single_rank():
+    from paper_2603_02642_b200.dist import collective_loop
+    st = {"l": 0}
+
+    def it(n):
+        st["l"] = min(23, st["l"] + n)
+        return st["l"]
+    done, ncoll = collective_loop(it, lambda: [0.0, 0.0, 1.0, 0.0], None, 23, 4)
+    assert done == 23 and ncoll == 0
+    with pytest.raises(ValueError):
+        collective_loop(it, lambda: [0, 0, 0, 0], None, 5, 0)
