@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-conv", action="store_true")
     ap.add_argument("--no-dr", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
     return ap.parse_args()
 
 
@@ -467,6 +468,38 @@ def run_ours(args, rank, world, local_rank):
                                  "ms_per_solve": sms}
             s3.close()
 
+    # c4 constraint / horizon scaling points (BASELINE configs[3]; one quadcopter instance
+    # each, both engines, fixed iterations) with their SURVEY §8(d) bytes and fraction
+    c4 = None
+    if not args.no_c4 and rank == 0:
+        from gen.problems import make_quad, stack_instances, CONFIGS
+        peak_c4, _ = load_peaks()
+        c4 = []
+        for T4, nobs in ((50, 10), (200, 50), (800, 200)):
+            shp4, d4 = make_quad(CONFIGS["c4"], 0, T=T4, n_obs=nobs)
+            E4, E4s, E4B, _ = shape_stats(shp4)
+            dd4 = nrto.to_tensors(stack_instances([(shp4, d4)])[1], device=dev)
+            bytes_it = 8 * (2 * E4 + E4s + E4B)
+            row = {"T": T4, "n_obs": nobs, "n_g": int(shp4.n_g), "E": int(E4),
+                   "alg_bytes_per_iteration": bytes_it}
+            for eng, kw4, name in ((nrto.NRTO_FULLADMM, dict(max_iter=10), "fulladmm"),
+                                   (nrto.NRTO_DR, dict(max_admm_iter=2, max_dr_iter=10), "dr")):
+                s4 = nrto.InnerSolver(shp4, dd4, fixed_iters=1, **kw4)
+                o4 = nrto.alloc_out(shp4, 1, s4.E, device=dev, full=False)
+                s4.solve(eng, out=o4)
+                torch.cuda.synchronize()
+                a4, b4 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a4.record(stream); s4.solve(eng, out=o4); b4.record(stream)
+                torch.cuda.synchronize()
+                ms4 = a4.elapsed_time(b4)
+                its = kw4.get("max_iter", 0) or kw4["max_admm_iter"] * kw4["max_dr_iter"]
+                gbs = bytes_it * its / (ms4 / 1e3) / 1e9
+                row[name] = {"us_per_iteration": 1000 * ms4 / its, "achieved_gbs_8d": gbs,
+                             "frac_8d": gbs / peak_c4, "iterations": its}
+                s4.close()
+            del dd4
+            c4.append(row)
+
     # case mix over all ranks (SURVEY §8d representativeness rule: case 3 >= 5 % after l = 5)
     ct = torch.as_tensor(case_tot, dtype=torch.float64, device=dev)
     if world > 1:
@@ -551,6 +584,7 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "dr_engine": dr,
         "single_instance": singles,
+        "c4_sweep": c4,
         "residuals": {"max_r_p_at_L": max_rp, "unconverged_at_L": n_unconv,
                       "any_diverged": any_div},
     }

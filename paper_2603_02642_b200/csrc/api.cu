@@ -155,6 +155,11 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
       if (s->cone_kind[j] == 1 && s->cone_knot[j] == k) crow.push_back(j);
   }
   cptr[T] = (int32_t)crow.size();
+  std::vector<int32_t> qrow;   // QP row order (qp.cu, pipelined rows phase)
+  for (int p = 1; p <= T; ++p) {
+    for (int q = sptr[p]; q < sptr[p + 1]; ++q) qrow.push_back(srow[q]);
+    for (int q = cptr[p - 1]; q < cptr[p]; ++q) qrow.push_back(crow[q]);
+  }
   std::vector<int32_t> knot(s->cone_knot, s->cone_knot + ng), kind(ng);
   for (int j = 0; j < ng; ++j) kind[j] = s->cone_kind[j];
   // ---- tiles of <= 8 cones with equal (kind, knot) for the fused pass, and
@@ -229,6 +234,9 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   AL(dknot, ng); AL(dkind, ng); AL(doff, ng + 1); AL(doffB, ng + 1);
   AL(dkptr, T + 1); AL(dkcone, kcone.size()); AL(dsptr, T + 2); AL(dsrow, srow.size());
   AL(dcptr, T + 1); AL(dcrow, crow.size());
+  int32_t* dqrow;
+  AL(dqrow, ng);
+  v.qrow = dqrow;
   v.knot = dknot; v.kind = dkind; v.off = doff; v.offB = doffB; v.kptr = dkptr; v.kcone = dkcone;
   v.sptr = dsptr; v.srow = dsrow; v.cptr = dcptr; v.crow = dcrow;
   double *A, *Bm, *grad, *g0, *Psi, *tau, *W, *Ru, *uhat, *rtrust;
@@ -277,6 +285,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   hup(dkptr, kptr.data(), (T + 1) * 4); hup(dkcone, kcone.data(), kcone.size() * 4);
   hup(dsptr, sptr.data(), (T + 2) * 4); hup(dsrow, srow.data(), srow.size() * 4);
   hup(dcptr, cptr.data(), (T + 1) * 4); hup(dcrow, crow.data(), crow.size() * 4);
+  hup(dqrow, qrow.data(), qrow.size() * 4);
   hup(dtiles, tiles.data(), tiles.size() * 4); hup(dwitems, witems.data(), witems.size() * 4);
   if (v.fused == 2) {
     hup(v.ttb, ttb.data(), ttb.size() * 4);

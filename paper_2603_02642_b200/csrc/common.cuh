@@ -43,6 +43,7 @@ struct Dev {
   const int32_t* kptr; const int32_t* kcone;   // cones with a b-block at step k (k < T)
   const int32_t* sptr; const int32_t* srow;    // state rows at knot k (k = 0..T)
   const int32_t* cptr; const int32_t* crow;    // control rows at step k (k < T)
+  const int32_t* qrow;   // [ng] rows in knot order: for p = 1..T state rows at knot p, then control rows at step p-1 (QP)
   // primitives (device copies)
   const double *A, *Bm, *grad, *g0, *Psi, *tau, *W, *Ru, *uhat, *rtrust;
   // setup products

@@ -434,16 +434,29 @@ __device__ __forceinline__ void cpa8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src) : "memory");
 }
+__device__ __forceinline__ void cpa16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src) : "memory");
+}
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr int kQPRing = QP_RING;   // power of two (common.cuh)
 #ifndef QP_MINB
-#define QP_MINB 5
+#define QP_MINB 4
 #endif
 #ifndef QP_THREADS
 #define QP_THREADS 256
+#endif
+#ifndef QP_CHUNK            // recurrence steps per bulk copy (divides QP_RING)
+#define QP_CHUNK 1
+#endif
+#ifndef QP_RFENCE           // membar.cta before each recurrence-step publication
+#define QP_RFENCE 1
+#endif
+#ifndef QP_EAHEAD           // e_k prefetch distance of the forward sweep
+#define QP_EAHEAD 4
 #endif
 
 // ---------------------------------------------------------------------------
@@ -534,6 +547,98 @@ __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int ti
           if (nz > 1) atomicAdd(dst + rec_idx(rc[u], 1), w * g01[u].y);
           for (int q = 2; q < nz; ++q)
             atomicAdd(dst + rec_idx(rc[u], q), w * gval[(int64_t)j * kRowNZ + q]);
+        } else {
+          const int n = (kind == 0) ? nx : nu;
+          for (int i = 0; i < n; ++i) atomicAdd(dst + i, w * gj[i]);
+        }
+      }
+    }
+  }
+}
+
+// Spin until a shared-memory epoch flag reaches `ep` (producer: data, membar.cta,
+// flag), then order the following reads after it.
+__device__ __forceinline__ void qp_spin(volatile int16_t* f, int16_t ep) {
+  while (*f < ep) __nanosleep(20);
+  __threadfence_block();
+}
+
+// Rows of one QP iteration in knot order (v.qrow: for p = 1..T the state rows at
+// knot p, then the control rows at step p-1), each processed once dx_k (fx[k],
+// state rows) / du~_k (fu[k], control rows) is published; same arithmetic as
+// qp_rows<false>.
+template <int U>
+__device__ __forceinline__ void qp_rows_pipe(const Dev& v, int64_t bg, int ng, int tid, int nt,
+                                             const double* __restrict__ grad,
+                                             const double* __restrict__ g0, double* p, double* zl,
+                                             double* yl, double* vv, const double* sX,
+                                             const double* gR, double* gS, double* gU, bool more,
+                                             volatile int16_t* fx, volatile int16_t* fu, int16_t ep,
+                                             double rho, double rq,
+                                             double sq, double aq, double den, double beta) {
+  const int nx = v.d.nx, nu = v.d.nu;
+  const int4* __restrict__ rows = v.rowpk + bg;
+  const double* __restrict__ gval = v.gval + bg * kRowNZ;
+  for (int q0 = tid; q0 < ng; q0 += U * nt) {
+    int4 rc[U];
+    double2 g01[U];
+    int jj[U];
+    double vj[U], pj[U], zlj[U], ylj[U], g0j[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * nt;
+      if (q < ng) {
+        const int j = v.qrow[q];
+        jj[u] = j;
+        rc[u] = rows[j];
+        g01[u] = *reinterpret_cast<const double2*>(gval + (int64_t)j * kRowNZ);
+        pj[u] = p[j]; zlj[u] = zl[j]; ylj[u] = yl[j]; vj[u] = vv[j]; g0j[u] = g0[j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * nt;
+      if (q >= ng) continue;
+      const int j = jj[u];
+      const int k = rc[u].x, kind = rc[u].y & 0xff, nz = (rc[u].y >> 8) & 0xff;
+      qp_spin(kind == 0 ? &fx[k] : &fu[k], ep);
+      const double* gj = grad + (int64_t)j * nx;
+      double bd = 0.0;
+      if (kind == 0) {
+        const double* x = sX + (int64_t)k * nx;
+        if (nz <= kRowNZ) {
+          if (nz > 0) bd += g01[u].x * x[rec_idx(rc[u], 0)];
+          if (nz > 1) bd += g01[u].y * x[rec_idx(rc[u], 1)];
+          for (int s = 2; s < nz; ++s) bd += gval[(int64_t)j * kRowNZ + s] * x[rec_idx(rc[u], s)];
+        } else {
+          for (int i = 0; i < nx; ++i) bd += gj[i] * x[i];
+        }
+      } else {
+        const double* x = gR + (int64_t)k * nu;
+        if (nz <= kRowNZ) {
+          if (nz > 0) bd += g01[u].x * __ldcg(x + rec_idx(rc[u], 0));
+          if (nz > 1) bd += g01[u].y * __ldcg(x + rec_idx(rc[u], 1));
+          for (int s = 2; s < nz; ++s) bd += gval[(int64_t)j * kRowNZ + s] * __ldcg(x + rec_idx(rc[u], s));
+        } else {
+          for (int i = 0; i < nu; ++i) bd += gj[i] * __ldcg(x + i);
+        }
+      }
+      const double r0 = sq * pj[u] + rho * vj[u] + rq * zlj[u] - ylj[u];
+      const double ptl = (r0 - rq * bd) / den;
+      const double pn = aq * ptl + (1.0 - aq) * pj[u];
+      const double zh = aq * (bd + ptl) + (1.0 - aq) * zlj[u];
+      const double zn = nan_min(zh + ylj[u] / rq, -g0j[u]);
+      const double yn = ylj[u] + rq * (zh - zn);
+      p[j] = pn; zl[j] = zn; yl[j] = yn;
+      if (more) {
+        const double r = sq * pn + rho * vj[u] + rq * zn - yn;
+        const double w = rq * zn - yn - beta * r;
+        double* dst = (kind == 0) ? gS + (int64_t)k * nx : gU + (int64_t)k * nu;
+        if (nz <= kRowNZ) {
+          if (nz > 0) atomicAdd(dst + rec_idx(rc[u], 0), w * g01[u].x);
+          if (nz > 1) atomicAdd(dst + rec_idx(rc[u], 1), w * g01[u].y);
+          for (int s = 2; s < nz; ++s)
+            atomicAdd(dst + rec_idx(rc[u], s), w * gval[(int64_t)j * kRowNZ + s]);
         } else {
           const int n = (kind == 0) ? nx : nu;
           for (int i = 0; i < n; ++i) atomicAdd(dst + i, w * gj[i]);
@@ -636,6 +741,8 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
   double* sS = sm;                                    // [(T+1) nx]
   double* ring = sS + (T + 1) * nx;                   // [kQPRing][nx nx]
   uint64_t* qbar = reinterpret_cast<uint64_t*>(ring + kQPRing * nx * nx);   // [kQPRing]
+  double* eb = reinterpret_cast<double*>(qbar + kQPRing);                      // [QP_EAHEAD+1][16] e_k
+  int16_t* flg = reinterpret_cast<int16_t*>(eb + 16 * (QP_EAHEAD + 1));        // [5][T+1] (pipelined)
   const int nn = nx * nx;
   const int nits = v.prm.qp_iters;
   int it_dbg = 0;
@@ -647,6 +754,8 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
   }
   for (int r = tid; r < (T + 1) * nx; r += nt) gS[r] = 0.0;
   for (int r = tid; r < T * nu; r += nt) gU[r] = 0.0;
+  if (NXM > 0)
+    for (int r = tid; r < 5 * (T + 1); r += nt) flg[r] = 0;
   __syncthreads();
   QP_CLK(0);
   if (nits > 0) {                                     // rhs / w / scatter of iteration 0
@@ -655,6 +764,245 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
     __syncthreads();
     QP_CLK(1);
   }
+  if constexpr (NXM > 0) {
+    // ---- pipelined QP iteration (warp-specialised): warp 0 runs the two
+    // Riccati recurrences; warps 1.. run every k-parallel phase BEHIND it, per knot,
+    // synchronised by per-knot epoch flags in shared memory (membar.cta + volatile):
+    //   fa[k]: a_k, r_u,k ready      (helpers -> warp 0, backward sweep)
+    //   fs[k]: s_k ready             (warp 0 -> helpers: kff_k, e_k)
+    //   fe[k]: kff_k, e_k ready      (helpers -> warp 0, forward sweep)
+    //   fx[p]: dx_p, du~_{p-1} ready (warp 0 -> helpers: rows in knot order)
+    // so only one block barrier per QP iteration remains (before the ball).
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nhw = (nt >> 5) - 1;
+    volatile int16_t* fa = flg;
+    volatile int16_t* fs = fa + (T + 1);
+    volatile int16_t* fe = fs + (T + 1);
+    volatile int16_t* fx = fe + (T + 1);
+    volatile int16_t* fu = fx + (T + 1);
+    double* gE = v.dxt + (int64_t)b * (T + 1) * nx;    // e_k = B_k kff_k
+    for (int it = 0; it < nits; ++it) {
+      it_dbg = it;
+      const int16_t ep = (int16_t)(it + 1);
+      if (warp == 0) {
+        // The two recurrences read Acl_k^T (backward) and Acl_k (forward) as ONE stream of
+        // chunks of QP_CHUNK consecutive steps (one bulk copy each, kQPRing / QP_CHUNK
+        // slots), continued across the QP iterations of the launch, so the forward
+        // sweep's first chunks arrive during the backward tail.
+        constexpr int C = QP_CHUNK;
+        constexpr int S = kQPRing / C;
+        const int NC = (T + C - 1) / C;
+        const int ptot = nits * 2 * NC;
+        const double* AT = F.AclT + (int64_t)b * T * nn;
+        const double* AG = F.Acl + (int64_t)b * T * nn;
+        auto chunk = [&](int p, int& lo, int& hi) {
+          const int g = p % (2 * NC);
+          if (g < NC) { hi = T - 1 - g * C; lo = max(0, hi - C + 1); return true; }
+          lo = (g - NC) * C; hi = min(T, lo + C) - 1; return false;
+        };
+        auto issue = [&](int p) {
+          if (lane != 0 || p >= ptot) return;
+          int lo, hi;
+          const bool bw = chunk(p, lo, hi);
+          const int sl = p % S;
+          const uint32_t bytes = (uint32_t)((hi - lo + 1) * nn * 8);
+          qp_expect_tx(&qbar[sl], bytes);
+          qp_bulk(ring + sl * C * nn, (bw ? AT : AG) + (int64_t)lo * nn, bytes, &qbar[sl]);
+        };
+        if (it == 0)
+          for (int p = 0; p < S; ++p) issue(p);
+        const int pb = it * 2 * NC;
+        // backward recurrence s_k = a_k + Acl_k^T s_{k+1}
+        const int ic = lane < nx ? lane : 0;
+        qp_spin(&fa[T], ep);
+        const double* base = ring;
+        int lo = 0, hi = -1;
+        for (int k = T - 1; k >= 0; --k) {
+          const int c = (T - 1 - k) / C, p = pb + c;
+          if (k > hi || k < lo) {
+            chunk(p, lo, hi);
+            qp_wait(&qbar[p % S], (uint32_t)(p / S) & 1u);
+            base = ring + (p % S) * C * nn;
+          }
+          qp_spin(&fa[k], ep);
+          const double* Ar = base + (k - lo) * nn + ic * nx;
+          const double* sn = sS + (k + 1) * nx;
+          double c0 = sS[k * nx + ic], c1 = 0.0;
+#pragma unroll
+          for (int r = 0; r < NXM; r += 2)
+            if (r < nx) {
+              const double2 a = *reinterpret_cast<const double2*>(Ar + r);
+              const double2 x2 = *reinterpret_cast<const double2*>(sn + r);
+              c0 = fma(a.x, x2.x, c0);
+              c1 = fma(a.y, x2.y, c1);
+            }
+          __syncwarp();
+          if (lane < nx) sS[k * nx + lane] = c0 + c1;
+#if QP_RFENCE
+          __threadfence_block();
+#endif
+          __syncwarp();
+          if (lane == 0) fs[k] = ep;
+          if (k == lo) issue(p + S);
+        }
+        QP_CLK(4);
+        // forward recurrence dx_{k+1} = Acl_k dx_k + e_k.  e_k reaches shared memory by
+        // cp.async QP_EAHEAD steps ahead (an outstanding plain global load would be
+        // waited for by a membar.cta)
+        constexpr int DE = QP_EAHEAD;
+        auto fetch_e = [&](int k) {
+          if (k < T) {
+            qp_spin(&fe[k], ep);
+            if (2 * lane < nx) cpa16(eb + (k % (DE + 1)) * 16 + 2 * lane, gE + k * nx + 2 * lane);
+          }
+          cpa_commit();
+        };
+        for (int k = 0; k < DE; ++k) fetch_e(k);
+        lo = 0; hi = -1;
+        for (int k = 0; k < T; ++k) {
+          const int c = k / C, p = pb + NC + c;
+          fetch_e(k + DE);
+          cpa_wait<DE>();
+          if (k == 0 && lane < nx) sS[lane] = 0.0;       // dx_0 = 0 (s_0 is not read by anyone)
+          __syncwarp();
+          if (k > hi || k < lo) {
+            chunk(p, lo, hi);
+            qp_wait(&qbar[p % S], (uint32_t)(p / S) & 1u);
+            base = ring + (p % S) * C * nn;
+          }
+          const double* Ar = base + (k - lo) * nn + ic * nx;
+          const double* xk = sS + k * nx;
+          double c0 = eb[(k % (DE + 1)) * 16 + ic], c1 = 0.0;
+#pragma unroll
+          for (int r = 0; r < NXM; r += 2)
+            if (r < nx) {
+              const double2 a = *reinterpret_cast<const double2*>(Ar + r);
+              const double2 x2 = *reinterpret_cast<const double2*>(xk + r);
+              c0 = fma(a.x, x2.x, c0);
+              c1 = fma(a.y, x2.y, c1);
+            }
+          __syncwarp();
+          if (lane < nx) sS[(k + 1) * nx + lane] = c0 + c1;
+#if QP_RFENCE
+          __threadfence_block();
+#endif
+          __syncwarp();
+          if (lane == 0) fx[k + 1] = ep;
+          if (k == hi) issue(p + S);
+        }
+        cpa_wait<0>();
+        QP_CLK(7);
+      } else {
+        // helpers, knot k by warp (k mod nhw): a_k, r_u,k (descending, ahead of warp 0)
+        for (int k = T - (warp - 1); k >= 0; k -= nhw) {
+          double ru = 0.0;                               // r_u,k (recomputed by the kff helper)
+          if (k < T && lane < nu) {
+            const int r = k * nu + lane;
+            ru = sq * du[r] + __ldcg(gU + r) + cu2[r];   // cu2 = -2 R_u u_hat (setup)
+          }
+          double acc = 0.0;
+          if (lane < nx && k > 0) {
+            const int r = k * nx + lane;
+            acc = __ldcg(gS + r) + rq * zb[r] - yb[r];
+          }
+          if (k < T) {
+            const double* Kk = Kf + (int64_t)k * nu * nx + (lane < nx ? lane : 0);
+#pragma unroll
+            for (int m = 0; m < (NUM > 0 ? NUM : 8); ++m) {
+              const double rm = __shfl_sync(0xffffffffu, ru, m);
+              if (m < nu && lane < nx) acc -= Kk[m * nx] * rm;
+            }
+          }
+          if (lane < nx) sS[k * nx + lane] = acc;       // a_k (k < T), s_T
+          __threadfence_block();
+          __syncwarp();
+          if (lane == 0) fa[k] = ep;
+        }
+        // kff_k = H^-1 r_u,k + H^-1 B_k^T s_{k+1}, e_k = B_k kff_k (descending, behind warp 0)
+        for (int k = T - 1 - (warp - 1); k >= 0; k -= nhw) {
+          qp_spin(k + 1 == T ? &fa[T] : &fs[k + 1], ep);
+          qp_spin(&fa[k], ep);
+          double ru = 0.0;
+          if (lane < nu) {
+            const int r = k * nu + lane;
+            ru = sq * du[r] + __ldcg(gU + r) + cu2[r];
+          }
+          double kf = 0.0;
+          const double* H = Hi + (int64_t)k * nu * nu + (lane < nu ? lane : 0) * nu;
+#pragma unroll
+          for (int q = 0; q < (NUM > 0 ? NUM : 8); ++q) {
+            const double rq_ = __shfl_sync(0xffffffffu, ru, q);
+            if (q < nu && lane < nu) kf = fma(H[q], rq_, kf);
+          }
+          if (lane < nu) {
+            const double* hb = HB + (int64_t)k * nu * nx + lane * nx;
+            const double* sk = sS + (k + 1) * nx;
+            kf = dotn<NXM>(nx, [&](int q) { return hb[q]; }, [&](int q) { return sk[q]; }, kf);
+            gK[k * nu + lane] = kf;
+            gU[k * nu + lane] = 0.0;                     // scatter target of the next iteration
+          }
+          if (lane < nx) {
+            gS[k * nx + lane] = 0.0;
+            if (k == T - 1) gS[T * nx + lane] = 0.0;
+          }
+          double e = 0.0;
+          const double* Bk = Bm + (int64_t)k * nx * nu + (lane < nx ? lane : 0) * nu;
+#pragma unroll
+          for (int m = 0; m < (NUM > 0 ? NUM : 8); ++m) {
+            const double km = __shfl_sync(0xffffffffu, kf, m);
+            if (m < nu && lane < nx) e = fma(Bk[m], km, e);
+          }
+          if (lane < nx) gE[k * nx + lane] = e;
+          __threadfence_block();
+          __syncwarp();
+          if (lane == 0) fe[k] = ep;
+        }
+        if (warp == 1) {
+          // du~_k = kff_k - Kf_k dx_k and du_k (relaxed), 4 knots per publication (fu)
+          const int c = lane / nu, m = lane - c * nu;
+          for (int k0 = 0; k0 < T; k0 += 4) {
+            const int k = k0 + c;
+            qp_spin(&fx[min(k0 + 3, T - 1)], ep);
+            if (c < 4 && k < T) {
+              const double* Kk = Kf + (int64_t)k * nu * nx + m * nx;
+              const double* xk = sS + k * nx;
+              const double dd = __ldcg(gK + k * nu + m) -
+                                dotn<NXM>(nx, [&](int q) { return Kk[q]; }, [&](int q) { return xk[q]; }, 0.0);
+              gR[k * nu + m] = dd;
+              du[k * nu + m] = aq * dd + (1.0 - aq) * du[k * nu + m];
+            }
+            __threadfence_block();
+            __syncwarp();
+            if (lane < 4 && k0 + lane < T) fu[k0 + lane] = ep;
+          }
+        } else {
+          // rows in knot order, each as soon as dx_k (fx) / du~_k (fu) is published
+          const bool more = it + 1 < nits;
+          qp_rows_pipe<kRowBatch>(v, bg, ng, tid - 64, nt - 64, grad, g0, p, zl, yl, rp, sS, gR, gS, gU,
+                                  more, fx, fu, ep, rho, rq, sq, aq, den, beta);
+        }
+      }
+      __syncthreads();
+      QP_CLK(9);
+      double nb = 0.0;                                  // trust-region ball
+      for (int r = tid; r < (T + 1) * nx; r += nt) {
+        const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
+        sS[r] = zh;
+        const double w = zh + yb[r] / rq;
+        nb += w * w;
+      }
+      nb = sqrt(block_sum(nb, red));
+      const double scl = (nb > rtr) ? rtr / nb : 1.0;
+      for (int r = tid; r < (T + 1) * nx; r += nt) {
+        const double zh = sS[r];
+        const double zn = scl * (zh + yb[r] / rq);
+        yb[r] += rq * (zh - zn);
+        zb[r] = zn;
+      }
+      __syncthreads();
+      QP_CLK(10);
+    }
+  } else {
   for (int it = 0; it < nits; ++it) {
     it_dbg = it;
     for (int r = tid; r < T * nu; r += nt) {          // r_u (consumes and clears U)
@@ -857,6 +1205,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
     __syncthreads();
     QP_CLK(10);
   }
+  }
   double ap = 0.0, ad = 0.0;
   double* tin = v.tin + bg;
   double* ptp = v.ptprev + bg;
@@ -963,8 +1312,9 @@ cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
 
 cudaError_t launch_qp_sparse(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid) {
   const Dims& d = h->dev.d;
-  const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx + kQPRing) * sizeof(double);
-  if (smem > 48 * 1024) return launch_qp(h, engine, l, st);
+  const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx + kQPRing) * sizeof(double) +
+                      16 * (QP_EAHEAD + 1) * sizeof(double) + (size_t)5 * (d.T + 1) * sizeof(int16_t);
+  if (smem > 48 * 1024 || h->dev.prm.qp_iters > 32000) return launch_qp(h, engine, l, st);
   if (d.nx <= 127) {
     const int g = (grid > 0 && grid < d.B) ? grid : d.B;
     if (d.nx == 14 && d.nu == 7) k_qp_sparse<14, 7><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
