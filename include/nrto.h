@@ -37,14 +37,32 @@
  *     its n_z = (T+1) n_x vector ((k_j+1) n_x doubles; blocks k > k_j are
  *     identically zero); control cone j stores block k (n_x
  *     doubles).  nrto_layout returns the offsets; E = total length.
- *   - Every call is asynchronous on the stream it is given (a cudaStream_t
- *     passed as void*, NULL = legacy default stream) unless a HOST memory
- *     flag forces staging copies; results are valid after the stream syncs.
- *     Internally nrto_inner_solve may run work on handle-owned streams (the
- *     overlapped QP, the control-cone kernel) and, for fixed-iteration solves
- *     without profiling, replay a CUDA graph of the whole iteration loop that
- *     it captured on an earlier call with the same device state; all of it is
- *     joined back to `stream` by events before the call's outputs are written.
+ *   - Calls are enqueued on the stream they are given (a cudaStream_t passed
+ *     as void*, NULL = legacy default stream); results are valid after the
+ *     stream syncs.  Internally nrto_inner_solve may run work on handle-owned
+ *     streams (the overlapped QP, the control-cone kernel) and, for
+ *     fixed-iteration solves without profiling, replay a CUDA graph of the
+ *     whole iteration loop that it captured on an earlier call with the same
+ *     device state; all of it is joined back to `stream` by events before the
+ *     call's outputs are written.
+ *   - Calls that BLOCK THE HOST (synchronise):
+ *       nrto_setup        shape upload (synchronous cudaMemcpy) and the SPD
+ *                         check of the setup factors (stream sync);
+ *       nrto_refresh      the SPD check (stream sync after the setup kernels);
+ *       nrto_inner_solve  with termination on (fixed_iters == 0): one device
+ *                         -> host read of the active-instance count every
+ *                         check_every outer iterations; the first DR solve
+ *                         after a setup/refresh (SPD check of the DR factors);
+ *                         any call with memory == NRTO_MEM_HOST (stream sync
+ *                         after the output copies);
+ *       nrto_solve_begin  the first DR use after a setup/refresh (as above);
+ *       nrto_profile_read, nrto_pass_bytes, nrto_case_stats_read, nrto_destroy.
+ *     Everything else (fixed-iteration solves with device outputs,
+ *     nrto_gain_update, nrto_soc_project, nrto_solve_iterate / _flags / _end
+ *     with device outputs) is asynchronous.
+ *   - Device memory is allocated with cudaMalloc at setup (handle-owned; the
+ *     first solve also allocates small staging / trace buffers) -- no
+ *     allocation happens inside the iteration loop.
  *
  * Errors: functions return nrto_err; no C++ exception crosses the ABI.  On a
  * non-OK return nrto_last_error() gives a thread-local message.  Per-instance
@@ -221,6 +239,30 @@ nrto_err nrto_profile_read(nrto_handle h, int32_t kclass, double* total_ms, int6
  * cones with s^{l-1} != 1 and y^l written where it is needed later (DESIGN §7,
  * lazy y).  0 when the TMA pass is not in use.  Synchronises the device. */
 nrto_err nrto_pass_bytes(nrto_handle h, int64_t* bytes);
+
+/* General uncertainty set: zeta = Gamma z with
+ * z^T S z <= tau, Gamma in R^{(T+1) n_x x n_z}, S dense SPD, so A_hat_j =
+ * sqrt(tau) Psi Gamma^T [A_bar_j; 0] and b_hat_j = sqrt(tau) Psi Gamma^T F_zeta^T
+ * grad g_j couple all time blocks.  memory: as nrto_data.
+ *   Gamma [b][(T+1) n_x][n_z] row-major;  Psi [b][n_z][n_z] with Psi^T Psi = S^-1. */
+typedef struct {
+  int32_t memory;
+  int32_t n_z;
+  const double* Gamma;
+  const double* Psi;
+} nrto_uncertainty;
+
+/* Setup for a general set: as nrto_setup (data->Psi is ignored; data->tau is
+ * used), plus the dense gain system M^-1 = Q_v + rho sum_j A_hat_j^T A_hat_j
+ * formed on the device and factored by Cholesky once (T n_u n_x <=
+ * 4096).  The handle supports nrto_inner_solve with NRTO_FULLADMM only (in-order
+ * schedule); its nu / lam_nu outputs are DENSE [b][n_g][n_z] rows.
+ * nrto_refresh / nrto_gain_update return NRTO_EINVAL on it; the DR engine too.
+ * Errors as nrto_setup; NRTO_ENOTSPD if a Cholesky pivot of M^-1 is <= 0.
+ * Synchronises the host. */
+nrto_err nrto_setup_general(const nrto_shape* shape, const nrto_data* data,
+                            const nrto_uncertainty* unc, const nrto_params* params,
+                            void* stream, nrto_handle* out);
 
 /* Incremental driving of the inner solve, for callers that interleave their
  * own work between outer iterations -- e.g. the batch-wide allreduce(MAX) of

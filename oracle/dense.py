@@ -19,19 +19,29 @@ from .soc import proj_soc
 
 # --------------------------------------------------------------- problem data
 class DenseProblem:
-    """All constants of one SL iteration, formed literally."""
+    """All constants of one SL iteration, formed literally.
 
-    def __init__(self, shape, data, S=None):
+    General uncertainty set: zeta = Gamma z, z^T S z <= tau with
+    Gamma in R^{(T+1)n_x x n_z} (default I) and S in S^{n_z}_{++} (default the
+    block-diagonal S of the generator's Psi_k blocks); Psi^T Psi = S^{-1} and
+    A_hat_j = sqrt(tau) Psi Gamma^T [A_bar_j; 0], b_hat_j = sqrt(tau) Psi
+    Gamma^T F_zeta^T grad g_j.
+    """
+
+    def __init__(self, shape, data, S=None, Gamma=None):
         nx, nu, T = shape.n_x, shape.n_u, shape.T
         ng = shape.n_g
         self.nx, self.nu, self.T, self.ng = nx, nu, T, ng
         self.knot = np.asarray(shape.cone_knot)
         self.kind = np.asarray(shape.cone_kind)
         A, B = np.asarray(data["A"]), np.asarray(data["B"])
-        NX = (T + 1) * nx            # dim of stacked x and of zeta (Gamma = I, n_z = NX)
+        NX = (T + 1) * nx            # dim of stacked x and of zeta
         NU = T * nu
         NK = T * nu * nx             # dim k_v
-        self.NX, self.NU, self.NK, self.nz = NX, NU, NK, NX
+        G = np.eye(NX) if Gamma is None else np.asarray(Gamma, float)
+        nz = G.shape[1]
+        self.Gamma = G
+        self.NX, self.NU, self.NK, self.nz = NX, NU, NK, nz
 
         # F_u, F_zeta: delta_x = F_u delta_u + F_zeta zeta for the linearised
         # dynamics dx_{k+1} = A_k dx_k + B_k du_k + d_k, dx_0 = d_bar_0
@@ -56,6 +66,8 @@ class DenseProblem:
         # S and Psi with Psi^T Psi = S^{-1}; default S = blkdiag(S_k)
         # with S_k^{-1} = Psi_k^T Psi_k from the generator's blocks.
         if S is None:
+            if Gamma is not None:
+                raise ValueError("a general Gamma needs its S")
             S = np.zeros((NX, NX))
             for k in range(T + 1):
                 Pk = np.asarray(data["Psi"][k])
@@ -71,15 +83,16 @@ class DenseProblem:
         self.g0 = np.asarray(data["g0"], float)
         grad = np.asarray(data["grad"], float)
         self.b = np.zeros((ng, NU))
-        self.Ahat = np.zeros((ng, NX, NK))
-        self.bhat = np.zeros((ng, NX))
+        self.Ahat = np.zeros((ng, nz, NK))
+        self.bhat = np.zeros((ng, nz))
+        PG = self.Psi @ G.T                                           # Psi Gamma^T
         for j in range(ng):
             k_j = int(self.knot[j])
             if self.kind[j] == 0:
                 gfull = np.zeros(NX)
                 gfull[k_j * nx:(k_j + 1) * nx] = grad[j]
                 self.b[j] = self.F_u.T @ gfull                        # b_j = F_u^T grad g_j
-                self.bhat[j] = st * self.Psi @ self.F_z.T @ gfull      # b_hat_j
+                self.bhat[j] = st * PG @ self.F_z.T @ gfull            # b_hat_j
             else:
                 self.b[j, k_j * nu:(k_j + 1) * nu] = grad[j, :nu]      # dh_j/du
             Abar = np.zeros((T * nx, NK))
@@ -87,7 +100,7 @@ class DenseProblem:
                 bjk = self.b[j, k * nu:(k + 1) * nu]
                 Abar[k * nx:(k + 1) * nx, k * nu * nx:(k + 1) * nu * nx] = \
                     np.kron(np.eye(nx), bjk[None, :])                  # I (x) b_{j,k}^T
-            self.Ahat[j] = st * self.Psi @ np.vstack([Abar, np.zeros((nx, NK))])
+            self.Ahat[j] = st * PG @ np.vstack([Abar, np.zeros((nx, NK))])
 
         # cost blocks
         W = np.asarray(data["W_K"], float)
@@ -192,12 +205,12 @@ def fulladmm(pb: DenseProblem, prm, trace=None):
     M, q, calM, calMbar from P:1165-1182 are formed as dense matrices.
     """
     rho = prm["rho"]
-    ng, NK, NX = pb.ng, pb.NK, pb.NX
+    ng, NK, NZ = pb.ng, pb.NK, pb.nz
     M, q, calM, calMbar = gain_operators(pb.Qv, pb.Ahat, pb.bhat, rho)
 
-    kv = np.zeros(NK); lam_nu = np.zeros((ng, NX)); lam_p = np.zeros(ng)
+    kv = np.zeros(NK); lam_nu = np.zeros((ng, NZ)); lam_p = np.zeros(ng)
     p = np.zeros(ng); pt_prev = np.zeros(ng)          # Algorithm 1 line 2 (R10)
-    nu = np.zeros((ng, NX)); pt = np.zeros(ng); du = np.zeros(pb.NU)
+    nu = np.zeros((ng, NZ)); pt = np.zeros(ng); du = np.zeros(pb.NU)
     qp = DenseQP(pb, rho, prm["rho_qp"], prm["sigma_qp"], prm["alpha_qp"])
     status, it = 1, 0
     r_p = r_d = np.inf
@@ -238,7 +251,7 @@ class DenseDR:
 
     def __init__(self, pb: DenseProblem, rho, alpha, sigma, r_s):
         self.pb = pb
-        ng, NK, NX = pb.ng, pb.NK, pb.NX
+        ng, NK, NX = pb.ng, pb.NK, pb.nz           # cone rows have the n_z of zeta = Gamma z
         self.m = ng * (1 + NX)
         n = NK + ng
         self.rho, self.alpha = rho, alpha
@@ -262,7 +275,7 @@ class DenseDR:
 
     def proj_K(self, s):
         out = s.copy()
-        NX = self.pb.NX
+        NX = self.pb.nz
         for j in range(self.pb.ng):
             r0 = j * (1 + NX)
             t, y = proj_soc(s[r0], s[r0 + 1:r0 + 1 + NX])

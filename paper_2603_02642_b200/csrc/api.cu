@@ -303,6 +303,8 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
 extern "C" nrto_err nrto_refresh(nrto_handle h, const nrto_data* data, void* stream) {
   if (!h) return fail(NRTO_ESTATE, "handle is NULL");
   if (!data) return fail(NRTO_EINVAL, "data is NULL");
+  if (h->general && !h->gen_refresh_ok)
+    return fail(NRTO_EINVAL, "nrto_refresh of a general-set handle: call nrto_setup_general again");
   Dev& v = h->dev;
   const Dims& d = v.d;
   const int ng = d.ng, T = d.T, nx = d.nx, nu = d.nu;
@@ -478,6 +480,45 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     if (h->prof) { cudaEventRecord(b, st); h->recs.push_back({NRTO_K_QP, a, b}); }
     return e;
   };
+  if (h->general) {                     // general (Gamma, S) set, FullADMM in order
+    if (engine != NRTO_FULLADMM) return fail(NRTO_EINVAL, "general-set handles support NRTO_FULLADMM only");
+    CK(launch_fa_reset(h, st));
+    CK(gen_reset(h, st));
+    for (int l = 1; l <= prm.max_iter; ++l) {
+      CK(gen_iteration(h, l, st));
+      if (!prm.fixed_iters && l % prm.check_every == 0 && l < prm.max_iter) {
+        const int c = poll_active(h, dcount, 0, st, &ce);
+        if (ce != cudaSuccess) return cuda_fail(ce, "poll");
+        if (c == 0) break;
+      }
+    }
+    v.case_cnt = nullptr;
+    CK(gen_finish(h, mc_d, st));
+    CK(launch_finish_inst(h, ml_d, obj_d, st));
+    const bool host = o->memory == NRTO_MEM_HOST;
+    const size_t D8 = sizeof(double);
+    const int64_t nzr = B * d.ng * h->gen.nz;
+    CK(copy_out(o->kv, v.K, B * d.NK * D8, host, st));
+    CK(copy_out(o->du, v.du, B * d.T * d.nu * D8, host, st));
+    CK(copy_out(o->p, v.p, B * d.ng * D8, host, st));
+    CK(copy_out(o->p_tilde, v.pt, B * d.ng * D8, host, st));
+    CK(copy_out(o->lam_p, v.lamp, B * d.ng * D8, host, st));
+    CK(copy_out(o->iters, v.iters, B * 4, host, st));
+    CK(copy_out(o->status, v.status, B * 4, host, st));
+    CK(copy_out(o->r_p, v.r_p, B * D8, host, st));
+    CK(copy_out(o->r_d, v.r_d, B * D8, host, st));
+    CK(copy_out(o->nu, h->gen.nu, nzr * D8, host, st));
+    CK(copy_out(o->lam_nu, h->gen.lam, nzr * D8, host, st));
+    if (v.hist) CK(copy_out(o->hist, v.hist, (size_t)B * v.hist_L * 3 * D8, host, st));
+    v.hist = nullptr;
+    if (host) {
+      CK(copy_out(o->objective, obj_d, B * D8, true, st));
+      CK(copy_out(o->margin_cone, mc_d, B * d.ng * D8, true, st));
+      CK(copy_out(o->margin_lin, ml_d, B * d.ng * D8, true, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    return NRTO_OK;
+  }
   if (engine == NRTO_FULLADMM) {
     CK(launch_fa_reset(h, st));
     // QP(l) only gates project(l+1): in fixed-iteration mode it runs on the aux
@@ -716,6 +757,7 @@ extern "C" nrto_err nrto_gain_update(nrto_handle h, const double* nu, const doub
                                      double* kv_next, void* stream) {
   if (!h) return fail(NRTO_ESTATE, "handle is NULL");
   if (!nu || !kv_prev || !kv_next) return fail(NRTO_EINVAL, "NULL argument");
+  if (h->general) return fail(NRTO_EINVAL, "nrto_gain_update is not available for a general-set handle");
   CK(launch_gain_update(h, nu, kv_prev, kv_next, (cudaStream_t)stream));
   return NRTO_OK;
 }
@@ -753,6 +795,7 @@ extern "C" nrto_err nrto_destroy(nrto_handle h) {
   if (h->stage_b) cudaFree(h->stage_b);
   if (h->stage_e2) cudaFree(h->stage_e2);
   if (h->case_buf) cudaFree(h->case_buf);
+  gen_free(h);
   free_all(h);
   delete h;
   return NRTO_OK;
@@ -873,6 +916,7 @@ extern "C" nrto_err nrto_solve_begin(nrto_handle h, int32_t engine, void* stream
   v.hist = nullptr;
   v.hist_L = engine == NRTO_FULLADMM ? v.prm.max_iter : v.prm.max_admm_iter;
   v.case_cnt = nullptr;
+  if (h->general) return fail(NRTO_EINVAL, "general-set handles: use nrto_inner_solve");
   if (engine == NRTO_FULLADMM) {
     CK(launch_fa_reset(h, st));
   } else {
@@ -922,4 +966,73 @@ extern "C" nrto_err nrto_solve_end(nrto_handle h, const nrto_out* o, void* strea
   const nrto_err se = out_staging(h, o, &nu_d, &lam_d, &obj_d, &mc_d, &ml_d);
   if (se != NRTO_OK) return se;
   return write_outputs(h, engine, o, (cudaStream_t)stream, nu_d, lam_d, obj_d, mc_d, ml_d);
+}
+
+// ---------------------------------------------------------------------------
+// General uncertainty set (general.cu)
+__global__ void k_fill_eye_blocks(double* Psi, int nblk, int nx, double* tau, int B) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)nblk * nx * nx;
+  if (id < n) { const int64_t r = id % ((int64_t)nx * nx); Psi[id] = (r / nx == r % nx) ? 1.0 : 0.0; }
+  if (id < B) tau[id] = 1.0;
+}
+
+extern "C" nrto_err nrto_setup_general(const nrto_shape* s, const nrto_data* data,
+                                       const nrto_uncertainty* unc, const nrto_params* prm,
+                                       void* stream, nrto_handle* out) {
+  if (!out) return fail(NRTO_EINVAL, "out handle pointer is NULL");
+  *out = nullptr;
+  nrto_err e = check_shape(s);
+  if (e != NRTO_OK) return e;
+  if (!data || !unc || !prm) return fail(NRTO_EINVAL, "data / uncertainty / params is NULL");
+  if (unc->n_z < 1 || !unc->Gamma || !unc->Psi) return fail(NRTO_EINVAL, "n_z >= 1, Gamma and Psi required");
+  const int64_t NK = (int64_t)s->T * s->n_u * s->n_x;
+  if (NK > 4096) return fail(NRTO_EINVAL, "general sets: T n_u n_x must be <= 4096 (dense M^-1)");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool host = data->memory == NRTO_MEM_HOST;
+  const int64_t B = s->batch;
+  // shadow primitives: Psi_k = I, tau = 1 -> the regular setup yields the raw costates
+  double *psi = nullptr, *tau1 = nullptr, *taud = nullptr;
+  const int64_t npsi = B * (s->T + 1) * s->n_x * s->n_x;
+  CK(cudaMalloc((void**)&psi, (size_t)npsi * 8));
+  CK(cudaMalloc((void**)&tau1, (size_t)B * 8));
+  k_fill_eye_blocks<<<(unsigned)((std::max<int64_t>(npsi, B) + 255) / 256), 256, 0, st>>>(
+      psi, (int)(B * (s->T + 1)), s->n_x, tau1, (int)B);
+  nrto_data sd = *data;
+  sd.memory = NRTO_MEM_DEVICE;
+  std::vector<double*> tmp;
+  auto dev_copy = [&](const double* src, int64_t n) -> const double* {
+    if (!host || !src) return src;
+    double* p = nullptr;
+    if (cudaMalloc((void**)&p, (size_t)std::max<int64_t>(n, 1) * 8) != cudaSuccess) return nullptr;
+    cudaMemcpyAsync(p, src, (size_t)n * 8, cudaMemcpyHostToDevice, st);
+    tmp.push_back(p);
+    return p;
+  };
+  const int T = s->T, nx = s->n_x, nu = s->n_u, ng = s->n_g;
+  sd.A = dev_copy(data->A, B * T * nx * nx); sd.B = dev_copy(data->B, B * T * nx * nu);
+  sd.grad = dev_copy(data->grad, B * ng * nx); sd.g0 = dev_copy(data->g0, B * ng);
+  sd.W_K = dev_copy(data->W_K, B * T * nu * nu); sd.R_u = dev_copy(data->R_u, B * T * nu * nu);
+  sd.u_hat = dev_copy(data->u_hat, B * T * nu); sd.r_trust = dev_copy(data->r_trust, B);
+  sd.Psi = psi; sd.tau = tau1;
+  nrto_handle h = nullptr;
+  e = nrto_setup(s, &sd, prm, stream, &h);
+  if (e == NRTO_OK) {
+    cudaError_t ce = cudaMalloc((void**)&taud, (size_t)B * 8);
+    if (ce == cudaSuccess) {
+      h->gen.allocs[h->gen.nallocs++] = taud;
+      ce = cudaMemcpyAsync(taud, data->tau, (size_t)B * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st);
+    }
+    h->gen.tau = taud;
+    int spd = 0;
+    if (ce == cudaSuccess) ce = gen_setup(h, unc->Gamma, unc->Psi, unc->n_z, unc->memory == NRTO_MEM_HOST, st, &spd);
+    if (ce != cudaSuccess) { e = cuda_fail(ce, "nrto_setup_general"); nrto_destroy(h); h = nullptr; }
+    else if (spd) { e = fail(NRTO_ENOTSPD, "M^-1 = Q_v + rho sum A_hat^T A_hat is not SPD"); nrto_destroy(h); h = nullptr; }
+    else h->general = 1;
+  }
+  cudaStreamSynchronize(st);
+  for (double* p : tmp) cudaFree(p);
+  cudaFree(psi); cudaFree(tau1);
+  *out = h;
+  return e;
 }

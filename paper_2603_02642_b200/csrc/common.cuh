@@ -123,6 +123,25 @@ struct Dev {
 
 }  // namespace nrto
 
+namespace nrto {
+// General uncertainty set state (general.cu)
+struct GenState {
+  int nz = 0;
+  double* tau = nullptr;   // [B] the instances' tau (the regular setup ran with tau = 1)
+  double* W = nullptr;     // [B][n_z][NX]  sqrt(tau) Psi Gamma^T
+  double* Bh = nullptr;    // [B][n_g][n_z] b_hat_j
+  double* L = nullptr;     // [B][NK][NK]   Cholesky factor of M^{-1}
+  double* lam = nullptr;   // [B][n_g][n_z] scaled lam_nu
+  double* nu = nullptr;    // [B][n_g][n_z]
+  double* a = nullptr;     // [B][n_g][n_z] scratch: A_hat k + b_hat / nu - b_hat
+  double* V = nullptr;     // [B][n_g][NX]  scratch: A_bar k + c  /  (nu - b_hat) W
+  double* Cf = nullptr;    // [B][n_g][NX]  raw costates c_j (dense rows)
+  double* rhs = nullptr;   // [B][NK]
+  void* allocs[16];
+  int nallocs = 0;
+};
+}  // namespace nrto
+
 struct nrto_prof_rec { int cls; cudaEvent_t a, b; };
 
 struct nrto_handle_s {
@@ -164,6 +183,9 @@ struct nrto_handle_s {
   unsigned long long* case_buf = nullptr;   // [case_cap][3]
   int64_t case_cap = 0;
   int case_L = 0;                           // rows written by the last FullADMM solve
+  int general = 0;                          // general (Gamma, S) set: nrto_setup_general
+  int gen_refresh_ok = 0;
+  nrto::GenState gen;
   int inc_engine = -1;                      // incremental solve in progress (nrto_solve_begin)
   int inc_l = 0;                            // outer iterations run by it
 };
@@ -261,6 +283,13 @@ cudaError_t launch_soc_project(const double* t, const double* y, const int64_t* 
                                int64_t n, double* to, double* yo, cudaStream_t st);
 cudaError_t launch_count_active(nrto_handle_s* h, int32_t* d_count, int dr, cudaStream_t st);
 cudaError_t launch_solve_flags(nrto_handle_s* h, double* flags, cudaStream_t st);
+cudaError_t launch_finish_inst(nrto_handle_s* h, double* margin_lin, double* objective, cudaStream_t st);
+cudaError_t gen_setup(nrto_handle_s* h, const double* Gamma, const double* Psi, int nz, bool host,
+                      cudaStream_t st, int* spd_err);
+cudaError_t gen_reset(nrto_handle_s* h, cudaStream_t st);
+cudaError_t gen_iteration(nrto_handle_s* h, int l, cudaStream_t st);
+cudaError_t gen_finish(nrto_handle_s* h, double* mcone, cudaStream_t st);
+void gen_free(nrto_handle_s* h);
 int read_setup_error(cudaStream_t st);
 cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st);
 cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st);

@@ -941,6 +941,19 @@ cudaError_t launch_finish(nrto_handle_s* h, int engine, const nrto_out* o, cudaS
   return cudaGetLastError();
 }
 
+cudaError_t launch_finish_inst(nrto_handle_s* h, double* margin_lin, double* objective, cudaStream_t st) {
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  const size_t fsm = (size_t)(d.T + 1) * d.nx * sizeof(double);
+  if (fsm > 48 * 1024) {
+    if (fsm > 227 * 1024) return cudaErrorInvalidValue;
+    cudaFuncSetAttribute(k_finish_inst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+  }
+  k_finish_inst<<<d.B, 128, fsm, st>>>(v, margin_lin, objective);
+  h->launches++;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gain_update(nrto_handle_s* h, const double* nu, const double* kv_prev,
                                double* kv_next, cudaStream_t st) {
   Dev& v = h->dev;

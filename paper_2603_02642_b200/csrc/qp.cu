@@ -450,13 +450,7 @@ constexpr int kQPRing = QP_RING;   // power of two (common.cuh)
 #define QP_THREADS 256
 #endif
 #ifndef QP_CHUNK            // recurrence steps per bulk copy (divides QP_RING)
-#define QP_CHUNK 1
-#endif
-#ifndef QP_RFENCE           // membar.cta before each recurrence-step publication
-#define QP_RFENCE 1
-#endif
-#ifndef QP_EAHEAD           // e_k prefetch distance of the forward sweep
-#define QP_EAHEAD 4
+#define QP_CHUNK 4
 #endif
 
 // ---------------------------------------------------------------------------
@@ -559,8 +553,19 @@ __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int ti
 // Spin until a shared-memory epoch flag reaches `ep` (producer: data, membar.cta,
 // flag), then order the following reads after it.
 __device__ __forceinline__ void qp_spin(volatile int16_t* f, int16_t ep) {
-  while (*f < ep) __nanosleep(20);
-  __threadfence_block();
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared((const void*)f);
+  for (;;) {
+    unsigned short x;
+    asm volatile("ld.acquire.cta.shared.b16 %0, [%1];" : "=h"(x) : "r"(a) : "memory");
+    if ((int16_t)x >= ep) break;
+    __nanosleep(20);
+  }
+}
+// Publish an epoch flag: release store (orders this thread's earlier accesses,
+// incl. the data the flag announces, before it at CTA scope).
+__device__ __forceinline__ void qp_publish(volatile int16_t* f, int16_t ep) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared((const void*)f);
+  asm volatile("st.release.cta.shared.b16 [%0], %1;" ::"r"(a), "h"((unsigned short)ep) : "memory");
 }
 
 // Rows of one QP iteration in knot order (v.qrow: for p = 1..T the state rows at
@@ -741,8 +746,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
   double* sS = sm;                                    // [(T+1) nx]
   double* ring = sS + (T + 1) * nx;                   // [kQPRing][nx nx]
   uint64_t* qbar = reinterpret_cast<uint64_t*>(ring + kQPRing * nx * nx);   // [kQPRing]
-  double* eb = reinterpret_cast<double*>(qbar + kQPRing);                      // [QP_EAHEAD+1][16] e_k
-  int16_t* flg = reinterpret_cast<int16_t*>(eb + 16 * (QP_EAHEAD + 1));        // [5][T+1] (pipelined)
+  int16_t* flg = reinterpret_cast<int16_t*>(qbar + kQPRing);                  // [6][T+1] (pipelined)
   const int nn = nx * nx;
   const int nits = v.prm.qp_iters;
   int it_dbg = 0;
@@ -755,7 +759,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
   for (int r = tid; r < (T + 1) * nx; r += nt) gS[r] = 0.0;
   for (int r = tid; r < T * nu; r += nt) gU[r] = 0.0;
   if (NXM > 0)
-    for (int r = tid; r < 5 * (T + 1); r += nt) flg[r] = 0;
+    for (int r = tid; r < 6 * (T + 1); r += nt) flg[r] = 0;
   __syncthreads();
   QP_CLK(0);
   if (nits > 0) {                                     // rhs / w / scatter of iteration 0
@@ -780,7 +784,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
     volatile int16_t* fe = fs + (T + 1);
     volatile int16_t* fx = fe + (T + 1);
     volatile int16_t* fu = fx + (T + 1);
-    double* gE = v.dxt + (int64_t)b * (T + 1) * nx;    // e_k = B_k kff_k
+    volatile int16_t* fk = fu + (T + 1);
     for (int it = 0; it < nits; ++it) {
       it_dbg = it;
       const int16_t ep = (int16_t)(it + 1);
@@ -817,14 +821,20 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
         qp_spin(&fa[T], ep);
         const double* base = ring;
         int lo = 0, hi = -1;
+        long long tb0 = 0, tb1 = 0, tb2 = 0;
         for (int k = T - 1; k >= 0; --k) {
           const int c = (T - 1 - k) / C, p = pb + c;
+          const long long q0 = clock64();
           if (k > hi || k < lo) {
             chunk(p, lo, hi);
             qp_wait(&qbar[p % S], (uint32_t)(p / S) & 1u);
             base = ring + (p % S) * C * nn;
           }
+          const long long q1 = clock64();
+          tb0 += q1 - q0;
           qp_spin(&fa[k], ep);
+          const long long q2 = clock64();
+          tb1 += q2 - q1;
           const double* Ar = base + (k - lo) * nn + ic * nx;
           const double* sn = sS + (k + 1) * nx;
           double c0 = sS[k * nx + ic], c1 = 0.0;
@@ -838,41 +848,35 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
             }
           __syncwarp();
           if (lane < nx) sS[k * nx + lane] = c0 + c1;
-#if QP_RFENCE
-          __threadfence_block();
-#endif
           __syncwarp();
-          if (lane == 0) fs[k] = ep;
+          if (lane == 0) qp_publish(&fs[k], ep);
           if (k == lo) issue(p + S);
+          tb2 += clock64() - q2;
+        }
+        if (b == 0 && tid == 0 && it_dbg < 2) {
+          g_qp_clk[it_dbg * 32 + 12] = tb0; g_qp_clk[it_dbg * 32 + 13] = tb1; g_qp_clk[it_dbg * 32 + 14] = tb2;
         }
         QP_CLK(4);
-        // forward recurrence dx_{k+1} = Acl_k dx_k + e_k.  e_k reaches shared memory by
-        // cp.async QP_EAHEAD steps ahead (an outstanding plain global load would be
-        // waited for by a membar.cta)
-        constexpr int DE = QP_EAHEAD;
-        auto fetch_e = [&](int k) {
-          if (k < T) {
-            qp_spin(&fe[k], ep);
-            if (2 * lane < nx) cpa16(eb + (k % (DE + 1)) * 16 + 2 * lane, gE + k * nx + 2 * lane);
-          }
-          cpa_commit();
-        };
-        for (int k = 0; k < DE; ++k) fetch_e(k);
+        // forward recurrence dx_{k+1} = Acl_k dx_k + e_k, e_k in shared slot k+1 (overwritten
+        // by dx_{k+1})
+        for (int k = lane; k < T; k += 32) qp_spin(&fe[k], ep);   // every e_k (e_0 comes last)
+        if (lane < nx) sS[lane] = 0.0;                     // dx_0 = 0 (s_0 is not read by anyone)
+        __syncwarp();
         lo = 0; hi = -1;
+        long long tq0 = 0, tq1 = 0, tq2 = 0;
         for (int k = 0; k < T; ++k) {
           const int c = k / C, p = pb + NC + c;
-          fetch_e(k + DE);
-          cpa_wait<DE>();
-          if (k == 0 && lane < nx) sS[lane] = 0.0;       // dx_0 = 0 (s_0 is not read by anyone)
-          __syncwarp();
+          const long long q1 = clock64();
           if (k > hi || k < lo) {
             chunk(p, lo, hi);
             qp_wait(&qbar[p % S], (uint32_t)(p / S) & 1u);
             base = ring + (p % S) * C * nn;
           }
+          const long long q2 = clock64();
+          tq1 += q2 - q1;
           const double* Ar = base + (k - lo) * nn + ic * nx;
           const double* xk = sS + k * nx;
-          double c0 = eb[(k % (DE + 1)) * 16 + ic], c1 = 0.0;
+          double c0 = sS[(k + 1) * nx + ic], c1 = 0.0;
 #pragma unroll
           for (int r = 0; r < NXM; r += 2)
             if (r < nx) {
@@ -883,14 +887,14 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
             }
           __syncwarp();
           if (lane < nx) sS[(k + 1) * nx + lane] = c0 + c1;
-#if QP_RFENCE
-          __threadfence_block();
-#endif
           __syncwarp();
-          if (lane == 0) fx[k + 1] = ep;
+          if (lane == 0) qp_publish(&fx[k + 1], ep);
           if (k == hi) issue(p + S);
+          tq2 += clock64() - q2;
         }
-        cpa_wait<0>();
+        if (b == 0 && tid == 0 && it_dbg < 2) {
+          g_qp_clk[it_dbg * 32 + 16] = tq0; g_qp_clk[it_dbg * 32 + 17] = tq1; g_qp_clk[it_dbg * 32 + 18] = tq2;
+        }
         QP_CLK(7);
       } else {
         // helpers, knot k by warp (k mod nhw): a_k, r_u,k (descending, ahead of warp 0)
@@ -914,55 +918,91 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
             }
           }
           if (lane < nx) sS[k * nx + lane] = acc;       // a_k (k < T), s_T
-          __threadfence_block();
           __syncwarp();
-          if (lane == 0) fa[k] = ep;
+          if (lane == 0) qp_publish(&fa[k], ep);
         }
-        // kff_k = H^-1 r_u,k + H^-1 B_k^T s_{k+1}, e_k = B_k kff_k (descending, behind warp 0)
-        for (int k = T - 1 - (warp - 1); k >= 0; k -= nhw) {
-          qp_spin(k + 1 == T ? &fa[T] : &fs[k + 1], ep);
-          qp_spin(&fa[k], ep);
-          double ru = 0.0;
-          if (lane < nu) {
-            const int r = k * nu + lane;
-            ru = sq * du[r] + __ldcg(gU + r) + cu2[r];
-          }
-          double kf = 0.0;
-          const double* H = Hi + (int64_t)k * nu * nu + (lane < nu ? lane : 0) * nu;
+        // kff_k = H^-1 r_u,k + H^-1 B_k^T s_{k+1}, e_k = B_k kff_k (descending, behind warp 0).
+        // Lane (m, part) = (lane / 4, lane % 4) sums part of the NUM + NXM terms of kff[m];
+        // the constants of a warp's next knot are loaded while it waits for the current one.
+        {
+          constexpr int NT = NUM + NXM;                  // terms per kff row
+          constexpr int NP = (NT + 3) / 4;               // terms per lane
+          const int m = lane >> 2, part = lane & 3;
+          const bool mok = m < nu;
+          double hv[NP], bv[NUM], pr[3];
+          auto load = [&](int k) {
 #pragma unroll
-          for (int q = 0; q < (NUM > 0 ? NUM : 8); ++q) {
-            const double rq_ = __shfl_sync(0xffffffffu, ru, q);
-            if (q < nu && lane < nu) kf = fma(H[q], rq_, kf);
-          }
-          if (lane < nu) {
-            const double* hb = HB + (int64_t)k * nu * nx + lane * nx;
+            for (int u = 0; u < NP; ++u) {
+              const int t = part * NP + u;
+              hv[u] = 0.0;
+              if (mok && t < NT && k >= 0)
+                hv[u] = (t < NUM) ? Hi[(int64_t)k * nu * nu + m * nu + t]
+                                  : HB[(int64_t)k * nu * nx + m * nx + (t - NUM)];
+            }
+#pragma unroll
+            for (int q = 0; q < NUM; ++q)
+              bv[q] = (lane < nx && k >= 0) ? Bm[(int64_t)k * nx * nu + lane * nu + q] : 0.0;
+            if (lane < nu && k >= 0) {
+              const int r = k * nu + lane;
+              pr[0] = du[r]; pr[1] = __ldcg(gU + r); pr[2] = cu2[r];
+            }
+          };
+          int k = T - 1 - (warp - 1);
+          load(k);
+          for (; k >= 0; k -= nhw) {
+            double cur_h[NP], cur_b[NUM], cur_p[3];
+#pragma unroll
+            for (int u = 0; u < NP; ++u) cur_h[u] = hv[u];
+#pragma unroll
+            for (int q = 0; q < NUM; ++q) cur_b[q] = bv[q];
+            cur_p[0] = pr[0]; cur_p[1] = pr[1]; cur_p[2] = pr[2];
+            load(k - nhw);                               // next knot of this warp
+            const double ru = (lane < nu) ? sq * cur_p[0] + cur_p[1] + cur_p[2] : 0.0;
+            qp_spin(k + 1 == T ? &fa[T] : &fs[k + 1], ep);
             const double* sk = sS + (k + 1) * nx;
-            kf = dotn<NXM>(nx, [&](int q) { return hb[q]; }, [&](int q) { return sk[q]; }, kf);
-            gK[k * nu + lane] = kf;
-            gU[k * nu + lane] = 0.0;                     // scatter target of the next iteration
-          }
-          if (lane < nx) {
-            gS[k * nx + lane] = 0.0;
-            if (k == T - 1) gS[T * nx + lane] = 0.0;
-          }
-          double e = 0.0;
-          const double* Bk = Bm + (int64_t)k * nx * nu + (lane < nx ? lane : 0) * nu;
+            double acc = 0.0;
 #pragma unroll
-          for (int m = 0; m < (NUM > 0 ? NUM : 8); ++m) {
-            const double km = __shfl_sync(0xffffffffu, kf, m);
-            if (m < nu && lane < nx) e = fma(Bk[m], km, e);
+            for (int u = 0; u < NP; ++u) {
+              const int t = part * NP + u;
+              // every lane executes the same shuffle (uniform call site, full mask)
+              const double xr = __shfl_sync(0xffffffffu, ru, (t < NUM) ? t : 0);
+              if (t < NT) acc = fma(cur_h[u], (t < NUM) ? xr : sk[t - NUM], acc);
+            }
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);   // kff[m] in lanes 4m..4m+3
+            double e = 0.0;
+#pragma unroll
+            for (int q = 0; q < NUM; ++q) {
+              const double kq = __shfl_sync(0xffffffffu, acc, 4 * q);
+              e = fma(cur_b[q], kq, e);
+            }
+            // e_k goes to shared slot k+1 (s_{k+1} is dead once warp 0 has published s_k)
+            qp_spin(&fs[k], ep);
+            if (lane < nx) sS[(k + 1) * nx + lane] = e;
+            __syncwarp();
+            if (lane == 0) qp_publish(&fe[k], ep);
+            // kff_k (read by warp 1 in the forward phase) and the cleared scatter targets
+            // of the next QP iteration go to global memory; one fence per warp below
+            if (mok && part == 0) gK[k * nu + m] = acc;
+            if (lane < nu) gU[k * nu + lane] = 0.0;
+            if (lane < nx) {
+              gS[k * nx + lane] = 0.0;
+              if (k == T - 1) gS[T * nx + lane] = 0.0;
+            }
           }
-          if (lane < nx) gE[k * nx + lane] = e;
           __threadfence_block();
           __syncwarp();
-          if (lane == 0) fe[k] = ep;
+          if (lane == 0)
+            for (int kk = T - 1 - (warp - 1); kk >= 0; kk -= nhw) qp_publish(&fk[kk], ep);
         }
         if (warp == 1) {
           // du~_k = kff_k - Kf_k dx_k and du_k (relaxed), 4 knots per publication (fu)
           const int c = lane / nu, m = lane - c * nu;
+          double nbp = 0.0;
           for (int k0 = 0; k0 < T; k0 += 4) {
             const int k = k0 + c;
             qp_spin(&fx[min(k0 + 3, T - 1)], ep);
+            if (c < 4 && k < T) qp_spin(&fk[k], ep);
             if (c < 4 && k < T) {
               const double* Kk = Kf + (int64_t)k * nu * nx + m * nx;
               const double* xk = sS + k * nx;
@@ -971,10 +1011,21 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
               gR[k * nu + m] = dd;
               du[k * nu + m] = aq * dd + (1.0 - aq) * du[k * nu + m];
             }
-            __threadfence_block();
+            __threadfence_block();                       // global du~ before fu
             __syncwarp();
-            if (lane < 4 && k0 + lane < T) fu[k0 + lane] = ep;
+            if (lane < 4 && k0 + lane < T) qp_publish(&fu[k0 + lane], ep);
+            // trust-region ball partial sum of the knots whose dx is final (zb, yb then sit
+            // in this SM's L1 for the update after the barrier)
+            const int r1 = (k0 + 4 >= T ? T + 1 : k0 + 4) * nx;
+            if (k0 + 4 >= T) qp_spin(&fx[T], ep);
+            for (int r = k0 * nx + lane; r < r1; r += 32) {
+              const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
+              const double w = zh + yb[r] / rq;
+              nbp += w * w;
+            }
           }
+          nbp = warp_sum(nbp);
+          if (lane == 0) red[31] = nbp;
         } else {
           // rows in knot order, each as soon as dx_k (fx) / du~_k (fu) is published
           const bool more = it + 1 < nits;
@@ -984,20 +1035,15 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
       }
       __syncthreads();
       QP_CLK(9);
-      double nb = 0.0;                                  // trust-region ball
-      for (int r = tid; r < (T + 1) * nx; r += nt) {
-        const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
-        sS[r] = zh;
-        const double w = zh + yb[r] / rq;
-        nb += w * w;
-      }
-      nb = sqrt(block_sum(nb, red));
-      const double scl = (nb > rtr) ? rtr / nb : 1.0;
-      for (int r = tid; r < (T + 1) * nx; r += nt) {
-        const double zh = sS[r];
-        const double zn = scl * (zh + yb[r] / rq);
-        yb[r] += rq * (zh - zn);
-        zb[r] = zn;
+      {                                                 // trust-region ball (norm by warp 1)
+        const double nb = sqrt(red[31]);
+        const double scl = (nb > rtr) ? rtr / nb : 1.0;
+        for (int r = tid; r < (T + 1) * nx; r += nt) {
+          const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
+          const double zn = scl * (zh + yb[r] / rq);
+          yb[r] += rq * (zh - zn);
+          zb[r] = zn;
+        }
       }
       __syncthreads();
       QP_CLK(10);
@@ -1313,7 +1359,7 @@ cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
 cudaError_t launch_qp_sparse(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid) {
   const Dims& d = h->dev.d;
   const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx + kQPRing) * sizeof(double) +
-                      16 * (QP_EAHEAD + 1) * sizeof(double) + (size_t)5 * (d.T + 1) * sizeof(int16_t);
+                      (size_t)6 * (d.T + 1) * sizeof(int16_t);
   if (smem > 48 * 1024 || h->dev.prm.qp_iters > 32000) return launch_qp(h, engine, l, st);
   if (d.nx <= 127) {
     const int g = (grid > 0 && grid < d.B) ? grid : d.B;

@@ -65,6 +65,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+
 #ifndef TMA_NW
 #define TMA_NW 16
 #endif
@@ -76,13 +84,15 @@ constexpr int kHdr = 32;  // header doubles: 2 kMaxStages barriers + cnt/tag
 struct TmaGeom {          // shared-memory geometry of one stage (doubles)
   int SY;                 // b_hat region: 16 blocks x 8 cones x n_x, block-major
   int SB;                 // b region: 16 blocks x 8 cones x nup
+  int SD;                 // D region (streamed-D variant): 16 blocks x n_x x n_u
   int stage;              // doubles per stage (SY is a multiple of 16 doubles)
 };
-__host__ __device__ inline TmaGeom tma_geom(int nx, int nup) {
+__host__ __device__ inline TmaGeom tma_geom(int nx, int nup, int nu = 0, bool ds = false) {
   TmaGeom g;
   g.SY = (16 * 8 * nx + 15) & ~15;
   g.SB = 16 * 8 * nup;
-  g.stage = g.SY + g.SB;
+  g.SD = ds ? ((16 * nx * nu + 15) & ~15) : 0;
+  g.stage = g.SY + g.SB + g.SD;
   return g;
 }
 // Per-tile metadata staged by the producer in shared memory (kMetaT-slot ring,
@@ -98,8 +108,10 @@ struct TileMeta {
   double pad[7];
 };
 static_assert(sizeof(TileMeta) == 256, "TileMeta is 32 doubles");
-__host__ __device__ inline size_t tma_fixed_doubles(int T, int nx, int nu) {
-  return kHdr + kRingT * 16 * 8 + kMetaT * 32 + (((size_t)T * nx * nu + 1) & ~(size_t)1);
+// ds: D_k is streamed per chunk through the stages (long horizons) instead of being
+// resident in shared memory for the whole horizon
+__host__ __device__ inline size_t tma_fixed_doubles(int T, int nx, int nu, bool ds = false) {
+  return kHdr + kRingT * 16 * 8 + kMetaT * 32 + (ds ? 0 : (((size_t)T * nx * nu + 1) & ~(size_t)1));
 }
 
 // Fused state-cone pass (norm-only form).  Per cone block k:
@@ -111,7 +123,7 @@ __host__ __device__ inline size_t tma_fixed_doubles(int T, int nx, int nu) {
 // consumers straight from global memory, issued before the stage wait.
 // NXE, NUE > 0: exact n_x, n_u fixed at compile time (benchmark shapes): every
 // bounds predicate of the inner block folds away.
-template <int NTI, int NKS, int KK, int NXE, int NUE, int NW = 16>
+template <int NTI, int NKS, int KK, int NXE, int NUE, int NW = 16, bool DS = false>
 __global__ void __launch_bounds__((NW + 1) * 32, 1)
 k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ witems, int nst,
          int margin) {
@@ -121,7 +133,7 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
   const Dims d = v.d;
   const int nx = NXE > 0 ? NXE : d.nx, nu = NUE > 0 ? NUE : d.nu, T = d.T;
   const int nup = NUE > 0 ? (NUE + (NUE & 1)) : d.nup;
-  const TmaGeom G = tma_geom(nx, nup);
+  const TmaGeom G = tma_geom(nx, nup, nu, DS);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + kMaxStages;
   int* cnt = reinterpret_cast<int*>(empty + kMaxStages);
@@ -129,7 +141,8 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
   double* ring = sm + kHdr;                                // [kRingT][NW][8]
   TileMeta* meta = reinterpret_cast<TileMeta*>(ring + kRingT * NW * 8);   // [kMetaT]
   double* Ds = ring + kRingT * NW * 8 + kMetaT * 32;       // [T][nx][nu]
-  double* stg = sm + tma_fixed_doubles(T, nx, nu);         // stages
+  double* stg = sm + tma_fixed_doubles(T, nx, nu, DS);     // stages
+  const double* __restrict__ Dg = (margin ? v.Ccur : v.D) + (int64_t)witems[4 * blockIdx.x] * T * nx * nu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int b = witems[4 * blockIdx.x], t0 = witems[4 * blockIdx.x + 1];
@@ -137,9 +150,8 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
   if (!margin && !v.active[b]) return;
   double* __restrict__ Y = v.Y + (int64_t)b * d.E;
   const int64_t bg = (int64_t)b * d.ng;
-  {
+  if (!DS) {
     // margin mode (finish): ||C^L_k b + b_hat|| of every state cone, no history, no store
-    const double* Dg = (margin ? v.Ccur : v.D) + (int64_t)b * T * nx * nu;
     for (int r = threadIdx.x; r < T * nx * nu; r += blockDim.x) Ds[r] = Dg[r];
   }
   if (threadIdx.x == 0) {
@@ -194,13 +206,16 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
         if (lane == 0) {
           mbar_wait(&empty[st], ph ^ 1);
           const uint32_t hb = (uint32_t)nc * nb * nx * 8u, bb = (uint32_t)nc * nbB * nup * 8u;
-          mbar_expect_tx(&full[st], hb + bb);
+          const uint32_t db = DS ? (uint32_t)nbB * nx * nu * 8u : 0u;
+          mbar_expect_tx(&full[st], hb + bb + db);
           moved += hb + bb + (unsigned long long)(nyr + nyw) * nb * nx * 8u;
           double* sH = stg + (size_t)st * G.stage;
           double* sB = sH + G.SY;
           // one bulk copy per array: the chunk is contiguous in the tile layout
           bulk_g2s(sH, bht + tb0 + (int64_t)kc * nc * nx, hb, &full[st], pol);
           if (bb > 0) bulk_g2s(sB, bdt + tb1 + (int64_t)kc * nc * nup, bb, &full[st], pol);
+          // D_k of the chunk's blocks (re-read by every tile of the instance: L2 hits)
+          if (DS && db > 0) bulk_g2s_keep(sB + G.SB, Dg + (int64_t)kc * nx * nu, db, &full[st]);
         }
         __syncwarp();
         if (++st == nst) { st = 0; ph ^= 1; }
@@ -240,7 +255,8 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
 #pragma unroll
       for (int bb = 0; bb < BPW; ++bb) load_y(yo[bb], warp + NW * bb);
     }
-#pragma unroll
+    constexpr int KU = KK <= 26 ? KK : 1;
+#pragma unroll KU
     for (int kk = 0; kk < KK; ++kk) {
       const int kc = CH * kk;
       if (kc > K) break;
@@ -280,7 +296,10 @@ k_fa_tma(Dev v, const int32_t* __restrict__ tiles, const int32_t* __restrict__ w
 #pragma unroll
             for (int nt = 0; nt < NTI; ++nt) {
               const int i = g + 8 * nt;
-              const double bq = (m < nu && i < nx) ? Ds[((size_t)k * nx + i) * nu + m] : 0.0;
+              const double bq = (m < nu && i < nx)
+                                    ? (DS ? sB[G.SB + ((size_t)lb * nx + i) * nu + m]
+                                          : Ds[((size_t)k * nx + i) * nu + m])
+                                    : 0.0;
               dmma2(c[nt], a, bq);
             }
           }
@@ -511,11 +530,13 @@ cudaError_t launch_gram_tiles(nrto_handle_s* h, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-static int tma_stages(const Dims& d) {
-  const TmaGeom G = tma_geom(d.nx, d.nup);
-  const size_t fixed = tma_fixed_doubles(d.T, d.nx, d.nu);
-  // leave room for one k_qp_sparse CTA beside the pass CTA (overlapped QP)
-  const size_t qp = ((size_t)(d.T + 1) * d.nx + (size_t)QP_RING * d.nx * d.nx) * sizeof(double);
+static int tma_stages(const Dims& d, bool ds = false) {
+  const TmaGeom G = tma_geom(d.nx, d.nup, d.nu, ds);
+  const size_t fixed = tma_fixed_doubles(d.T, d.nx, d.nu, ds);
+  // leave room for one k_qp_sparse CTA beside the pass CTA (overlapped QP): its
+  // recurrence vector, Acl ring, barriers and per-knot flags (qp.cu)
+  const size_t qp = ((size_t)(d.T + 1) * d.nx + (size_t)QP_RING * d.nx * d.nx + QP_RING) * sizeof(double) +
+                    (size_t)6 * (d.T + 1) * sizeof(int16_t);
   size_t capb = 225 * 1024;
   if (228 * 1024 > qp + 2048 + 3 * G.stage * sizeof(double) + fixed * sizeof(double))
     capb = std::min<size_t>(capb, 228 * 1024 - 2048 - qp);
@@ -524,24 +545,30 @@ static int tma_stages(const Dims& d) {
   return (int)std::min<size_t>(kMaxStages, (cap - fixed) / G.stage);
 }
 
+// streamed-D variant: when D of the whole horizon does not fit beside >= 3 stages
+static bool tma_dstream(const Dims& d) { return tma_stages(d, false) < 3; }
+
 size_t tma_smem_bytes(const Dims& d) {
-  const TmaGeom G = tma_geom(d.nx, d.nup);
-  return (tma_fixed_doubles(d.T, d.nx, d.nu) + (size_t)tma_stages(d) * G.stage) * sizeof(double);
+  const bool ds = tma_dstream(d);
+  const TmaGeom G = tma_geom(d.nx, d.nup, d.nu, ds);
+  return (tma_fixed_doubles(d.T, d.nx, d.nu, ds) + (size_t)tma_stages(d, ds) * G.stage) * sizeof(double);
 }
 
 bool tma_supported(const Dims& d) {
-  // T <= 415: the pass keeps D_k of the whole horizon in shared memory (tma_stages
-  // checks that it fits with >= 3 stages) and unrolls up to 26 chunks per tile
-  return (d.nx % 2 == 0) && d.nx <= 16 && d.nu <= 8 && d.T <= 415 && tma_stages(d) >= 3;
+  // n_x even (16-byte DMMA operand rows), n_x <= 16, n_u <= 8; horizons up to
+  // 1023 (64 chunks of 16 blocks per tile); D_k resident in shared memory when it
+  // fits beside >= 3 stages, otherwise streamed per chunk through the stages
+  if (!((d.nx % 2 == 0) && d.nx <= 16 && d.nu <= 8 && d.T <= 1023)) return false;
+  return tma_stages(d, false) >= 3 || tma_stages(d, true) >= 3;
 }
 
-template <int NTI, int NKS, int KK, int NXE = 0, int NUE = 0, int NW = 16>
+template <int NTI, int NKS, int KK, int NXE = 0, int NUE = 0, int NW = 16, bool DS = false>
 static cudaError_t launch_tma_t(nrto_handle_s* h, cudaStream_t st) {
   const size_t smem = tma_smem_bytes(h->dev.d);
-  auto kfn = k_fa_tma<NTI, NKS, KK, NXE, NUE, NW>;
+  auto kfn = k_fa_tma<NTI, NKS, KK, NXE, NUE, NW, DS>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kfn<<<h->dev.nwitems, (NW + 1) * 32, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems, tma_stages(h->dev.d),
-                                         h->tma_margin);
+  kfn<<<h->dev.nwitems, (NW + 1) * 32, smem, st>>>(h->dev, h->dev.tiles, h->dev.witems,
+                                                   tma_stages(h->dev.d, DS), h->tma_margin);
   h->launches++;
   return cudaGetLastError();
 }
@@ -554,13 +581,26 @@ static cudaError_t launch_tma_k(nrto_handle_s* h, int nti, int nks, cudaStream_t
   return launch_tma_t<2, 2, KK>(h, st);
 }
 
+template <int KK>
+static cudaError_t launch_tma_ds(nrto_handle_s* h, int nti, int nks, cudaStream_t st) {
+  if (nti == 1 && nks == 1) return launch_tma_t<1, 1, KK, 0, 0, 16, true>(h, st);
+  if (nti == 1 && nks == 2) return launch_tma_t<1, 2, KK, 0, 0, 16, true>(h, st);
+  if (nti == 2 && nks == 1) return launch_tma_t<2, 1, KK, 0, 0, 16, true>(h, st);
+  return launch_tma_t<2, 2, KK, 0, 0, 16, true>(h, st);
+}
+
 cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st) {
   const Dims& d = h->dev.d;
   const int nti = (d.nx + 7) / 8, nks = (d.nu + 3) / 4;
   cudaError_t e = cudaSuccess;
   if (h->dev.nwitems > 0) {
     // KK = chunks of 16 blocks per tile: covers K <= 16 KK - 1
-    if (d.nx == 14 && d.nu == 7 && d.T >= 64 && d.T < 112) e = launch_tma_t<2, 2, 7, 14, 7, TMA_NW>(h, st);
+    if (tma_dstream(d)) {
+      if (d.T < 208) e = launch_tma_ds<13>(h, nti, nks, st);
+      else if (d.T < 416) e = launch_tma_ds<26>(h, nti, nks, st);
+      else e = launch_tma_ds<64>(h, nti, nks, st);
+    }
+    else if (d.nx == 14 && d.nu == 7 && d.T >= 64 && d.T < 112) e = launch_tma_t<2, 2, 7, 14, 7, TMA_NW>(h, st);
     else if (d.nx == 12 && d.nu == 4 && d.T >= 32 && d.T < 64) e = launch_tma_t<2, 1, 4, 12, 4>(h, st);
     else if (d.T < 32) e = launch_tma_k<2>(h, nti, nks, st);
     else if (d.T < 64) e = launch_tma_k<4>(h, nti, nks, st);

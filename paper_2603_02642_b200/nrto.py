@@ -39,6 +39,10 @@ PARAM_DOUBLES = ("rho", "rho_admm", "alpha_dr", "sigma_dr", "r_s", "eps_p", "eps
 PARAM_INTS = ("max_iter", "max_admm_iter", "max_dr_iter", "qp_iters", "check_every", "fixed_iters")
 
 
+class nrto_uncertainty(C.Structure):
+    _fields_ = [("memory", C.c_int32), ("n_z", C.c_int32), ("Gamma", C.c_void_p), ("Psi", C.c_void_p)]
+
+
 class nrto_params(C.Structure):
     _fields_ = [(n, C.c_double) for n in PARAM_DOUBLES] + [(n, C.c_int32) for n in PARAM_INTS]
 
@@ -84,6 +88,9 @@ def lib():
         L.nrto_profile_read.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_double),
                                         C.POINTER(C.c_int64)]
         L.nrto_pass_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+        L.nrto_setup_general.argtypes = [C.POINTER(nrto_shape), C.POINTER(nrto_data),
+                                         C.POINTER(nrto_uncertainty), C.POINTER(nrto_params),
+                                         C.c_void_p, C.POINTER(C.c_void_p)]
         L.nrto_case_stats_enable.argtypes = [C.c_void_p, C.c_int32]
         L.nrto_case_stats_read.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]
         L.nrto_solve_begin.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
@@ -94,7 +101,7 @@ def lib():
                   "nrto_soc_project", "nrto_destroy", "nrto_refresh", "nrto_profile_enable",
                   "nrto_profile_read", "nrto_pass_bytes", "nrto_case_stats_enable",
                   "nrto_case_stats_read", "nrto_solve_begin", "nrto_solve_iterate",
-                  "nrto_solve_flags", "nrto_solve_end"):
+                  "nrto_solve_flags", "nrto_solve_end", "nrto_setup_general"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -176,6 +183,20 @@ def nrto_setup(shape, data: dict, params: nrto_params, stream=None, memory=NRTO_
     dd = nrto_data(memory, *[_ptr(data[k]) for k in DATA_KEYS])
     h = C.c_void_p()
     _check(lib().nrto_setup(C.byref(s), C.byref(dd), C.byref(params), _stream_ptr(stream), C.byref(h)))
+    return h.value
+
+
+def nrto_setup_general(shape, data: dict, Gamma, Psi, params: nrto_params, stream=None,
+                       memory=NRTO_MEM_DEVICE):
+    """General uncertainty set (zeta = Gamma z, Psi^T Psi = S^-1): tensors
+    Gamma [b][(T+1) n_x][n_z], Psi [b][n_z][n_z] in the same memory as data."""
+    batch = int(data["tau"].shape[0])
+    s = _shape_struct(shape, batch)
+    dd = nrto_data(memory, *[_ptr(data[k]) for k in DATA_KEYS])
+    un = nrto_uncertainty(memory, int(Gamma.shape[-1]), _ptr(Gamma), _ptr(Psi))
+    h = C.c_void_p()
+    _check(lib().nrto_setup_general(C.byref(s), C.byref(dd), C.byref(un), C.byref(params),
+                                    _stream_ptr(stream), C.byref(h)))
     return h.value
 
 
@@ -289,15 +310,22 @@ def alloc_out(shape, batch, E, device="cuda", pinned=False, full=True, ragged=Tr
 
 
 class InnerSolver:
-    """Owns one nrto handle for a batch of instances sharing a cone structure."""
+    """Owns one nrto handle for a batch of instances sharing a cone structure.
+    With Gamma / Psi given: a general uncertainty set (nrto_setup_general); the
+    ragged nu / lam_nu outputs are then dense [b][n_g][n_z] rows."""
 
-    def __init__(self, shape, data: dict, params=None, stream=None, memory=NRTO_MEM_DEVICE, **pkw):
+    def __init__(self, shape, data: dict, params=None, stream=None, memory=NRTO_MEM_DEVICE,
+                 Gamma=None, Psi=None, **pkw):
         self.shape = shape
         self.params = params if params is not None else nrto_default_params(**pkw)
         self.batch = int(data["tau"].shape[0])
         self.E, self.offsets = nrto_layout(shape, self.batch)
         self.stream = stream
-        self.handle = nrto_setup(shape, data, self.params, stream, memory)
+        if Gamma is not None:
+            self.E = shape.n_g * int(Gamma.shape[-1])
+            self.handle = nrto_setup_general(shape, data, Gamma, Psi, self.params, stream, memory)
+        else:
+            self.handle = nrto_setup(shape, data, self.params, stream, memory)
 
     def solve(self, engine=NRTO_FULLADMM, out=None, full=True, memory=NRTO_MEM_DEVICE):
         if out is None:

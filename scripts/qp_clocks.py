@@ -22,4 +22,7 @@ for it in (0, 1):
     start = c[1] if it == 0 else c[10]
     row = c[it * 32: it * 32 + 11]
     print(f" it{it}:", ", ".join(f"{names[p]} +{row[p] - start}" for p in range(2, 11) if row[p] > 0))
+    r = c[it * 32: it * 32 + 32]
+    if r[12] or r[16]:
+        print(f"   bwd: chunk-wait {r[12]}, a_k spin {r[13]}, step {r[14]};  fwd: e-wait {r[16]}, chunk-wait {r[17]}, step {r[18]}")
 s.close()
