@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnrto.so")
-SOURCES = ["api.cu", "setup.cu", "iter.cu", "qp.cu", "fused.cu", "tma.cu", "general.cu"]
+SOURCES = ["api.cu", "setup.cu", "iter.cu", "qp.cu", "fused.cu", "tma.cu", "general.cu", "persist.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
          "--expt-relaxed-constexpr", "-cudart", "static"]

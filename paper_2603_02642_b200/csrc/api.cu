@@ -247,9 +247,13 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   v.uhat = uhat; v.rtrust = rtrust;
   AL(v.bhat, B * d.E); AL(v.Bd, B * d.EB); AL(v.Zb, B * T * nu * nx); AL(v.Lam, B * T * nu * nu);
   AL(v.U, B * T * nx * nx); AL(v.Ulam, B * T * nx); AL(v.Urep, B * T); AL(v.psame, B * T);
+  v.scanM = 0; v.scanC = 0;
+  if (B <= kScanMaxBatch && T >= 2 && nx <= 32 && nu <= 32) scan_plan(T, v.scanM, v.scanC);
   for (EngineFactors* F : {&v.fa, &v.dr}) {
     AL(F->V, B * T * nu * nu); AL(F->den, B * T * nu * nx); AL(F->Kf, B * T * nu * nx);
     AL(F->Acl, B * T * nx * nx); AL(F->AclT, B * T * nx * nx); AL(F->Hinv, B * T * nu * nu); AL(F->HB, B * T * nu * nx);
+    F->PhiB = nullptr; F->PhiF = nullptr;
+    if (v.scanC > 0) { AL(F->PhiB, B * T * nx * nx); AL(F->PhiF, B * T * nx * nx); }
   }
   AL(v.Y, B * d.E); AL(v.s, B * ng); AL(v.tin, B * ng); AL(v.pt, B * ng); AL(v.ptprev, B * ng);
   AL(v.p, B * ng); AL(v.lamp, B * ng); AL(v.K, B * d.NK); AL(v.Ccur, B * T * nx * nu);
@@ -274,6 +278,19 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   cudaMemset(v.pass_bytes, 0, sizeof(unsigned long long));
   v.ylazy = 0;
   AL(v.clist, B * ng); AL(v.cw, B * ng); AL(v.ncorr, B);
+  // persistent DR loop (persist.cu): cone chunks of one instance
+  std::vector<int32_t> drch, drkr;
+  int drEc = 0, drEBc = 0;
+  dr_loop_plan(d, s->cone_knot, s->cone_kind, nsm, drch, drkr, drEc, drEBc);
+  v.drQ = drch.empty() ? 0 : (int)drch.size() - 1;
+  v.drchunk = nullptr; v.drkr = nullptr; v.drZpart = nullptr; v.drrq = nullptr; v.drbar = nullptr;
+  v.drEc = drEc; v.drEBc = drEBc;
+  if (v.drQ > 0) {
+    int32_t *dch, *dkr;
+    AL(dch, drch.size()); AL(dkr, drkr.size());
+    v.drchunk = dch; v.drkr = dkr;
+    AL(v.drZpart, B * v.drQ * T * nu * nx); AL(v.drrq, B * v.drQ); AL(v.drbar, 1);
+  }
 
   // shape arrays (pageable host vectors: synchronous copies)
   cudaError_t ce = cudaSuccess;
@@ -287,6 +304,12 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   hup(dcptr, cptr.data(), (T + 1) * 4); hup(dcrow, crow.data(), crow.size() * 4);
   hup(dqrow, qrow.data(), qrow.size() * 4);
   hup(dtiles, tiles.data(), tiles.size() * 4); hup(dwitems, witems.data(), witems.size() * 4);
+  if (v.drQ > 0) {
+    hup((void*)v.drchunk, drch.data(), drch.size() * 4);
+    hup((void*)v.drkr, drkr.data(), drkr.size() * 4);
+    if (ce == cudaSuccess) ce = cudaMemset(v.drbar, 0, sizeof(unsigned long long));
+    if (ce == cudaSuccess) h->dr_loop_grid = dr_loop_grid(v);
+  }
   if (v.fused == 2) {
     hup(v.ttb, ttb.data(), ttb.size() * 4);
     hup(v.ktile0, ktile0.data(), (T + 1) * 4);
@@ -466,7 +489,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
   }
 
   cudaError_t ce = cudaSuccess;
-  auto timed = [&](int cls, cudaError_t (*fn)(nrto_handle_s*, cudaStream_t)) -> cudaError_t {
+  auto timed = [&](int cls, auto&& fn) -> cudaError_t {
     cudaEvent_t a = nullptr, b = nullptr;
     if (h->prof) { a = prof_event(h); b = prof_event(h); cudaEventRecord(a, st); }
     cudaError_t e = fn(h, st);
@@ -702,6 +725,8 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
         cudaError_t e = cudaSuccess;
         for (int l = 1; l <= prm.max_admm_iter && e == cudaSuccess; ++l) {
           e = launch_dr_arm(h, h->gst);
+          if (e == cudaSuccess && dr_loop_supported(h)) e = launch_dr_loop(h, prm.max_dr_iter, h->gst);
+          else
           for (int m = 1; m <= prm.max_dr_iter && e == cudaSuccess; ++m) {
             if (e == cudaSuccess) e = launch_dr_gain(h, h->gst);
             if (e == cudaSuccess) e = launch_dr_pass(h, h->gst);
@@ -730,6 +755,11 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     } else
     for (int l = 1; l <= prm.max_admm_iter; ++l) {
       CK(launch_dr_arm(h, st));
+      if (dr_loop_supported(h)) {
+        // one cooperative launch runs the whole DR loop (and its own stop test)
+        CK(timed(NRTO_K_PASS, [&](nrto_handle_s* hh, cudaStream_t s2) {
+          return launch_dr_loop(hh, prm.max_dr_iter, s2); }));
+      } else
       for (int m = 1; m <= prm.max_dr_iter; ++m) {
         CK(timed(NRTO_K_GAIN, launch_dr_gain));
         CK(timed(NRTO_K_PASS, launch_dr_pass));

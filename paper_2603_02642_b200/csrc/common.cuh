@@ -31,6 +31,10 @@ struct EngineFactors {
   double* AclT;  // [B][T][nx][nx]  its transpose (row i = column i of Acl_k)
   double* Hinv;  // [B][T][nu][nu]  H_uu^{-1}
   double* HB;    // [B][T][nu][nx]  H_uu^{-1} B_k^T
+  // chunked (parallel-in-time) recurrences of the QP (qp.cu k_qp_scan);
+  // nullptr for large batches.  Chunk c covers steps [c M, min(T, (c+1) M) - 1]:
+  double* PhiB;  // [B][T][nx][nx]  Acl_k^T Acl_{k+1}^T ... Acl_hi^T  (k in its chunk)
+  double* PhiF;  // [B][T][nx][nx]  Acl_k Acl_{k-1} ... Acl_lo
 };
 
 // Plain-old-data view of all device state, passed to kernels by value.
@@ -119,6 +123,15 @@ struct Dev {
   int32_t* clist;          // [B][ng] mispredicted cones of the last pass
   double* cw;              // [B][ng] their weights s^l - shat
   int32_t* ncorr;          // [B]
+  // persistent DR loop (persist.cu); drQ = 0: not used
+  int drQ;                 // cone chunks per instance
+  const int32_t* drchunk;  // [drQ + 1] first cone of each chunk
+  const int32_t* drkr;     // [drQ][2] steps [klo, khi) with b-blocks in the chunk
+  double* drZpart;         // [B][drQ][T][nu][nx] chunk adjoint partials
+  double* drrq;            // [B][drQ] chunk sums of ||s~^l - s~^{l-1}||^2
+  unsigned long long* drbar;   // grid-barrier counter (zeroed by k_dr_arm)
+  int drEc, drEBc;         // largest chunk: eta~ elements, b-row elements
+  int scanM, scanC;        // QP recurrence chunks: length M, count C (0: no scan QP)
 };
 
 }  // namespace nrto
@@ -188,6 +201,7 @@ struct nrto_handle_s {
   nrto::GenState gen;
   int inc_engine = -1;                      // incremental solve in progress (nrto_solve_begin)
   int inc_l = 0;                            // outer iterations run by it
+  int dr_loop_grid = 0;                     // persistent DR loop grid (0: not usable)
 };
 
 namespace nrto {
@@ -263,6 +277,46 @@ __device__ __forceinline__ double shat_of(const Dev& v, double sprev) {
   return (sprev == 1.0) ? 1.0 : 0.0;
 }
 
+// Gain chain solve for one (instance, step): K = V [(V^T R U) ./ den] U^T,
+// R given in sR (nu x nx).  Uses scratch sX (nu x nx); nt threads cooperate.
+template <int NXC = 0, int NUC = 0>
+__device__ __forceinline__ void chain_solve(const double* V, const double* U, const double* den,
+                                            double* sR, double* sX, int nu_rt, int nx_rt, int tid, int nt) {
+  const int nx = NXC > 0 ? NXC : nx_rt, nu = NUC > 0 ? NUC : nu_rt;
+  for (int r = tid; r < nu * nx; r += nt) {        // sX = V^T R
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < nu; ++q) acc += V[q * nu + a] * sR[q * nx + c];
+    sX[r] = acc;
+  }
+  __syncthreads();
+  for (int r = tid; r < nu * nx; r += nt) {        // sR = (sX U) ./ den
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[q * nx + c];
+    sR[r] = acc * den[r];
+  }
+  __syncthreads();
+  for (int r = tid; r < nu * nx; r += nt) {        // sX = V sR
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < nu; ++q) acc += V[a * nu + q] * sR[q * nx + c];
+    sX[r] = acc;
+  }
+  __syncthreads();
+  for (int r = tid; r < nu * nx; r += nt) {        // sR = sX U^T  (= K)
+    const int a = r / nx, c = r % nx;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[c * nx + q];
+    sR[r] = acc;
+  }
+  __syncthreads();
+}
+
 // Launchers (defined in the .cu files; return cudaGetLastError()).
 cudaError_t launch_setup(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_reset(nrto_handle_s* h, cudaStream_t st);
@@ -307,5 +361,15 @@ cudaError_t launch_setup_mma(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_fa_tma(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_project(nrto_handle_s* h, cudaStream_t st);
 cudaError_t launch_qp_sparse(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid = 0);
+// persistent DR loop (persist.cu)
+void dr_loop_plan(const Dims& d, const int32_t* knot, const int8_t* kind, int nsm,
+                  std::vector<int32_t>& chunk, std::vector<int32_t>& kr, int& Ec, int& EBc);
+int dr_loop_grid(const Dev& v);
+bool dr_loop_supported(const nrto_handle_s* h);
+cudaError_t launch_dr_loop(nrto_handle_s* h, int ndr, cudaStream_t st);
+// chunked-scan QP (qp.cu): used for batches up to kScanMaxBatch instances
+constexpr int kScanMaxBatch = 64;
+void scan_plan(int T, int& M, int& C);
+cudaError_t launch_scan_factors(nrto_handle_s* h, int engine, cudaStream_t st);
 
 }  // namespace nrto

@@ -92,46 +92,6 @@ __global__ void k_adjoint(Dev v, const double* __restrict__ y, const double* __r
   }
 }
 
-// Gain chain solve for one (instance, step): K = V [(V^T R U) ./ den] U^T,
-// R given in sR (nu x nx).  Uses scratch sX (nu x nx); nt threads cooperate.
-template <int NXC = 0, int NUC = 0>
-__device__ __forceinline__ void chain_solve(const double* V, const double* U, const double* den,
-                                            double* sR, double* sX, int nu_rt, int nx_rt, int tid, int nt) {
-  const int nx = NXC > 0 ? NXC : nx_rt, nu = NUC > 0 ? NUC : nu_rt;
-  for (int r = tid; r < nu * nx; r += nt) {        // sX = V^T R
-    const int a = r / nx, c = r % nx;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < nu; ++q) acc += V[q * nu + a] * sR[q * nx + c];
-    sX[r] = acc;
-  }
-  __syncthreads();
-  for (int r = tid; r < nu * nx; r += nt) {        // sR = (sX U) ./ den
-    const int a = r / nx, c = r % nx;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[q * nx + c];
-    sR[r] = acc * den[r];
-  }
-  __syncthreads();
-  for (int r = tid; r < nu * nx; r += nt) {        // sX = V sR
-    const int a = r / nx, c = r % nx;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < nu; ++q) acc += V[a * nu + q] * sR[q * nx + c];
-    sX[r] = acc;
-  }
-  __syncthreads();
-  for (int r = tid; r < nu * nx; r += nt) {        // sR = sX U^T  (= K)
-    const int a = r / nx, c = r % nx;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[c * nx + q];
-    sR[r] = acc;
-  }
-  __syncthreads();
-}
-
 // FullADMM (14b) per (instance, step k):
 //   R = 2 W K^{l-1} + rho sqrt(tau) (Z - Zb) Psi_k   (= block k of
 //   Q_v k^{l-1} + rho sum_j A_hat_j^T (nu_j - b_hat_j))

@@ -2,6 +2,8 @@
 // fused with the dual update and the residual / termination test of the outer
 // iteration: FullADMM (16) + P:505-507, or NRTO-ADMM (5c).
 #include "common.cuh"
+#include <cmath>
+#include <cstdlib>
 #include <algorithm>
 
 namespace nrto {
@@ -712,7 +714,7 @@ __device__ __forceinline__ void qp_wait(uint64_t* bar, uint32_t parity) {
 // NXM, NUM > 0: the exact n_x, n_u, fixed at compile time (shape-specialised
 // instances for the benchmark shapes: every small loop fully unrolled, loads
 // issued together); 0: runtime sizes.
-template <int NXM, int NUM>
+template <int NXM, int NUM, bool PIPE>
 __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int b, double* sm,
                                             double* red) {
   const Dims d = v.d;
@@ -768,7 +770,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
     __syncthreads();
     QP_CLK(1);
   }
-  if constexpr (NXM > 0) {
+  if constexpr (NXM > 0 && PIPE) {
     // ---- pipelined QP iteration (warp-specialised): warp 0 runs the two
     // Riccati recurrences; warps 1.. run every k-parallel phase BEHIND it, per knot,
     // synchronised by per-knot epoch flags in shared memory (membar.cta + volatile):
@@ -1287,15 +1289,359 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// Chunked-scan QP for small batches (parallel-in-time
+// Riccati).  Same OSQP iteration as qp_instance (R1, F4), but the two linear
+// recurrences of the Riccati x-step,
+//   s_k = a_k + Acl_k^T s_{k+1}   (backward)     dx_{k+1} = Acl_k dx_k + e_k   (forward),
+// are not run as 2T dependent steps on one warp.  The horizon is cut into C
+// chunks of M steps; each warp runs its chunk's recurrence from a zero boundary
+// (the last / first chunk from the exact s_T / dx_0 = 0), one warp chains the C
+// chunk boundaries with the transfer matrices of setup (k_scan_factors),
+//   s_lo = s~_lo + PhiB_lo s_{hi+1},     dx_{hi+1} = x~_{hi+1} + PhiF_hi dx_lo,
+// and every thread fixes up the interior steps in parallel.  Depth per sweep
+// M + C + 1 instead of T (T = 100: 10 + 10 + 1).  Everything k-parallel (a_k,
+// kff_k, e_k, du~_k, the rows, the ball) runs on all 512 threads between block
+// barriers; Acl of the horizon is staged in shared memory when it fits.
+void scan_plan(int T, int& M, int& C) {
+  int m = (int)std::ceil(std::sqrt((double)T));
+  int c = (T + m - 1) / m;
+  while (c > 16) { ++m; c = (T + m - 1) / m; }    // one warp per chunk (512 threads)
+  M = m; C = c;
+}
+
+__global__ void k_scan_factors(Dev v, int eng) {
+  extern __shared__ double sm[];
+  const Dims d = v.d;
+  const int nx = d.nx, T = d.T, M = v.scanM, C = v.scanC, nn = nx * nx;
+  const int b = blockIdx.x / C, c = blockIdx.x % C;
+  const int lo = c * M, hi = min(T, (c + 1) * M) - 1;
+  const EngineFactors& F = eng == 0 ? v.fa : v.dr;
+  const double* Acl = F.Acl + (int64_t)b * T * nn;
+  double* PB = F.PhiB + (int64_t)b * T * nn;
+  double* PF = F.PhiF + (int64_t)b * T * nn;
+  const int tid = threadIdx.x, i = tid / nx, j = tid % nx;
+  double* P = sm;
+  if (tid < nn) { P[tid] = Acl[(int64_t)hi * nn + j * nx + i]; PB[(int64_t)hi * nn + tid] = P[tid]; }
+  __syncthreads();
+  for (int k = hi - 1; k >= lo; --k) {            // PhiB_k = Acl_k^T PhiB_{k+1}
+    double acc = 0.0;
+    if (tid < nn)
+      for (int r = 0; r < nx; ++r) acc += Acl[(int64_t)k * nn + r * nx + i] * P[r * nx + j];
+    __syncthreads();
+    if (tid < nn) { P[tid] = acc; PB[(int64_t)k * nn + tid] = acc; }
+    __syncthreads();
+  }
+  if (tid < nn) { P[tid] = Acl[(int64_t)lo * nn + tid]; PF[(int64_t)lo * nn + tid] = P[tid]; }
+  __syncthreads();
+  for (int k = lo + 1; k <= hi; ++k) {            // PhiF_k = Acl_k PhiF_{k-1}
+    double acc = 0.0;
+    if (tid < nn)
+      for (int r = 0; r < nx; ++r) acc += Acl[(int64_t)k * nn + i * nx + r] * P[r * nx + j];
+    __syncthreads();
+    if (tid < nn) { P[tid] = acc; PF[(int64_t)k * nn + tid] = acc; }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_scan_factors(nrto_handle_s* h, int engine, cudaStream_t st) {
+  const Dev& v = h->dev;
+  const int nn = v.d.nx * v.d.nx;
+  k_scan_factors<<<v.d.B * v.scanC, (nn + 31) / 32 * 32, nn * sizeof(double), st>>>(v, engine);
+  h->launches++;
+  return cudaGetLastError();
+}
+
+// One step of a warp recurrence: lane i < nx returns base_i + sum_r Mat(i, r) x_r,
+// x held one element per lane.
+template <int NXM, class MF>
+__device__ __forceinline__ double scan_step(int nx, int lane, double base, double x, MF mat) {
+  double c0 = base, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+  const int ic = lane < nx ? lane : 0;
+  constexpr int NR = NXM > 0 ? NXM : 32;
+#pragma unroll
+  for (int r = 0; r < NR; r += 4) {
+    // every lane runs the same shuffles (uniform call site, full mask)
+    const double x0 = __shfl_sync(0xffffffffu, x, r + 0);
+    const double x1 = __shfl_sync(0xffffffffu, x, (r + 1) & 31);
+    const double x2 = __shfl_sync(0xffffffffu, x, (r + 2) & 31);
+    const double x3 = __shfl_sync(0xffffffffu, x, (r + 3) & 31);
+    if (r + 0 < nx) c0 = fma(mat(ic, r + 0), x0, c0);
+    if (r + 1 < nx) c1 = fma(mat(ic, r + 1), x1, c1);
+    if (r + 2 < nx) c2 = fma(mat(ic, r + 2), x2, c2);
+    if (r + 3 < nx) c3 = fma(mat(ic, r + 3), x3, c3);
+    if (NXM == 0 && r + 4 >= nx) break;
+  }
+  return (c0 + c1) + (c2 + c3);
+}
+
+static size_t scan_smem(const Dims& d, int C, int stageA) {
+  return ((size_t)(d.T + 1) * d.nx + (size_t)d.T * d.nx + 2 * (size_t)d.T * d.nu +
+          2 * (size_t)C * d.nx * d.nx + (stageA ? (size_t)d.T * d.nx * d.nx : 0)) * sizeof(double);
+}
+
+template <int NXM, int NUM>
+__global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, int stageA) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const Dims d = v.d;
+  const int nx = NXM > 0 ? NXM : d.nx, nu = NUM > 0 ? NUM : d.nu, T = d.T, ng = d.ng;
+  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int M = v.scanM, C = v.scanC, nn = nx * nx;
+  if (!v.active[b]) return;
+  const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
+  const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
+  const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp, aq = v.prm.alpha_qp;
+  const double den = rho + sq + rq, beta = rq / den;
+  const int64_t bg = (int64_t)b * ng;
+  const double* __restrict__ grad = v.grad + bg * nx;
+  const double* __restrict__ g0 = v.g0 + bg;
+  double* p = v.p + bg; double* zl = v.zl + bg; double* yl = v.yl + bg;
+  double* rp = v.rp + bg;
+  const double* pt = v.pt + bg; double* lam = v.lamp + bg;
+  double* zb = v.zb + (int64_t)b * (T + 1) * nx; double* yb = v.yb + (int64_t)b * (T + 1) * nx;
+  double* du = v.du + (int64_t)b * T * nu;
+  double* gS = v.rx + (int64_t)b * (T + 1) * nx;      // S_k = sum_{state j@k} w_j grad_j (atomic)
+  double* gU = v.dut + (int64_t)b * T * nu;           // U_k = sum_{ctrl j@k} w_j h'_j   (atomic)
+  const double* __restrict__ cu2 = v.cu2 + (int64_t)b * T * nu;
+  const double* __restrict__ Bm = v.Bm + (int64_t)b * T * nx * nu;
+  const double* __restrict__ Kf = F.Kf + (int64_t)b * T * nu * nx;
+  const double* __restrict__ AclG = F.Acl + (int64_t)b * T * nn;
+  const double* __restrict__ Hi = F.Hinv + (int64_t)b * T * nu * nu;
+  const double* __restrict__ HB = F.HB + (int64_t)b * T * nu * nx;
+  const double* __restrict__ PBg = F.PhiB + (int64_t)b * T * nn;
+  const double* __restrict__ PFg = F.PhiF + (int64_t)b * T * nn;
+  const double rtr = v.rtrust[b];
+  const double rinv = (engine == NRTO_FULLADMM) ? 1.0 : 1.0 / rho;
+  double* sS = sm;                          // [(T+1) nx]  s~/s, then dx~/dx, then z^_ball
+  double* sA = sS + (T + 1) * nx;           // [T nx]      a_k, then e_k
+  double* sR = sA + T * nx;                 // [T nu]      r_u,k, then du~_k
+  double* sK = sR + T * nu;                 // [T nu]      kff_k
+  double* sPb = sK + T * nu;                // [C][nx][nx] PhiB at chunk starts
+  double* sPf = sPb + C * nn;               // [C][nx][nx] PhiF at chunk ends
+  double* sAcl = sPf + C * nn;              // [T][nx][nx] (stageA)
+  const double* Acl = stageA ? sAcl : AclG;
+  if (stageA)
+    for (int r = tid; r < T * nn; r += nt) sAcl[r] = AclG[r];
+  for (int r = tid; r < C * nn; r += nt) {
+    const int c = r / nn, e = r - c * nn;
+    sPb[r] = PBg[(int64_t)(c * M) * nn + e];
+    sPf[r] = PFg[(int64_t)(min(T, (c + 1) * M) - 1) * nn + e];
+  }
+  for (int r = tid; r < (T + 1) * nx; r += nt) gS[r] = 0.0;
+  for (int r = tid; r < T * nu; r += nt) gU[r] = 0.0;
+  __syncthreads();
+  const int nits = v.prm.qp_iters;
+  if (nits > 0) {                                     // rhs / w / scatter of iteration 0
+    qp_rows<true, kRowBatch>(v, bg, ng, tid, nt, grad, g0, p, zl, yl, rp, pt, lam, sS, sR, gS, gU, true,
+                             rho, rq, sq, aq, den, beta, rinv);
+    __syncthreads();
+  }
+  for (int it = 0; it < nits; ++it) {
+    for (int r = tid; r < T * nu; r += nt) {          // r_u (consumes and clears U)
+      sR[r] = sq * du[r] + __ldcg(gU + r) + cu2[r];   // cu2 = -2 R_u u_hat (setup)
+      gU[r] = 0.0;
+    }
+    __syncthreads();
+    for (int r = tid; r < (T + 1) * nx; r += nt) {    // r_x and a_k (consumes and clears S)
+      const int k = r / nx, i = r - k * nx;
+      double acc = (k > 0) ? __ldcg(gS + r) + rq * zb[r] - yb[r] : 0.0;
+      gS[r] = 0.0;
+      if (k < T) {
+        const double* Kk = Kf + (int64_t)k * nu * nx + i;
+        const double* rk = sR + k * nu;
+        acc -= dotn<NUM>(nu, [&](int m) { return Kk[m * nx]; }, [&](int m) { return rk[m]; }, 0.0);
+      }
+      sS[r] = acc;        // a_k (k < T), s_T
+    }
+    __syncthreads();
+    if (warp < C) {                                   // chunk-local backward recurrences
+      const int lo = warp * M, hi = min(T, (warp + 1) * M) - 1;
+      double x = (warp == C - 1 && lane < nx) ? sS[T * nx + lane] : 0.0;
+      for (int k = hi; k >= lo; --k) {
+        const double* Ak = Acl + (size_t)k * nn;
+        const double base = lane < nx ? sS[k * nx + lane] : 0.0;
+        x = scan_step<NXM>(nx, lane, base, x, [&](int i, int r) { return Ak[r * nx + i]; });
+        if (lane < nx) sS[k * nx + lane] = x;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {                                  // chunk boundaries, last to first
+      double x = lane < nx ? sS[(C - 1) * M * nx + lane] : 0.0;
+      for (int c = C - 2; c >= 0; --c) {
+        const double* P = sPb + c * nn;
+        const double base = lane < nx ? sS[c * M * nx + lane] : 0.0;
+        x = scan_step<NXM>(nx, lane, base, x, [&](int i, int r) { return P[i * nx + r]; });
+        if (lane < nx) sS[c * M * nx + lane] = x;
+      }
+    }
+    __syncthreads();
+    // interior fix-up s_k += PhiB_k s_{hi+1} (reads only chunk-start slots, which it
+    // does not write)
+    for (int r = tid; r < T * nx; r += nt) {
+      const int k = r / nx, i = r - k * nx, c = k / M;
+      if (c == C - 1 || k == c * M) continue;
+      const double* Pk = PBg + (int64_t)k * nn + i * nx;
+      const double* sn = sS + (c + 1) * M * nx;
+      sS[r] += dotn<NXM>(nx, [&](int q) { return Pk[q]; }, [&](int q) { return sn[q]; }, 0.0);
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nu; r += nt) {          // kff_k = H^-1 r_u,k + H^-1 B_k^T s_{k+1}
+      const int k = r / nu, m = r - k * nu;
+      const double* H = Hi + (int64_t)k * nu * nu + m * nu;
+      const double* hb = HB + (int64_t)k * nu * nx + m * nx;
+      const double* rk = sR + k * nu;
+      const double* sk = sS + (k + 1) * nx;
+      double acc = dotn<NUM>(nu, [&](int q) { return H[q]; }, [&](int q) { return rk[q]; }, 0.0);
+      acc = dotn<NXM>(nx, [&](int q) { return hb[q]; }, [&](int q) { return sk[q]; }, acc);
+      sK[r] = acc;
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nx; r += nt) {          // e_k = B_k kff_k
+      const int k = r / nx, i = r - k * nx;
+      const double* Bk = Bm + (int64_t)k * nx * nu + i * nu;
+      const double* kk = sK + k * nu;
+      sA[r] = dotn<NUM>(nu, [&](int m) { return Bk[m]; }, [&](int m) { return kk[m]; }, 0.0);
+    }
+    __syncthreads();
+    if (warp < C) {                                   // chunk-local forward recurrences
+      const int lo = warp * M, hi = min(T, (warp + 1) * M) - 1;
+      if (warp == 0 && lane < nx) sS[lane] = 0.0;     // dx_0 = 0
+      double x = 0.0;
+      for (int k = lo; k <= hi; ++k) {
+        const double* Ak = Acl + (size_t)k * nn;
+        const double base = lane < nx ? sA[k * nx + lane] : 0.0;
+        x = scan_step<NXM>(nx, lane, base, x, [&](int i, int r) { return Ak[i * nx + r]; });
+        if (lane < nx) sS[(k + 1) * nx + lane] = x;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {                                  // chunk boundaries, first to last
+      double x = lane < nx ? sS[min(T, M) * nx + lane] : 0.0;
+      for (int c = 1; c < C; ++c) {
+        const int hi = min(T, (c + 1) * M) - 1;
+        const double* P = sPf + c * nn;
+        const double base = lane < nx ? sS[(hi + 1) * nx + lane] : 0.0;
+        x = scan_step<NXM>(nx, lane, base, x, [&](int i, int r) { return P[i * nx + r]; });
+        if (lane < nx) sS[(hi + 1) * nx + lane] = x;
+      }
+    }
+    __syncthreads();
+    // interior fix-up dx_{k+1} += PhiF_k dx_lo (reads only chunk-start slots lo_c,
+    // writes lo_c + 1 .. hi_c)
+    for (int r = tid; r < T * nx; r += nt) {
+      const int k = r / nx, i = r - k * nx, c = k / M;
+      const int hi = min(T, (c + 1) * M) - 1;
+      if (c == 0 || k == hi) continue;
+      const double* Pk = PFg + (int64_t)k * nn + i * nx;
+      const double* xl = sS + c * M * nx;
+      sS[r + nx] += dotn<NXM>(nx, [&](int q) { return Pk[q]; }, [&](int q) { return xl[q]; }, 0.0);
+    }
+    __syncthreads();
+    for (int r = tid; r < T * nu; r += nt) {          // du~_k = kff_k - Kf_k dx_k ; relaxed du
+      const int k = r / nu, m = r - k * nu;
+      const double* Kk = Kf + (int64_t)k * nu * nx + m * nx;
+      const double* xk = sS + k * nx;
+      const double dd = sK[r] - dotn<NXM>(nx, [&](int q) { return Kk[q]; }, [&](int q) { return xk[q]; }, 0.0);
+      sR[r] = dd;
+      du[r] = aq * dd + (1.0 - aq) * du[r];
+    }
+    __syncthreads();
+    const bool more = it + 1 < nits;
+    qp_rows<false, kRowBatch>(v, bg, ng, tid, nt, grad, g0, p, zl, yl, rp, pt, lam, sS, sR, gS, gU, more,
+                              rho, rq, sq, aq, den, beta, rinv);
+    __syncthreads();
+    double nb = 0.0;                                  // trust-region ball
+    for (int r = tid; r < (T + 1) * nx; r += nt) {
+      const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
+      sS[r] = zh;
+      const double w = zh + yb[r] / rq;
+      nb += w * w;
+    }
+    nb = sqrt(block_sum(nb, red));
+    const double scl = (nb > rtr) ? rtr / nb : 1.0;
+    for (int r = tid; r < (T + 1) * nx; r += nt) {
+      const double zh = sS[r];
+      const double zn = scl * (zh + yb[r] / rq);
+      yb[r] += rq * (zh - zn);
+      zb[r] = zn;
+    }
+    __syncthreads();
+  }
+  double ap = 0.0, ad = 0.0;
+  double* tin = v.tin + bg;
+  double* ptp = v.ptprev + bg;
+  for (int j = tid; j < ng; j += nt) {
+    const double dp = p[j] - pt[j];
+    if (engine == NRTO_FULLADMM) {
+      lam[j] += dp;
+      tin[j] = p[j] + lam[j];
+    } else {
+      lam[j] += rho * dp;
+    }
+    ap += dp * dp;
+    const double dd = pt[j] - ptp[j];
+    ad += dd * dd;
+    ptp[j] = pt[j];
+  }
+  ap = block_sum(ap, red);
+  ad = block_sum(ad, red);
+  if (tid == 0) {
+    const double rpv = sqrt(ap), rdv = rho * sqrt(ad);
+    v.r_p[b] = rpv;
+    v.r_d[b] = rdv;
+    record_hist(v, b, l, rpv, rdv, engine);
+    v.iters[b] = l;
+    if (!isfinite(rpv) || !isfinite(rdv)) {
+      v.status[b] = NRTO_DIVERGED;
+      v.active[b] = 0;
+    } else if (!v.prm.fixed_iters && (l % v.prm.check_every) == 0 && rpv <= v.prm.eps_p &&
+               rdv <= v.prm.eps_d) {
+      v.status[b] = NRTO_CONVERGED;
+      v.active[b] = 0;
+    }
+  }
+}
+
+// Chunked-scan QP usable for this launch (grid 0 / >= B: one CTA per instance).
+static int scan_stage(const nrto_handle_s* h, int grid) {
+  const Dev& v = h->dev;
+  static const int env = [] { const char* e = getenv("NRTO_QP_SCAN"); return e ? atoi(e) : 1; }();
+  if (!env || v.scanC <= 0 || !v.fa.PhiB || v.d.B > kScanMaxBatch) return -1;
+  if (grid > 0 && grid < v.d.B) return -1;
+  const size_t lim = 220 * 1024;
+  if (scan_smem(v.d, v.scanC, 1) <= lim) return 1;
+  if (scan_smem(v.d, v.scanC, 0) <= lim) return 0;
+  return -1;
+}
+
+static cudaError_t launch_qp_scan(nrto_handle_s* h, int engine, int l, int stageA, cudaStream_t st) {
+  const Dims& d = h->dev.d;
+  const size_t smem = scan_smem(d, h->dev.scanC, stageA);
+  void* kern;
+  if (d.nx == 14 && d.nu == 7) kern = (void*)k_qp_scan<14, 7>;
+  else if (d.nx == 12 && d.nu == 4) kern = (void*)k_qp_scan<12, 4>;
+  else if (d.nx == 3 && d.nu == 2) kern = (void*)k_qp_scan<3, 2>;
+  else kern = (void*)k_qp_scan<0, 0>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (d.nx == 14 && d.nu == 7) k_qp_scan<14, 7><<<d.B, 512, smem, st>>>(h->dev, engine, l, stageA);
+  else if (d.nx == 12 && d.nu == 4) k_qp_scan<12, 4><<<d.B, 512, smem, st>>>(h->dev, engine, l, stageA);
+  else if (d.nx == 3 && d.nu == 2) k_qp_scan<3, 2><<<d.B, 512, smem, st>>>(h->dev, engine, l, stageA);
+  else k_qp_scan<0, 0><<<d.B, 512, smem, st>>>(h->dev, engine, l, stageA);
+  h->launches++;
+  return cudaGetLastError();
+}
+
 // One CTA per instance (grid = B, all resident: in-order schedule) or a
 // persistent grid looping over instances (overlapped schedule: one QP CTA per SM
 // beside the cone pass, so the QP never holds more than that share of the SMs).
-template <int NXM, int NUM>
+template <int NXM, int NUM, bool PIPE>
 __global__ void __launch_bounds__(QP_THREADS, QP_MINB) k_qp_sparse(Dev v, int engine, int l) {
   extern __shared__ double sm[];
   __shared__ double red[32];
   for (int b = blockIdx.x; b < v.d.B; b += gridDim.x) {
-    qp_instance<NXM, NUM>(v, engine, l, b, sm, red);
+    qp_instance<NXM, NUM, PIPE>(v, engine, l, b, sm, red);
     __syncthreads();
   }
 }
@@ -1358,14 +1704,27 @@ cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
 
 cudaError_t launch_qp_sparse(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid) {
   const Dims& d = h->dev.d;
+  { const int sa = scan_stage(h, grid); if (sa >= 0) return launch_qp_scan(h, engine, l, sa, st); }
   const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx + kQPRing) * sizeof(double) +
                       (size_t)6 * (d.T + 1) * sizeof(int16_t);
   if (smem > 48 * 1024 || h->dev.prm.qp_iters > 32000) return launch_qp(h, engine, l, st);
   if (d.nx <= 127) {
     const int g = (grid > 0 && grid < d.B) ? grid : d.B;
-    if (d.nx == 14 && d.nu == 7) k_qp_sparse<14, 7><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
-    else if (d.nx == 12 && d.nu == 4) k_qp_sparse<12, 4><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
-    else k_qp_sparse<0, 0><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
+    // warp-specialised pipelined iteration (PIPE) or the phase-synchronous one with
+    // the bulk-copy recurrence ring; NRTO_QP_PIPE: 0 never, 1 always, 2 (default) only
+    // for in-order launches (one CTA per instance) -- beside the cone pass the pipelined
+    // variant's spinning helper warps take issue slots from the pass
+    static const int pipe_env = [] { const char* e = getenv("NRTO_QP_PIPE"); return e ? atoi(e) : 2; }();
+    const bool pipe = pipe_env == 1 || (pipe_env == 2 && g >= d.B);
+    if (d.nx == 14 && d.nu == 7) {
+      if (pipe) k_qp_sparse<14, 7, true><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
+      else k_qp_sparse<14, 7, false><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
+    } else if (d.nx == 12 && d.nu == 4) {
+      if (pipe) k_qp_sparse<12, 4, true><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
+      else k_qp_sparse<12, 4, false><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
+    } else {
+      k_qp_sparse<0, 0, false><<<g, QP_THREADS, smem, st>>>(h->dev, engine, l);
+    }
     h->launches++;
     return cudaGetLastError();
   }
@@ -1379,6 +1738,7 @@ static size_t qp_smem(const Dims& d, int stageA) {
 
 cudaError_t launch_qp(nrto_handle_s* h, int engine, int l, cudaStream_t st) {
   const Dims& d = h->dev.d;
+  { const int sa = scan_stage(h, 0); if (sa >= 0) return launch_qp_scan(h, engine, l, sa, st); }
   const size_t lim = 200 * 1024;
   int stageA = qp_smem(d, 1) <= lim;
   if (stageA || qp_smem(d, 0) <= lim) {
@@ -1411,6 +1771,7 @@ __global__ void k_reset_inst(Dev v, int engine) {
 __global__ void k_dr_arm(Dev v) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < v.d.B) v.dr_active[b] = v.active[b];
+  if (b == 0 && v.drbar) *v.drbar = 0ULL;    // grid barrier of the persistent DR loop
 }
 
 static cudaError_t zero(nrto_handle_s* h, double* p, int64_t n, cudaStream_t st) {

@@ -473,6 +473,7 @@ cudaError_t launch_engine_factors(nrto_handle_s* h, int engine, cudaStream_t st)
   const int rs = 3 * d.nx * d.nx + 2 * d.nx * d.nu + 3 * d.nu * d.nu + 2 * d.nu * d.nx;
   k_riccati<<<d.B, 128, rs * sizeof(double), st>>>(v, engine);
   h->launches++;
+  if (v.scanC > 0) return launch_scan_factors(h, engine, st);
   return cudaGetLastError();
 }
 

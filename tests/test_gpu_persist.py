@@ -1,0 +1,115 @@
+"""GPU: the single-instance paths of SURVEY §8f NEXT-3 against the oracle and
+against the kernels they replace (switched off by environment in a child
+process): the persistent single-launch DR loop (csrc/persist.cu, NEXT-3(ii),
+NRTO_DR_PERSIST=0) and the chunked-scan (parallel-in-time) Riccati QP
+(csrc/qp.cu k_qp_scan, NEXT-3(iii), NRTO_QP_SCAN=0)."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from gen import stack_instances
+from gen.problems import make_quad, make_unicycle
+from tests.helpers import close
+from tests.test_gpu_parity import CASES, assert_parity, gpu_solve, oracle_run, single
+
+from paper_2603_02642_b200 import nrto
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np, torch
+from tests.test_gpu_parity import CASES, single
+from paper_2603_02642_b200 import nrto
+case, eng = sys.argv[1], int(sys.argv[2])
+shape, data = CASES[case]()
+kw = dict(max_admm_iter=3, max_dr_iter=12, fixed_iters=1) if eng else dict(max_iter=12, fixed_iters=1)
+s = nrto.InnerSolver(shape, nrto.to_tensors(single(shape, data), device="cuda"), **kw)
+o = nrto.alloc_out(shape, 1, s.E, device="cuda")
+res = []
+for _ in range(2):                      # second solve: warm DR state (P:1340)
+    s.solve(eng, out=o)
+    torch.cuda.synchronize()
+    res.append({k: o[k].cpu().numpy().ravel().tolist() for k in ("kv", "du", "p", "p_tilde", "lam_p")})
+print(json.dumps(res))
+"""
+
+
+def _run_child(case, eng, **env_kw):
+    env = dict(os.environ, **{k: str(v) for k, v in env_kw.items()})
+    r = subprocess.run([sys.executable, "-c", CHILD % ROOT, case, str(eng)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_persistent_dr_matches_launch_per_phase_path():
+    """Same warm-started c2 solves (two calls) through both DR implementations."""
+    a = _run_child("c2", 1, NRTO_DR_PERSIST=1)
+    b = _run_child("c2", 1, NRTO_DR_PERSIST=0, NRTO_QP_SCAN=1)
+    for sa, sb in zip(a, b):
+        for k in sa:
+            assert close(np.array(sa[k]), np.array(sb[k]), tol=1e-11), k
+
+
+def test_persistent_dr_batch_ragged_instances():
+    """A batch of 5 quadcopters (persistent path, several instances share the grid:
+    item and task loops wrap) matches the oracle instance by instance."""
+    items = [make_quad(2, i, T=16, n_obs=4) for i in range(5)]
+    shape, batch = stack_instances(items)
+    kw = dict(max_admm_iter=3, max_dr_iter=9, fixed_iters=1)
+    g = gpu_solve(shape, batch, nrto.NRTO_DR, **kw)
+    for i, (_, d) in enumerate(items):
+        o = oracle_run(shape, d, nrto.NRTO_DR, **kw)
+        assert_parity(g, o, i=i, engine=1)
+
+
+def test_persistent_dr_early_stop_per_instance():
+    """DR stop test inside the persistent loop (every CTA derives r_dr itself):
+    instances stop their DR loops at different iterations, as in the oracle."""
+    items = [make_unicycle(1, i) for i in range(4)]
+    shape, batch = stack_instances(items)
+    kw = dict(max_admm_iter=6, max_dr_iter=60, eps_dr=1e-5, eps_p=1e-7, eps_d=1e-7)
+    g = gpu_solve(shape, batch, nrto.NRTO_DR, **kw)
+    for i, (_, d) in enumerate(items):
+        o = oracle_run(shape, d, nrto.NRTO_DR, **kw)
+        assert_parity(g, o, i=i, engine=1)
+
+
+def test_persistent_dr_zero_dr_iterations():
+    """max_dr_iter = 0: the loop runs no pass; the solve still matches the oracle."""
+    shape, data = CASES["c1"]()
+    kw = dict(max_admm_iter=2, max_dr_iter=0, fixed_iters=1)
+    g = gpu_solve(shape, single(shape, data), nrto.NRTO_DR, **kw)
+    o = oracle_run(shape, data, nrto.NRTO_DR, **kw)
+    assert_parity(g, o, engine=1)
+
+
+@pytest.mark.parametrize("case,eng", [("c1", 0), ("c3s", 0), ("c2", 0), ("c2", 1)])
+def test_scan_qp_matches_sequential_recurrences(case, eng):
+    """The chunked-scan QP against the sequential-recurrence QP kernels (staged /
+    pipelined sparse) on the same solves: reassociated sums only."""
+    a = _run_child(case, eng, NRTO_QP_SCAN=1)
+    b = _run_child(case, eng, NRTO_QP_SCAN=0)
+    for sa, sb in zip(a, b):
+        for k in sa:
+            assert close(np.array(sa[k]), np.array(sb[k]), tol=1e-10), (case, eng, k)
+
+
+def test_scan_qp_long_horizon_chunks():
+    """T = 200 (chunks of 15 steps, 14 chunks) and T = 7 (chunks of 3): the scan
+    QP inside FullADMM matches the oracle."""
+    from gen.problems import make_quad
+    for T in (7, 200):
+        shape, data = make_quad(4, 1, T=T, n_obs=3)
+        g = gpu_solve(shape, single(shape, data), nrto.NRTO_FULLADMM, max_iter=6, fixed_iters=1)
+        o = oracle_run(shape, data, nrto.NRTO_FULLADMM, max_iter=6, fixed_iters=1)
+        assert_parity(g, o)
