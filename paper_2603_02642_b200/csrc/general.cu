@@ -460,3 +460,26 @@ void gen_free(nrto_handle_s* h) {
 }
 
 }  // namespace nrto
+
+// Debug copy of internal general-set arrays to caller memory (not part of nrto.h):
+// which = 0 W [B][n_z][NX], 1 b_hat [B][n_g][n_z], 2 L [B][NK][NK], 3 ragged costates
+// (v.bhat) [B][E], 4 ragged b rows (v.Bd) [B][EB], 5 dense M^-1 rebuilt into dst.
+extern "C" int nrto_debug_gen_copy(nrto_handle h, int which, double* dst, int64_t n) {
+  using namespace nrto;
+  const GenState& g = h->gen;
+  const Dev& v = h->dev;
+  const double* src = nullptr;
+  int64_t avail = 0;
+  const int64_t B = v.d.B, NX = (int64_t)(v.d.T + 1) * v.d.nx, NK = v.d.NK;
+  switch (which) {
+    case 0: src = g.W; avail = B * g.nz * NX; break;
+    case 1: src = g.Bh; avail = B * v.d.ng * g.nz; break;
+    case 2: src = g.L; avail = B * NK * NK; break;
+    case 3: src = v.bhat; avail = B * v.d.E; break;
+    case 4: src = v.Bd; avail = B * v.d.EB; break;
+    default: return -1;
+  }
+  if (!src || n > avail) return -2;
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpy(dst, src, (size_t)n * 8, cudaMemcpyDeviceToHost);
+}

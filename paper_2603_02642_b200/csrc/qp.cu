@@ -1353,24 +1353,32 @@ cudaError_t launch_scan_factors(nrto_handle_s* h, int engine, cudaStream_t st) {
 }
 
 // One step of a warp recurrence: lane i < nx returns base_i + sum_r Mat(i, r) x_r,
-// x held one element per lane.
+// x in shared memory (broadcast reads; LDS.128 pairs when n_x is a compile-time
+// even number), four independent FMA chains.
 template <int NXM, class MF>
-__device__ __forceinline__ double scan_step(int nx, int lane, double base, double x, MF mat) {
+__device__ __forceinline__ double scan_step(int nx, int lane, double base, const double* x, MF mat) {
   double c0 = base, c1 = 0.0, c2 = 0.0, c3 = 0.0;
   const int ic = lane < nx ? lane : 0;
-  constexpr int NR = NXM > 0 ? NXM : 32;
+  if constexpr (NXM > 0 && (NXM % 2) == 0) {
 #pragma unroll
-  for (int r = 0; r < NR; r += 4) {
-    // every lane runs the same shuffles (uniform call site, full mask)
-    const double x0 = __shfl_sync(0xffffffffu, x, r + 0);
-    const double x1 = __shfl_sync(0xffffffffu, x, (r + 1) & 31);
-    const double x2 = __shfl_sync(0xffffffffu, x, (r + 2) & 31);
-    const double x3 = __shfl_sync(0xffffffffu, x, (r + 3) & 31);
-    if (r + 0 < nx) c0 = fma(mat(ic, r + 0), x0, c0);
-    if (r + 1 < nx) c1 = fma(mat(ic, r + 1), x1, c1);
-    if (r + 2 < nx) c2 = fma(mat(ic, r + 2), x2, c2);
-    if (r + 3 < nx) c3 = fma(mat(ic, r + 3), x3, c3);
-    if (NXM == 0 && r + 4 >= nx) break;
+    for (int r = 0; r < NXM; r += 2) {
+      const double2 xx = *reinterpret_cast<const double2*>(x + r);
+      if ((r >> 1) & 1) { c2 = fma(mat(ic, r), xx.x, c2); c3 = fma(mat(ic, r + 1), xx.y, c3); }
+      else { c0 = fma(mat(ic, r), xx.x, c0); c1 = fma(mat(ic, r + 1), xx.y, c1); }
+    }
+  } else {
+    constexpr int NR = NXM > 0 ? NXM : 32;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      if (r >= nx) break;
+      const double t = mat(ic, r);
+      switch (r & 3) {
+        case 0: c0 = fma(t, x[r], c0); break;
+        case 1: c1 = fma(t, x[r], c1); break;
+        case 2: c2 = fma(t, x[r], c2); break;
+        default: c3 = fma(t, x[r], c3); break;
+      }
+    }
   }
   return (c0 + c1) + (c2 + c3);
 }
@@ -1458,22 +1466,29 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
     __syncthreads();
     if (warp < C) {                                   // chunk-local backward recurrences
       const int lo = warp * M, hi = min(T, (warp + 1) * M) - 1;
-      double x = (warp == C - 1 && lane < nx) ? sS[T * nx + lane] : 0.0;
       for (int k = hi; k >= lo; --k) {
         const double* Ak = Acl + (size_t)k * nn;
         const double base = lane < nx ? sS[k * nx + lane] : 0.0;
-        x = scan_step<NXM>(nx, lane, base, x, [&](int i, int r) { return Ak[r * nx + i]; });
+        // s~_{hi+1} = 0 for all but the last chunk (which starts from the exact s_T)
+        const double x = (k == hi && warp != C - 1)
+                             ? base
+                             : scan_step<NXM>(nx, lane, base, sS + (k + 1) * nx,
+                                              [&](int i, int r) { return Ak[r * nx + i]; });
+        __syncwarp();
         if (lane < nx) sS[k * nx + lane] = x;
+        __syncwarp();
       }
     }
     __syncthreads();
     if (warp == 0) {                                  // chunk boundaries, last to first
-      double x = lane < nx ? sS[(C - 1) * M * nx + lane] : 0.0;
       for (int c = C - 2; c >= 0; --c) {
         const double* P = sPb + c * nn;
         const double base = lane < nx ? sS[c * M * nx + lane] : 0.0;
-        x = scan_step<NXM>(nx, lane, base, x, [&](int i, int r) { return P[i * nx + r]; });
+        const double x = scan_step<NXM>(nx, lane, base, sS + (c + 1) * M * nx,
+                                        [&](int i, int r) { return P[i * nx + r]; });
+        __syncwarp();
         if (lane < nx) sS[c * M * nx + lane] = x;
+        __syncwarp();
       }
     }
     __syncthreads();
@@ -1508,23 +1523,28 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
     if (warp < C) {                                   // chunk-local forward recurrences
       const int lo = warp * M, hi = min(T, (warp + 1) * M) - 1;
       if (warp == 0 && lane < nx) sS[lane] = 0.0;     // dx_0 = 0
-      double x = 0.0;
       for (int k = lo; k <= hi; ++k) {
         const double* Ak = Acl + (size_t)k * nn;
         const double base = lane < nx ? sA[k * nx + lane] : 0.0;
-        x = scan_step<NXM>(nx, lane, base, x, [&](int i, int r) { return Ak[i * nx + r]; });
+        // x~_lo = 0 (slot lo belongs to the previous chunk's warp)
+        const double x = (k == lo) ? base
+                                   : scan_step<NXM>(nx, lane, base, sS + k * nx,
+                                                    [&](int i, int r) { return Ak[i * nx + r]; });
         if (lane < nx) sS[(k + 1) * nx + lane] = x;
+        __syncwarp();
       }
     }
     __syncthreads();
     if (warp == 0) {                                  // chunk boundaries, first to last
-      double x = lane < nx ? sS[min(T, M) * nx + lane] : 0.0;
       for (int c = 1; c < C; ++c) {
         const int hi = min(T, (c + 1) * M) - 1;
         const double* P = sPf + c * nn;
         const double base = lane < nx ? sS[(hi + 1) * nx + lane] : 0.0;
-        x = scan_step<NXM>(nx, lane, base, x, [&](int i, int r) { return P[i * nx + r]; });
+        const double x = scan_step<NXM>(nx, lane, base, sS + c * M * nx,
+                                        [&](int i, int r) { return P[i * nx + r]; });
+        __syncwarp();
         if (lane < nx) sS[(hi + 1) * nx + lane] = x;
+        __syncwarp();
       }
     }
     __syncthreads();

@@ -147,6 +147,11 @@ def nrto_layout(shape, batch=1):
 def _ptr(t):
     if t is None:
         return None
+    if not t.is_contiguous():
+        # the C ABI reads plain row-major arrays: a strided view (e.g. a transposed
+        # numpy array wrapped by torch.tensor, which keeps its strides) would be read
+        # in storage order
+        raise ValueError("nrto: array arguments must be contiguous (row-major)")
     return C.c_void_p(t.data_ptr())
 
 
@@ -193,6 +198,7 @@ def nrto_setup_general(shape, data: dict, Gamma, Psi, params: nrto_params, strea
     batch = int(data["tau"].shape[0])
     s = _shape_struct(shape, batch)
     dd = nrto_data(memory, *[_ptr(data[k]) for k in DATA_KEYS])
+    Gamma, Psi = Gamma.contiguous(), Psi.contiguous()
     un = nrto_uncertainty(memory, int(Gamma.shape[-1]), _ptr(Gamma), _ptr(Psi))
     h = C.c_void_p()
     _check(lib().nrto_setup_general(C.byref(s), C.byref(dd), C.byref(un), C.byref(params),
