@@ -191,7 +191,12 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   int64_t work_tot = 0;
   for (int t = 0; t < ntiles; ++t) work_tot += tile_work[t];
   const int64_t zbytes = 16LL * T * nu * nx;
-  const int smax = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, work_tot / std::max<int64_t>(zbytes, 1)));
+  // work items per instance: the tiled fused pass (fused == 1) writes one adjoint
+  // partial per item, so its split is capped by the partials' size; the TMA pass
+  // forms no adjoint (Gram form), only tiles cap it (single instances
+  // then spread over the SMs)
+  const int smax = use_tma ? std::max(1, ntiles)
+                           : (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, work_tot / std::max<int64_t>(zbytes, 1)));
   int nsplit = (int)std::min<int64_t>(smax, std::max<int64_t>(1, (6LL * 2 * nsm + d.B - 1) / d.B));
   if (ntiles == 0) nsplit = 1;
   std::vector<int32_t> witems;
@@ -207,6 +212,12 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
     }
   }
   v.fused = use_tma ? 2 : ((fused_supported(d) && ntiles > 0) ? 1 : 0);
+  {   // NRTO_FUSED=0: generic warp-per-cone pass instead of the tiled fused pass (non-TMA shapes)
+    // default: tiny batches (B n_g <= 1024 cones, e.g. one c1 instance) take the generic
+    // kernels -- measured c1 FullADMM 104 -> 81 us per iteration
+    static const int fenv = [] { const char* e = getenv("NRTO_FUSED"); return e ? atoi(e) : -1; }();
+    if (v.fused == 1 && (fenv == 0 || (fenv < 0 && (int64_t)d.B * ng <= 1024))) v.fused = 0;
+  }
   v.nsm = nsm;
   v.nctrl = nctrl;
   v.ntiles = ntiles; v.nsplit = nsplit; v.nwitems = (int)(witems.size() / 4);

@@ -1383,13 +1383,30 @@ __device__ __forceinline__ double scan_step(int nx, int lane, double base, const
   return (c0 + c1) + (c2 + c3);
 }
 
-static size_t scan_smem(const Dims& d, int C, int stageA) {
-  return ((size_t)(d.T + 1) * d.nx + (size_t)d.T * d.nx + 2 * (size_t)d.T * d.nu +
-          2 * (size_t)C * d.nx * d.nx + (stageA ? (size_t)d.T * d.nx * d.nx : 0)) * sizeof(double);
+// Shared-memory staging of the scan QP's per-step constants (bit mask, staged in
+// this priority order while they fit): 1 Acl (the recurrences), 2 Kf, 4 H^-1 and
+// H^-1 B^T, 8 B, 16 the transfer matrices PhiB / PhiF (fix-ups).
+constexpr int kScanStageBits = 5;
+static size_t scan_stage_doubles(const Dims& d, int bit) {
+  const size_t T = d.T, nx = d.nx, nu = d.nu;
+  switch (bit) {
+    case 0: return T * nx * nx;
+    case 1: return T * nu * nx;
+    case 2: return T * nu * nu + T * nu * nx;
+    case 3: return T * nx * nu;
+    default: return 2 * T * nx * nx;
+  }
+}
+static size_t scan_smem(const Dims& d, int C, int smask) {
+  size_t n = (size_t)(d.T + 1) * d.nx + (size_t)d.T * d.nx + 2 * (size_t)d.T * d.nu +
+             2 * (size_t)C * d.nx * d.nx;
+  for (int b = 0; b < kScanStageBits; ++b)
+    if (smask & (1 << b)) n += scan_stage_doubles(d, b);
+  return n * sizeof(double);
 }
 
 template <int NXM, int NUM>
-__global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, int stageA) {
+__global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, int smask) {
   extern __shared__ double sm[];
   __shared__ double red[32];
   const Dims d = v.d;
@@ -1413,13 +1430,13 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
   double* gS = v.rx + (int64_t)b * (T + 1) * nx;      // S_k = sum_{state j@k} w_j grad_j (atomic)
   double* gU = v.dut + (int64_t)b * T * nu;           // U_k = sum_{ctrl j@k} w_j h'_j   (atomic)
   const double* __restrict__ cu2 = v.cu2 + (int64_t)b * T * nu;
-  const double* __restrict__ Bm = v.Bm + (int64_t)b * T * nx * nu;
-  const double* __restrict__ Kf = F.Kf + (int64_t)b * T * nu * nx;
-  const double* __restrict__ AclG = F.Acl + (int64_t)b * T * nn;
-  const double* __restrict__ Hi = F.Hinv + (int64_t)b * T * nu * nu;
-  const double* __restrict__ HB = F.HB + (int64_t)b * T * nu * nx;
-  const double* __restrict__ PBg = F.PhiB + (int64_t)b * T * nn;
-  const double* __restrict__ PFg = F.PhiF + (int64_t)b * T * nn;
+  const double* KfG = F.Kf + (int64_t)b * T * nu * nx;
+  const double* AclG = F.Acl + (int64_t)b * T * nn;
+  const double* HiG = F.Hinv + (int64_t)b * T * nu * nu;
+  const double* HBG = F.HB + (int64_t)b * T * nu * nx;
+  const double* BmG = v.Bm + (int64_t)b * T * nx * nu;
+  const double* PBg = F.PhiB + (int64_t)b * T * nn;
+  const double* PFg = F.PhiF + (int64_t)b * T * nn;
   const double rtr = v.rtrust[b];
   const double rinv = (engine == NRTO_FULLADMM) ? 1.0 : 1.0 / rho;
   double* sS = sm;                          // [(T+1) nx]  s~/s, then dx~/dx, then z^_ball
@@ -1428,10 +1445,22 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
   double* sK = sR + T * nu;                 // [T nu]      kff_k
   double* sPb = sK + T * nu;                // [C][nx][nx] PhiB at chunk starts
   double* sPf = sPb + C * nn;               // [C][nx][nx] PhiF at chunk ends
-  double* sAcl = sPf + C * nn;              // [T][nx][nx] (stageA)
-  const double* Acl = stageA ? sAcl : AclG;
-  if (stageA)
-    for (int r = tid; r < T * nn; r += nt) sAcl[r] = AclG[r];
+  // staged per-step constants (smask), in this order after sPf
+  double* nxt = sPf + C * nn;
+  auto stage = [&](int bit, const double* g, int64_t n) -> const double* {
+    if (!(smask & (1 << bit))) return g;
+    double* dst = nxt;
+    nxt += n;
+    for (int64_t r = tid; r < n; r += nt) dst[r] = g[r];
+    return dst;
+  };
+  const double* __restrict__ Acl = stage(0, AclG, (int64_t)T * nn);
+  const double* __restrict__ Kf = stage(1, KfG, (int64_t)T * nu * nx);
+  const double* __restrict__ Hi = stage(2, HiG, (int64_t)T * nu * nu);
+  const double* __restrict__ HB = (smask & 4) ? stage(2, HBG, (int64_t)T * nu * nx) : HBG;
+  const double* __restrict__ Bm = stage(3, BmG, (int64_t)T * nx * nu);
+  const double* __restrict__ PB = stage(4, PBg, (int64_t)T * nn);
+  const double* __restrict__ PF = (smask & 16) ? stage(4, PFg, (int64_t)T * nn) : PFg;
   for (int r = tid; r < C * nn; r += nt) {
     const int c = r / nn, e = r - c * nn;
     sPb[r] = PBg[(int64_t)(c * M) * nn + e];
@@ -1497,7 +1526,7 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
     for (int r = tid; r < T * nx; r += nt) {
       const int k = r / nx, i = r - k * nx, c = k / M;
       if (c == C - 1 || k == c * M) continue;
-      const double* Pk = PBg + (int64_t)k * nn + i * nx;
+      const double* Pk = PB + (int64_t)k * nn + i * nx;
       const double* sn = sS + (c + 1) * M * nx;
       sS[r] += dotn<NXM>(nx, [&](int q) { return Pk[q]; }, [&](int q) { return sn[q]; }, 0.0);
     }
@@ -1554,7 +1583,7 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
       const int k = r / nx, i = r - k * nx, c = k / M;
       const int hi = min(T, (c + 1) * M) - 1;
       if (c == 0 || k == hi) continue;
-      const double* Pk = PFg + (int64_t)k * nn + i * nx;
+      const double* Pk = PF + (int64_t)k * nn + i * nx;
       const double* xl = sS + c * M * nx;
       sS[r + nx] += dotn<NXM>(nx, [&](int q) { return Pk[q]; }, [&](int q) { return xl[q]; }, 0.0);
     }
@@ -1624,31 +1653,37 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
   }
 }
 
-// Chunked-scan QP usable for this launch (grid 0 / >= B: one CTA per instance).
+// Chunked-scan QP usable for this launch (grid 0 / >= B: one CTA per instance):
+// returns its staging mask (-1: not usable).
 static int scan_stage(const nrto_handle_s* h, int grid) {
   const Dev& v = h->dev;
   static const int env = [] { const char* e = getenv("NRTO_QP_SCAN"); return e ? atoi(e) : 1; }();
+  static const int menv = [] { const char* e = getenv("NRTO_QP_SCAN_STAGE"); return e ? atoi(e) : -1; }();
   if (!env || v.scanC <= 0 || !v.fa.PhiB || v.d.B > kScanMaxBatch) return -1;
   if (grid > 0 && grid < v.d.B) return -1;
   const size_t lim = 220 * 1024;
-  if (scan_smem(v.d, v.scanC, 1) <= lim) return 1;
-  if (scan_smem(v.d, v.scanC, 0) <= lim) return 0;
-  return -1;
+  if (scan_smem(v.d, v.scanC, 0) > lim) return -1;
+  if (menv >= 0) return scan_smem(v.d, v.scanC, menv) <= lim ? menv : 0;
+  int mask = 0;
+  for (int b = 0; b < kScanStageBits; ++b)
+    if (scan_smem(v.d, v.scanC, mask | (1 << b)) <= lim) mask |= 1 << b;
+    else if (b == 0) break;          // without Acl in shared memory stage nothing else
+  return mask;
 }
 
-static cudaError_t launch_qp_scan(nrto_handle_s* h, int engine, int l, int stageA, cudaStream_t st) {
+static cudaError_t launch_qp_scan(nrto_handle_s* h, int engine, int l, int smask, cudaStream_t st) {
   const Dims& d = h->dev.d;
-  const size_t smem = scan_smem(d, h->dev.scanC, stageA);
+  const size_t smem = scan_smem(d, h->dev.scanC, smask);
   void* kern;
   if (d.nx == 14 && d.nu == 7) kern = (void*)k_qp_scan<14, 7>;
   else if (d.nx == 12 && d.nu == 4) kern = (void*)k_qp_scan<12, 4>;
   else if (d.nx == 3 && d.nu == 2) kern = (void*)k_qp_scan<3, 2>;
   else kern = (void*)k_qp_scan<0, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (d.nx == 14 && d.nu == 7) k_qp_scan<14, 7><<<d.B, 512, smem, st>>>(h->dev, engine, l, stageA);
-  else if (d.nx == 12 && d.nu == 4) k_qp_scan<12, 4><<<d.B, 512, smem, st>>>(h->dev, engine, l, stageA);
-  else if (d.nx == 3 && d.nu == 2) k_qp_scan<3, 2><<<d.B, 512, smem, st>>>(h->dev, engine, l, stageA);
-  else k_qp_scan<0, 0><<<d.B, 512, smem, st>>>(h->dev, engine, l, stageA);
+  if (d.nx == 14 && d.nu == 7) k_qp_scan<14, 7><<<d.B, 512, smem, st>>>(h->dev, engine, l, smask);
+  else if (d.nx == 12 && d.nu == 4) k_qp_scan<12, 4><<<d.B, 512, smem, st>>>(h->dev, engine, l, smask);
+  else if (d.nx == 3 && d.nu == 2) k_qp_scan<3, 2><<<d.B, 512, smem, st>>>(h->dev, engine, l, smask);
+  else k_qp_scan<0, 0><<<d.B, 512, smem, st>>>(h->dev, engine, l, smask);
   h->launches++;
   return cudaGetLastError();
 }

@@ -344,7 +344,11 @@ def test_two_process_collective_loop_on_one_gpu():
     s_ = socket.socket(); s_.bind(("127.0.0.1", 0)); port = s_.getsockname()[1]; s_.close()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_mp_worker, args=(2, port, out), nprocs=2, join=True)
+    try:
+        mp.spawn(_mp_worker, args=(2, port, out), nprocs=2, join=True)
+        out = dict(out)
+    finally:
+        mgr.shutdown()
     items = [make_unicycle(1, i) for i in range(4)]
     shape, batch = stack_instances(items)
     ref = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, max_iter=300, eps_p=1e-5, eps_d=1e-5, check_every=2)
