@@ -607,7 +607,13 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
     // captured once into a CUDA graph (keyed by the device-state descriptor before
     // the loop) and replayed -- the per-iteration kernels are short, launch gaps matter
     static const int use_graph_fa = [] { const char* e = getenv("NRTO_GRAPH"); return e ? atoi(e) : 1; }();
-    if (!overlap && prm.fixed_iters && !h->prof && use_graph_fa) {
+    if (!overlap && fa_small_ok(h)) {
+      // small instances: the whole loop (all outer iterations, per-instance termination)
+      // in one launch, one CTA per instance (qp.cu k_fa_small)
+      v.iter = 0;
+      CK(timed(NRTO_K_QP, [&](nrto_handle_s* hh, cudaStream_t s2) { return launch_fa_small(hh, prm.max_iter, s2); }));
+      v.iter = prm.max_iter;
+    } else if (!overlap && prm.fixed_iters && !h->prof && use_graph_fa) {
       if (!h->gst) CK(cudaStreamCreateWithFlags(&h->gst, cudaStreamNonBlocking));
       if (!h->ev_in) CK(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
       if (!h->ev_out) CK(cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming));

@@ -5,23 +5,6 @@
 
 namespace nrto {
 
-// Geometry of cone j's ragged row.
-struct ConeGeom {
-  int kind, knot, L, klo, nbB;
-  int64_t off, offB;
-};
-__device__ __forceinline__ ConeGeom cone_geom(const Dev& v, int j) {
-  ConeGeom g;
-  g.kind = v.kind[j];
-  g.knot = v.knot[j];
-  g.off = v.off[j];
-  g.offB = v.offB[j];
-  g.L = (g.kind == 0) ? (g.knot + 1) * v.d.nx : v.d.nx;
-  g.klo = (g.kind == 0) ? 0 : g.knot;
-  g.nbB = (g.kind == 0) ? g.knot : 1;
-  return g;
-}
-
 // ---------------------------------------------------------------------------
 // FullADMM fused pass: Block-1 (13) of iteration l, with the dual update (16)
 // of iteration l-1 folded in.  The stored per-cone row is the projection
@@ -157,53 +140,6 @@ __global__ void k_fa_gain(Dev v, int mode, const double* kin, double* kout) {
     v.Ccur[idx] = c;
     v.D[idx] = 2.0 * c - cold;
   }
-}
-
-// Warp-level versions: one warp per (instance, step), 8 per CTA (the 7x14
-// chain has 98 outputs, so a CTA per step mostly idles and the tiny CTAs
-// crowd the SMs the concurrently running QP needs).
-// NXC, NUC > 0: sizes fixed at compile time (bench shapes; loops fully unrolled,
-// same summation order as the runtime-size version).
-template <int NXC = 0, int NUC = 0>
-__device__ __forceinline__ void chain_solve_w(const double* V, const double* U, const double* den,
-                                              double* sR, double* sX, int nu_rt, int nx_rt, int lane) {
-  const int nx = NXC > 0 ? NXC : nx_rt, nu = NUC > 0 ? NUC : nu_rt;
-#pragma unroll
-  for (int r = lane; r < nu * nx; r += 32) {
-    const int a = r / nx, c = r % nx;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < nu; ++q) acc += V[q * nu + a] * sR[q * nx + c];
-    sX[r] = acc;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int r = lane; r < nu * nx; r += 32) {
-    const int a = r / nx, c = r % nx;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[q * nx + c];
-    sR[r] = acc * den[r];
-  }
-  __syncwarp();
-#pragma unroll
-  for (int r = lane; r < nu * nx; r += 32) {
-    const int a = r / nx, c = r % nx;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < nu; ++q) acc += V[a * nu + q] * sR[q * nx + c];
-    sX[r] = acc;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int r = lane; r < nu * nx; r += 32) {
-    const int a = r / nx, c = r % nx;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < nx; ++q) acc += sX[a * nx + q] * U[c * nx + q];
-    sR[r] = acc;
-  }
-  __syncwarp();
 }
 
 template <int NXC = 0, int NUC = 0>

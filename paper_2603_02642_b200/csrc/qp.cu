@@ -1385,16 +1385,18 @@ __device__ __forceinline__ double scan_step(int nx, int lane, double base, const
 
 // Shared-memory staging of the scan QP's per-step constants (bit mask, staged in
 // this priority order while they fit): 1 Acl (the recurrences), 2 Kf, 4 H^-1 and
-// H^-1 B^T, 8 B, 16 the transfer matrices PhiB / PhiF (fix-ups).
-constexpr int kScanStageBits = 5;
+// H^-1 B^T, 8 B, 16 the transfer matrices PhiB / PhiF (short chunks), 32 the mutable
+// QP vectors (p, z, y, the ball pair, du, the knot accumulators) for the launch.
+constexpr int kScanStageBits = 6;
 static size_t scan_stage_doubles(const Dims& d, int bit) {
-  const size_t T = d.T, nx = d.nx, nu = d.nu;
+  const size_t T = d.T, nx = d.nx, nu = d.nu, ng = d.ng;
   switch (bit) {
     case 0: return T * nx * nx;
     case 1: return T * nu * nx;
     case 2: return T * nu * nu + T * nu * nx;
     case 3: return T * nx * nu;
-    default: return 2 * T * nx * nx;
+    case 4: return 2 * T * nx * nx;
+    default: return 4 * ng + 3 * (T + 1) * nx + 2 * T * nu;   // resident mutable vectors
   }
 }
 static size_t scan_smem(const Dims& d, int C, int smask) {
@@ -1406,12 +1408,11 @@ static size_t scan_smem(const Dims& d, int C, int smask) {
 }
 
 template <int NXM, int NUM>
-__global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, int smask) {
-  extern __shared__ double sm[];
-  __shared__ double red[32];
+__device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int smask, int b, double* sm,
+                                            double* red) {
   const Dims d = v.d;
   const int nx = NXM > 0 ? NXM : d.nx, nu = NUM > 0 ? NUM : d.nu, T = d.T, ng = d.ng;
-  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int M = v.scanM, C = v.scanC, nn = nx * nx;
   if (!v.active[b]) return;
@@ -1422,11 +1423,13 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
   const int64_t bg = (int64_t)b * ng;
   const double* __restrict__ grad = v.grad + bg * nx;
   const double* __restrict__ g0 = v.g0 + bg;
-  double* p = v.p + bg; double* zl = v.zl + bg; double* yl = v.yl + bg;
+  double* const p_g = v.p + bg; double* const zl_g = v.zl + bg; double* const yl_g = v.yl + bg;
+  double* p = p_g; double* zl = zl_g; double* yl = yl_g;
   double* rp = v.rp + bg;
   const double* pt = v.pt + bg; double* lam = v.lamp + bg;
-  double* zb = v.zb + (int64_t)b * (T + 1) * nx; double* yb = v.yb + (int64_t)b * (T + 1) * nx;
-  double* du = v.du + (int64_t)b * T * nu;
+  double* const zb_g = v.zb + (int64_t)b * (T + 1) * nx; double* const yb_g = v.yb + (int64_t)b * (T + 1) * nx;
+  double* const du_g = v.du + (int64_t)b * T * nu;
+  double* zb = zb_g; double* yb = yb_g; double* du = du_g;
   double* gS = v.rx + (int64_t)b * (T + 1) * nx;      // S_k = sum_{state j@k} w_j grad_j (atomic)
   double* gU = v.dut + (int64_t)b * T * nu;           // U_k = sum_{ctrl j@k} w_j h'_j   (atomic)
   const double* __restrict__ cu2 = v.cu2 + (int64_t)b * T * nu;
@@ -1461,6 +1464,23 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
   const double* __restrict__ Bm = stage(3, BmG, (int64_t)T * nx * nu);
   const double* __restrict__ PB = stage(4, PBg, (int64_t)T * nn);
   const double* __restrict__ PF = (smask & 16) ? stage(4, PFg, (int64_t)T * nn) : PFg;
+  // interior steps: long chunks re-run the chunk from its exact boundary (M more
+  // dependent steps, shared-memory operands only); short chunks add PhiB_k s_{hi+1} /
+  // PhiF_k dx_lo in one parallel phase (one round of transfer-matrix loads)
+  const bool rescan = M >= 8;
+  // bit 32: the QP's mutable vectors live in shared memory for the launch (copied in
+  // here, out before the tail); the knot accumulators S, U then take shared atomics
+  const bool res = (smask & 32) != 0;
+  if (res) {
+    auto take = [&](int64_t n) { double* q = nxt; nxt += n; return q; };
+    p = take(ng); zl = take(ng); yl = take(ng); rp = take(ng);
+    zb = take((int64_t)(T + 1) * nx); yb = take((int64_t)(T + 1) * nx); gS = take((int64_t)(T + 1) * nx);
+    du = take((int64_t)T * nu); gU = take((int64_t)T * nu);
+    for (int r = tid; r < ng; r += nt) { p[r] = p_g[r]; zl[r] = zl_g[r]; yl[r] = yl_g[r]; }
+    for (int r = tid; r < (T + 1) * nx; r += nt) { zb[r] = zb_g[r]; yb[r] = yb_g[r]; }
+    for (int r = tid; r < T * nu; r += nt) du[r] = du_g[r];
+  }
+  auto ldacc = [&](const double* q) { return res ? *q : __ldcg(q); };
   for (int r = tid; r < C * nn; r += nt) {
     const int c = r / nn, e = r - c * nn;
     sPb[r] = PBg[(int64_t)(c * M) * nn + e];
@@ -1477,27 +1497,28 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
   }
   for (int it = 0; it < nits; ++it) {
     for (int r = tid; r < T * nu; r += nt) {          // r_u (consumes and clears U)
-      sR[r] = sq * du[r] + __ldcg(gU + r) + cu2[r];   // cu2 = -2 R_u u_hat (setup)
+      sR[r] = sq * du[r] + ldacc(gU + r) + cu2[r];    // cu2 = -2 R_u u_hat (setup)
       gU[r] = 0.0;
     }
     __syncthreads();
     for (int r = tid; r < (T + 1) * nx; r += nt) {    // r_x and a_k (consumes and clears S)
       const int k = r / nx, i = r - k * nx;
-      double acc = (k > 0) ? __ldcg(gS + r) + rq * zb[r] - yb[r] : 0.0;
+      double acc = (k > 0) ? ldacc(gS + r) + rq * zb[r] - yb[r] : 0.0;
       gS[r] = 0.0;
       if (k < T) {
         const double* Kk = Kf + (int64_t)k * nu * nx + i;
         const double* rk = sR + k * nu;
         acc -= dotn<NUM>(nu, [&](int m) { return Kk[m * nx]; }, [&](int m) { return rk[m]; }, 0.0);
       }
-      sS[r] = acc;        // a_k (k < T), s_T
+      if (k < T) sA[r] = acc;                         // a_k
+      else sS[r] = acc;                               // s_T
     }
     __syncthreads();
     if (warp < C) {                                   // chunk-local backward recurrences
       const int lo = warp * M, hi = min(T, (warp + 1) * M) - 1;
       for (int k = hi; k >= lo; --k) {
         const double* Ak = Acl + (size_t)k * nn;
-        const double base = lane < nx ? sS[k * nx + lane] : 0.0;
+        const double base = lane < nx ? sA[k * nx + lane] : 0.0;
         // s~_{hi+1} = 0 for all but the last chunk (which starts from the exact s_T)
         const double x = (k == hi && warp != C - 1)
                              ? base
@@ -1521,14 +1542,25 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
       }
     }
     __syncthreads();
-    // interior fix-up s_k += PhiB_k s_{hi+1} (reads only chunk-start slots, which it
-    // does not write)
-    for (int r = tid; r < T * nx; r += nt) {
-      const int k = r / nx, i = r - k * nx, c = k / M;
-      if (c == C - 1 || k == c * M) continue;
-      const double* Pk = PB + (int64_t)k * nn + i * nx;
-      const double* sn = sS + (c + 1) * M * nx;
-      sS[r] += dotn<NXM>(nx, [&](int q) { return Pk[q]; }, [&](int q) { return sn[q]; }, 0.0);
+    if (!rescan) {
+      for (int r = tid; r < T * nx; r += nt) {        // interior fix-up s_k += PhiB_k s_{hi+1}
+        const int k = r / nx, i = r - k * nx, c = k / M;
+        if (c == C - 1 || k == c * M) continue;
+        const double* Pk = PB + (int64_t)k * nn + i * nx;
+        const double* sn = sS + (c + 1) * M * nx;
+        sS[r] += dotn<NXM>(nx, [&](int q) { return Pk[q]; }, [&](int q) { return sn[q]; }, 0.0);
+      }
+    } else if (warp < C - 1) {                        // interior: re-run each chunk from its
+      const int lo = warp * M, hi = min(T, (warp + 1) * M) - 1;   // exact boundary s_{hi+1}
+      for (int k = hi; k > lo; --k) {
+        const double* Ak = Acl + (size_t)k * nn;
+        const double base = lane < nx ? sA[k * nx + lane] : 0.0;
+        const double x = scan_step<NXM>(nx, lane, base, sS + (k + 1) * nx,
+                                        [&](int i, int r) { return Ak[r * nx + i]; });
+        __syncwarp();
+        if (lane < nx) sS[k * nx + lane] = x;
+        __syncwarp();
+      }
     }
     __syncthreads();
     for (int r = tid; r < T * nu; r += nt) {          // kff_k = H^-1 r_u,k + H^-1 B_k^T s_{k+1}
@@ -1577,15 +1609,25 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
       }
     }
     __syncthreads();
-    // interior fix-up dx_{k+1} += PhiF_k dx_lo (reads only chunk-start slots lo_c,
-    // writes lo_c + 1 .. hi_c)
-    for (int r = tid; r < T * nx; r += nt) {
-      const int k = r / nx, i = r - k * nx, c = k / M;
-      const int hi = min(T, (c + 1) * M) - 1;
-      if (c == 0 || k == hi) continue;
-      const double* Pk = PF + (int64_t)k * nn + i * nx;
-      const double* xl = sS + c * M * nx;
-      sS[r + nx] += dotn<NXM>(nx, [&](int q) { return Pk[q]; }, [&](int q) { return xl[q]; }, 0.0);
+    if (!rescan) {
+      for (int r = tid; r < T * nx; r += nt) {        // interior fix-up dx_{k+1} += PhiF_k dx_lo
+        const int k = r / nx, i = r - k * nx, c = k / M;
+        const int hi = min(T, (c + 1) * M) - 1;
+        if (c == 0 || k == hi) continue;
+        const double* Pk = PF + (int64_t)k * nn + i * nx;
+        const double* xl = sS + c * M * nx;
+        sS[r + nx] += dotn<NXM>(nx, [&](int q) { return Pk[q]; }, [&](int q) { return xl[q]; }, 0.0);
+      }
+    } else if (warp >= 1 && warp < C) {               // interior: re-run each chunk from its
+      const int lo = warp * M, hi = min(T, (warp + 1) * M) - 1;   // exact boundary dx_lo
+      for (int k = lo; k < hi; ++k) {
+        const double* Ak = Acl + (size_t)k * nn;
+        const double base = lane < nx ? sA[k * nx + lane] : 0.0;
+        const double x = scan_step<NXM>(nx, lane, base, sS + k * nx,
+                                        [&](int i, int r) { return Ak[i * nx + r]; });
+        if (lane < nx) sS[(k + 1) * nx + lane] = x;
+        __syncwarp();
+      }
     }
     __syncthreads();
     for (int r = tid; r < T * nu; r += nt) {          // du~_k = kff_k - Kf_k dx_k ; relaxed du
@@ -1617,6 +1659,11 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
       zb[r] = zn;
     }
     __syncthreads();
+  }
+  if (res) {                                          // resident vectors back to global
+    for (int r = tid; r < ng; r += nt) { p_g[r] = p[r]; zl_g[r] = zl[r]; yl_g[r] = yl[r]; }
+    for (int r = tid; r < (T + 1) * nx; r += nt) { zb_g[r] = zb[r]; yb_g[r] = yb[r]; }
+    for (int r = tid; r < T * nu; r += nt) du_g[r] = du[r];
   }
   double ap = 0.0, ad = 0.0;
   double* tin = v.tin + bg;
@@ -1653,6 +1700,129 @@ __global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, in
   }
 }
 
+template <int NXM, int NUM>
+__global__ void __launch_bounds__(512, 1) k_qp_scan(Dev v, int engine, int l, int smask) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  qp_scan_run<NXM, NUM>(v, engine, l, smask, blockIdx.x, sm, red);
+}
+
+// ---------------------------------------------------------------------------
+// Whole FullADMM loop of one small instance per CTA (SURVEY §8f NEXT-3(ii) for the
+// c1-class sizes, Algorithm 1): every outer iteration runs the generic
+// cone pass (13) with the pending dual update (16), the adjoint S7, the gain
+// update (14b) and the chunked-scan QP (14a) + duals / residuals back to back with
+// block barriers, instead of four kernel launches per iteration.  Same per-element
+// arithmetic as k_fa_pass, k_adjoint (cone-list order), k_fa_gain (warp-level
+// chain) and k_qp_scan; per-instance termination (R11, R12) ends the CTA's loop.
+template <int NXM, int NUM>
+__global__ void __launch_bounds__(512, 1) k_fa_small(Dev v, int L, int smask) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  const Dims d = v.d;
+  const int nx = NXM > 0 ? NXM : d.nx, nu = NUM > 0 ? NUM : d.nu, T = d.T, ng = d.ng;
+  const int NA = nu * nx;
+  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  const double st = sqrt(v.tau[b]);
+  const double rho = v.prm.rho;
+  for (int l = 1; l <= L; ++l) {
+    if (!v.active[b]) break;                          // set by the QP tail (barrier below)
+    // ---- (13) + pending (16): y = D b + b_hat + (1 - s) y, projection per cone
+    for (int j = warp; j < ng; j += nw) {
+      const ConeGeom g = cone_geom(v, j);
+      const int64_t ij = (int64_t)b * ng + j;
+      const double omsp = 1.0 - v.s[ij];
+      double* Y = v.Y + (int64_t)b * d.E + g.off;
+      const double* bh = v.bhat + (int64_t)b * d.E + g.off;
+      const double* Bd = v.Bd + (int64_t)b * d.EB + g.offB;
+      const double* Dm = v.D + (int64_t)b * T * nx * nu;
+      double n2 = 0.0;
+      for (int e = lane; e < g.L; e += 32) {
+        const int kb = e / nx, i = e - kb * nx;
+        double acc = (g.kind == 0) ? bh[e] : 0.0;
+        if (kb < g.nbB) {
+          const double* Dr = Dm + ((int64_t)(g.klo + kb) * nx + i) * nu;
+          const double* br = Bd + kb * d.nup;
+          for (int m = 0; m < nu; ++m) acc += Dr[m] * br[m];
+        }
+        const double y = acc + omsp * Y[e];
+        Y[e] = y;
+        n2 += y * y;
+      }
+      n2 = warp_sum(n2);
+      double s;
+      const double tp = soc_case(v.tin[ij], sqrt(n2), &s);
+      if (lane == 0) { v.s[ij] = s; v.pt[ij] = tp; }
+      if (v.case_cnt && l <= v.hist_L && lane == 0) {
+        unsigned long long* cc = v.case_cnt + (int64_t)(l - 1) * 3;
+        atomicAdd(cc + (s == 1.0 ? 0 : (s == 0.0 ? 1 : 2)), 1ULL);
+      }
+    }
+    __syncthreads();
+    // ---- S7: Z_k = sum_j s_j b_{j,k} y_{j,k}^T (cones with a block at k, list order)
+    for (int r = tid; r < T * NA; r += nt) {
+      const int k = r / NA, o = r - k * NA, m = o / nx, i = o - m * nx;
+      const double* yb = v.Y + (int64_t)b * d.E;
+      const double* Bd = v.Bd + (int64_t)b * d.EB;
+      double acc = 0.0;
+      for (int c = v.kptr[k]; c < v.kptr[k + 1]; ++c) {
+        const int j = v.kcone[c];
+        const int kb = (v.kind[j] == 0) ? k : 0;
+        acc += Bd[v.offB[j] + kb * d.nup + m] * yb[v.off[j] + kb * nx + i] * v.s[(int64_t)b * ng + j];
+      }
+      v.Z[((int64_t)b * T + k) * NA + o] = acc;
+    }
+    __syncthreads();
+    // ---- (14b): R = 2 W K + rho sqrt(tau) (Z - Zb) Psi_k, K = chain, C, D (warp per step)
+    for (int k = warp; k < T; k += nw) {
+      const int64_t bk = (int64_t)b * T + k;
+      double* sR = sm + (size_t)warp * 3 * NA;
+      double* sX = sR + NA;
+      double* sK = sX + NA;
+      const double* Pk = v.Psi + ((int64_t)b * (T + 1) + k) * nx * nx;
+      const double* Wk = v.W + bk * nu * nu;
+      double* Kb = v.K + (int64_t)b * d.NK + (int64_t)k * NA;
+      for (int r = lane; r < NA; r += 32) {
+        sX[r] = v.Z[bk * NA + r] - v.Zb[bk * NA + r];
+        const int m = r / nx, i = r % nx;
+        sK[r] = Kb[i * nu + m];
+      }
+      __syncwarp();
+      for (int r = lane; r < NA; r += 32) {
+        const int m = r / nx, i = r % nx;
+        double gp = 0.0, wk = 0.0;
+        for (int q = 0; q < nx; ++q) gp += sX[m * nx + q] * Pk[q * nx + i];
+        for (int q = 0; q < nu; ++q) wk += Wk[m * nu + q] * sK[q * nx + i];
+        sR[r] = 2.0 * wk + rho * st * gp;
+      }
+      __syncwarp();
+      chain_solve_w<NXM, NUM>(v.fa.V + bk * nu * nu, v.U + bk * nx * nx, v.fa.den + bk * NA, sR, sX,
+                               nu, nx, lane);
+      for (int r = lane; r < NA; r += 32) {
+        const int m = r / nx, i = r % nx;
+        Kb[i * nu + m] = sR[r];
+      }
+      for (int r = lane; r < NA; r += 32) {
+        const int i = r / nu, m = r % nu;
+        double acc = 0.0;
+        for (int q = 0; q < nx; ++q) acc += Pk[i * nx + q] * sR[m * nx + q];
+        const double c = st * acc;
+        const int64_t idx = bk * NA + r;
+        const double cold = v.Ccur[idx];
+        v.Cprev[idx] = cold;
+        v.Ccur[idx] = c;
+        v.D[idx] = 2.0 * c - cold;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- (14a) QP + (16) lam_p + residuals + termination
+    qp_scan_run<NXM, NUM>(v, NRTO_FULLADMM, l, smask, b, sm, red);
+    __syncthreads();
+  }
+}
+
 // Chunked-scan QP usable for this launch (grid 0 / >= B: one CTA per instance):
 // returns its staging mask (-1: not usable).
 static int scan_stage(const nrto_handle_s* h, int grid) {
@@ -1664,10 +1834,18 @@ static int scan_stage(const nrto_handle_s* h, int grid) {
   const size_t lim = 220 * 1024;
   if (scan_smem(v.d, v.scanC, 0) > lim) return -1;
   if (menv >= 0) return scan_smem(v.d, v.scanC, menv) <= lim ? menv : 0;
+  // staged data up to ~120 KB: beyond that the L1 cache, which shares the 256 KB
+  // with shared memory, serves the per-step constants better (c3: Acl alone is
+  // 157 KB; measured 573 -> 522 us per FullADMM iteration unstaged)
+  const size_t cap = std::max(scan_smem(v.d, v.scanC, 0), (size_t)120 * 1024);
   int mask = 0;
-  for (int b = 0; b < kScanStageBits; ++b)
-    if (scan_smem(v.d, v.scanC, mask | (1 << b)) <= lim) mask |= 1 << b;
+  const int order[kScanStageBits] = {0, 5, 1, 2, 3, 4};
+  for (int q = 0; q < kScanStageBits; ++q) {
+    const int b = order[q];
+    if (b == 4 && v.scanM >= 8) continue;          // long chunks re-scan: no transfer matrices
+    if (scan_smem(v.d, v.scanC, mask | (1 << b)) <= std::min(lim, cap)) mask |= 1 << b;
     else if (b == 0) break;          // without Acl in shared memory stage nothing else
+  }
   return mask;
 }
 
@@ -1754,6 +1932,27 @@ cudaError_t launch_sparse_rows(nrto_handle_s* h, cudaStream_t st) {
     k_sparse_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(h->dev);
     h->launches++;
   }
+  return cudaGetLastError();
+}
+
+bool fa_small_ok(const nrto_handle_s* h) {
+  const Dev& v = h->dev;
+  static const int env = [] { const char* e = getenv("NRTO_FA_SMALL"); return e ? atoi(e) : 1; }();
+  if (!env || v.fused != 0 || v.d.B > kScanMaxBatch || v.d.nx > 32) return false;
+  const int sm = scan_stage(h, 0);
+  if (sm < 0) return false;
+  return std::max(scan_smem(v.d, v.scanC, sm), (size_t)16 * 3 * v.d.nu * v.d.nx * sizeof(double)) <= 220 * 1024;
+}
+
+cudaError_t launch_fa_small(nrto_handle_s* h, int L, cudaStream_t st) {
+  const Dims& d = h->dev.d;
+  const int smask = scan_stage(h, 0);
+  const size_t smem = std::max(scan_smem(d, h->dev.scanC, smask), (size_t)16 * 3 * d.nu * d.nx * sizeof(double));
+  void* kern = (d.nx == 3 && d.nu == 2) ? (void*)k_fa_small<3, 2> : (void*)k_fa_small<0, 0>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (d.nx == 3 && d.nu == 2) k_fa_small<3, 2><<<d.B, 512, smem, st>>>(h->dev, L, smask);
+  else k_fa_small<0, 0><<<d.B, 512, smem, st>>>(h->dev, L, smask);
+  h->launches++;
   return cudaGetLastError();
 }
 

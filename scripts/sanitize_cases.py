@@ -19,9 +19,20 @@ def run(name, shape, batch, engine, **kw):
 
 one = lambda sh, d: stack_instances([(sh, d)])[1]
 sh, d = make_instance("c1")
-run("c1 FullADMM (staged QP, graph)", sh, one(sh, d), nrto.NRTO_FULLADMM, max_iter=3, fixed_iters=1)
+run("c1 FullADMM (whole-loop k_fa_small, scan QP staged + resident)", sh, one(sh, d), nrto.NRTO_FULLADMM,
+    max_iter=3, fixed_iters=1)
 run("c1 FullADMM termination", sh, one(sh, d), nrto.NRTO_FULLADMM, max_iter=6)
-run("c1 DR (graph)", sh, one(sh, d), nrto.NRTO_DR, max_admm_iter=2, max_dr_iter=3, fixed_iters=1)
+run("c1 DR (persistent k_dr_loop, graph)", sh, one(sh, d), nrto.NRTO_DR, max_admm_iter=2, max_dr_iter=3,
+    fixed_iters=1)
+run("c1 DR early stop (in-kernel stop test)", sh, one(sh, d), nrto.NRTO_DR, max_admm_iter=2, max_dr_iter=40,
+    eps_dr=1e-3)
+sh2, d2 = make_instance("c2")
+run("c2 DR (persistent loop, chunks)", sh2, one(sh2, d2), nrto.NRTO_DR, max_admm_iter=1, max_dr_iter=3,
+    fixed_iters=1)
+items = [make_quad(2, i, T=16, n_obs=4) for i in range(5)]
+sh5, b5 = stack_instances(items)
+run("quad batch 5 DR (several tasks per CTA)", sh5, b5, nrto.NRTO_DR, max_admm_iter=2, max_dr_iter=3,
+    fixed_iters=1)
 sh, d = make_franka(3, 0, T=12)
 run("c3s FullADMM (TMA pass, pipelined sparse QP)", sh, one(sh, d), nrto.NRTO_FULLADMM, max_iter=3, fixed_iters=1)
 run("c3s DR", sh, one(sh, d), nrto.NRTO_DR, max_admm_iter=2, max_dr_iter=3, fixed_iters=1)

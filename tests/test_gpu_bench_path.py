@@ -305,8 +305,13 @@ def test_case_stats_match_oracle():
         np.testing.assert_array_equal(cnt, np.asarray(o["cases"]))
 
 
-def _mp_worker(rank, world, port, out):
-    import os
+_MP_CHILD = r"""
+import json, os, sys
+sys.path.insert(0, %r)
+import torch.multiprocessing as mp
+
+
+def worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -328,33 +333,53 @@ def _mp_worker(rank, world, port, out):
 
     o, done, ncoll = solve_collective(s, nrto.NRTO_FULLADMM, allreduce=allreduce)
     torch.cuda.synchronize()
-    out[rank] = (first, o["iters"].cpu().numpy().tolist(), o["kv"].cpu().numpy(), done, ncoll)
+    q.put((rank, first, o["iters"].cpu().numpy().tolist(), o["kv"].cpu().numpy().tolist(), done, ncoll))
     s.close()
     dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    port = int(sys.argv[1])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps: p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in ps: p.join()
+    print(json.dumps({str(r[0]): r[1:] for r in res}))
+"""
 
 
 def test_two_process_collective_loop_on_one_gpu():
     """Two ranks (processes) on one GPU, instances sharded, the termination test
     allreduced every check_every iterations: both ranks run until the slowest
     instance of EITHER shard has converged, and every instance's result equals
-    its single-process solve."""
+    its single-process solve.  The ranks run under a child interpreter, so this
+    pytest process never forks (an OpenBLAS call of the oracle deadlocked in it
+    after an in-process torch.multiprocessing Manager)."""
     _require_gpu()
+    import json
+    import os
     import socket
-    import torch.multiprocessing as mp
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     s_ = socket.socket(); s_.bind(("127.0.0.1", 0)); port = s_.getsockname()[1]; s_.close()
-    mgr = mp.Manager()
-    out = mgr.dict()
-    try:
-        mp.spawn(_mp_worker, args=(2, port, out), nprocs=2, join=True)
-        out = dict(out)
-    finally:
-        mgr.shutdown()
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:         # spawn re-imports the main module: a file
+        script = os.path.join(td, "two_ranks.py")
+        with open(script, "w") as f:
+            f.write(_MP_CHILD % root)
+        r = subprocess.run([sys.executable, script, str(port)], capture_output=True, text=True,
+                           timeout=280)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = {int(k): v for k, v in json.loads(r.stdout.strip().splitlines()[-1]).items()}
     items = [make_unicycle(1, i) for i in range(4)]
     shape, batch = stack_instances(items)
     ref = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, max_iter=300, eps_p=1e-5, eps_d=1e-5, check_every=2)
     last = int(ref["iters"].max())
-    for r in range(2):
-        first, iters, kv, done, ncoll = out[r]
+    for rk in range(2):
+        first, iters, kv, done, ncoll = out[rk]
         assert done == last and ncoll == last // 2          # global stop, one collective per chunk
         np.testing.assert_array_equal(iters, ref["iters"][first:first + 2])
-        assert close(kv, ref["kv"][first:first + 2], tol=1e-12)
+        assert close(np.array(kv), ref["kv"][first:first + 2], tol=1e-12)

@@ -113,3 +113,27 @@ def test_scan_qp_long_horizon_chunks():
         g = gpu_solve(shape, single(shape, data), nrto.NRTO_FULLADMM, max_iter=6, fixed_iters=1)
         o = oracle_run(shape, data, nrto.NRTO_FULLADMM, max_iter=6, fixed_iters=1)
         assert_parity(g, o)
+
+
+@pytest.mark.parametrize("case", ["c1"])
+def test_small_instance_megakernel_matches_launch_per_phase(case):
+    """The whole-loop FullADMM kernel for small instances (k_fa_small, one CTA per
+    instance) against the four-launches-per-iteration path on the same solves."""
+    a = _run_child(case, 0, NRTO_FA_SMALL=1)
+    b = _run_child(case, 0, NRTO_FA_SMALL=0)
+    for sa, sb in zip(a, b):
+        for k in sa:
+            assert close(np.array(sa[k]), np.array(sb[k]), tol=1e-11), (case, k)
+
+
+def test_small_instance_megakernel_termination_and_trace():
+    """Per-instance termination inside the whole-loop kernel: a batch of unicycles
+    stops each instance at the oracle's iteration, with the residual trace."""
+    items = [make_unicycle(1, i) for i in range(5)]
+    shape, batch = stack_instances(items)
+    kw = dict(max_iter=200, eps_p=1e-4, eps_d=1e-4, check_every=3)
+    g = gpu_solve(shape, batch, nrto.NRTO_FULLADMM, **kw)
+    for i, (_, d) in enumerate(items):
+        o = oracle_run(shape, d, nrto.NRTO_FULLADMM, **kw)
+        assert int(g["iters"][i]) == int(o["iters"]), i
+        assert_parity(g, o, i=i)
