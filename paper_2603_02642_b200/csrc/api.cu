@@ -259,7 +259,13 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   AL(v.bhat, B * d.E); AL(v.Bd, B * d.EB); AL(v.Zb, B * T * nu * nx); AL(v.Lam, B * T * nu * nu);
   AL(v.U, B * T * nx * nx); AL(v.Ulam, B * T * nx); AL(v.Urep, B * T); AL(v.psame, B * T);
   v.scanM = 0; v.scanC = 0;
-  if (B <= kScanMaxBatch && T >= 2 && nx <= 32 && nu <= 32) scan_plan(T, v.scanM, v.scanC);
+  v.qpgrid = 0; v.qg_s = nullptr; v.qg_a = nullptr; v.qg_part = nullptr; v.qg_bar = nullptr;
+  if (B <= kScanMaxBatch && T >= 2 && nx <= 32 && nu <= 32) {
+    // one large instance (many rows or a horizon whose QP vectors exceed one CTA's
+    // shared memory): the grid-wide QP with its own chunking; else the one-CTA scan QP
+    if (qp_grid_plan(d, nsm, v.scanM, v.scanC)) v.qpgrid = 1;
+    else scan_plan(T, v.scanM, v.scanC);
+  }
   for (EngineFactors* F : {&v.fa, &v.dr}) {
     AL(F->V, B * T * nu * nu); AL(F->den, B * T * nu * nx); AL(F->Kf, B * T * nu * nx);
     AL(F->Acl, B * T * nx * nx); AL(F->AclT, B * T * nx * nx); AL(F->Hinv, B * T * nu * nu); AL(F->HB, B * T * nu * nx);
@@ -289,6 +295,9 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   cudaMemset(v.pass_bytes, 0, sizeof(unsigned long long));
   v.ylazy = 0;
   AL(v.clist, B * ng); AL(v.cw, B * ng); AL(v.ncorr, B);
+  if (v.qpgrid) {
+    AL(v.qg_s, B * (T + 1) * nx); AL(v.qg_a, B * T * nx); AL(v.qg_part, 2 * 1024); AL(v.qg_bar, 1);
+  }
   // persistent DR loop (persist.cu): cone chunks of one instance
   std::vector<int32_t> drch, drkr;
   int drEc = 0, drEBc = 0;
@@ -315,6 +324,10 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   hup(dcptr, cptr.data(), (T + 1) * 4); hup(dcrow, crow.data(), crow.size() * 4);
   hup(dqrow, qrow.data(), qrow.size() * 4);
   hup(dtiles, tiles.data(), tiles.size() * 4); hup(dwitems, witems.data(), witems.size() * 4);
+  if (v.qpgrid && ce == cudaSuccess) {
+    h->qp_grid = qp_grid_size(h);
+    if (h->qp_grid == 0) { v.qpgrid = 0; v.scanM = 0; v.scanC = 0; }   // not co-resident: older QP kernels
+  }
   if (v.drQ > 0) {
     hup((void*)v.drchunk, drch.data(), drch.size() * 4);
     hup((void*)v.drkr, drkr.data(), drkr.size() * 4);

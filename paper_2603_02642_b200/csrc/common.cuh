@@ -132,6 +132,12 @@ struct Dev {
   unsigned long long* drbar;   // grid-barrier counter (zeroed by k_dr_arm)
   int drEc, drEBc;         // largest chunk: eta~ elements, b-row elements
   int scanM, scanC;        // QP recurrence chunks: length M, count C (0: no scan QP)
+  // grid-wide QP for one large instance (qp.cu k_qp_grid): qpgrid = 1 when used
+  int qpgrid;
+  double* qg_s;            // [(T+1) nx] s_k
+  double* qg_a;            // [T nx]     a_k, then e_k
+  double* qg_part;         // [2][1024]  per-CTA partial sums
+  unsigned long long* qg_bar;   // grid-barrier counter (zeroed before each launch)
 };
 
 }  // namespace nrto
@@ -202,6 +208,7 @@ struct nrto_handle_s {
   int inc_engine = -1;                      // incremental solve in progress (nrto_solve_begin)
   int inc_l = 0;                            // outer iterations run by it
   int dr_loop_grid = 0;                     // persistent DR loop grid (0: not usable)
+  int qp_grid = 0;                          // grid-wide QP grid size (0: not usable)
 };
 
 namespace nrto {
@@ -437,6 +444,8 @@ void scan_plan(int T, int& M, int& C);
 cudaError_t launch_scan_factors(nrto_handle_s* h, int engine, cudaStream_t st);
 // whole FullADMM loop of a small instance per CTA (qp.cu)
 bool fa_small_ok(const nrto_handle_s* h);
+bool qp_grid_plan(const Dims& d, int nsm, int& M, int& C);
+int qp_grid_size(const nrto_handle_s* h);
 cudaError_t launch_fa_small(nrto_handle_s* h, int L, cudaStream_t st);
 
 }  // namespace nrto

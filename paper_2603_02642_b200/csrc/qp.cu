@@ -1075,9 +1075,11 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
     QP_CLK(3);
     if (tid < 32) {                                   // backward recurrence
       if constexpr (NXM > 0) {
-        // s_k[i] = a_k[i] + <AclT_k row i, s_{k+1}>: AclT_k arrives by one bulk copy
-        // per step into a kQPRing-slot ring (mbarrier), s_{k+1} by broadcast LDS.128
-        const double* AT = F.AclT + (int64_t)b * T * nn;
+        // s_k[i] = a_k[i] + <column i of Acl_k, s_{k+1}>: Acl_k arrives by one bulk copy
+        // per step into a kQPRing-slot ring (mbarrier; the same array as the forward
+        // sweep, so the QP streams Acl once, not Acl and its transpose), column reads
+        // conflict-free across lanes, s_{k+1} by broadcast LDS.128
+        const double* AT = F.Acl + (int64_t)b * T * nn;
         // ring position = running copy count n (2T per QP iteration): slot n % R,
         // parity (n / R) & 1 -- computed, not carried, to keep it out of local memory
         const int n0 = it * 2 * T;
@@ -1091,16 +1093,15 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
         for (int k = T - 1; k >= 0; --k) {
           const int n = n0 + (T - 1 - k), rslot = n & (kQPRing - 1);
           qp_wait(&qbar[rslot], (uint32_t)(n / kQPRing) & 1u);
-          const double* Ar = ring + rslot * nn + ic * nx;
+          const double* Ac = ring + rslot * nn + ic;
           const double* sn = sS + (k + 1) * nx;
           double c0 = sS[k * nx + ic], c1 = 0.0;
 #pragma unroll
           for (int r = 0; r < NXM; r += 2)
             if (r < nx) {
-              const double2 a = *reinterpret_cast<const double2*>(Ar + r);
               const double2 x2 = *reinterpret_cast<const double2*>(sn + r);
-              c0 = fma(a.x, x2.x, c0);
-              c1 = fma(a.y, x2.y, c1);
+              c0 = fma(Ac[r * nx], x2.x, c0);
+              c1 = fma(Ac[(r + 1) * nx], x2.y, c1);
             }
           __syncwarp();
           if (tid < nx) sS[k * nx + tid] = c0 + c1;
@@ -1823,13 +1824,390 @@ __global__ void __launch_bounds__(512, 1) k_fa_small(Dev v, int L, int smask) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Grid-wide QP for ONE large instance (SURVEY §8f NEXT-3(iii) at c4 scale: a
+// quadcopter with T = 800 and 166 k rows took 50 ms per QP launch on one CTA).
+// Same OSQP iteration and chunked-scan recurrences as qp_scan_run (R1, R26), but
+// every k-parallel phase and the row phase run on the whole grid (cooperative
+// launch, grid barriers), each chunk's recurrence on its own CTA with the chunk's
+// Acl in shared memory, the boundary chains on CTA 0.  Cross-CTA vectors go
+// through L2 (ld.global.cg); the row phase reads dx and du~ from a shared-memory
+// copy.  Ten grid barriers per QP iteration.
+__device__ __forceinline__ unsigned long long qg_ld_acquire(const unsigned long long* p) {
+  unsigned long long x;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+  return x;
+}
+__device__ __forceinline__ void qg_barrier(unsigned long long* ctr, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+    while (qg_ld_acquire(ctr) < target) {
+    }
+  }
+  __syncthreads();
+}
+
+bool qp_grid_plan(const Dims& d, int nsm, int& M, int& C) {
+  static const int env = [] { const char* e = getenv("NRTO_QP_GRID"); return e ? atoi(e) : -1; }();
+  if (d.B != 1 || env == 0 || d.T < 8) return false;
+  const size_t base = ((size_t)(d.T + 1) * d.nx + (size_t)d.T * d.nx + 2 * (size_t)d.T * d.nu) * 8;
+  // large: many rows, or the one-CTA scan QP's vectors alone exceed its shared memory
+  if (env != 1 && d.ng < 16384 && base <= 150 * 1024) return false;
+  int m = (int)std::ceil(std::sqrt((double)d.T));
+  int c = (d.T + m - 1) / m;
+  while (c > nsm) { ++m; c = (d.T + m - 1) / m; }
+  M = m; C = c;
+  return true;
+}
+
+static size_t qg_smem(const Dims& d, int M, int C) {
+  const size_t nn = (size_t)d.nx * d.nx;
+  return ((size_t)M * nn + 2 * (size_t)C * nn + (size_t)M * d.nx + (size_t)(M + 1) * d.nx +
+          (size_t)(d.T + 1) * d.nx + (size_t)d.T * d.nu) * sizeof(double);
+}
+
+template <int NXM, int NUM>
+__global__ void __launch_bounds__(512, 1) k_qp_grid(Dev v, int engine, int l) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ double bcast;
+  const Dims d = v.d;
+  const int nx = NXM > 0 ? NXM : d.nx, nu = NUM > 0 ? NUM : d.nu, T = d.T, ng = d.ng;
+  const int b = 0, tid = threadIdx.x, nt = blockDim.x, G = gridDim.x, cta = blockIdx.x;
+  const int gtid = cta * nt + tid, gnt = G * nt;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int M = v.scanM, C = v.scanC, nn = nx * nx;
+  if (!v.active[b]) return;                          // uniform over the grid
+  const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
+  const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
+  const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp, aq = v.prm.alpha_qp;
+  const double den = rho + sq + rq, beta = rq / den;
+  const double rinv = (engine == NRTO_FULLADMM) ? 1.0 : 1.0 / rho;
+  const double* __restrict__ grad = v.grad;
+  const double* __restrict__ g0 = v.g0;
+  double* p = v.p; double* zl = v.zl; double* yl = v.yl; double* rp = v.rp;
+  const double* pt = v.pt; double* lam = v.lamp;
+  double* zb = v.zb; double* yb = v.yb; double* du = v.du;
+  double* gS = v.rx; double* gU = v.dut; double* gR = v.ru; double* gK = v.kff;
+  double* gdx = v.dxt; double* gs = v.qg_s; double* ga = v.qg_a;
+  const double* __restrict__ cu2 = v.cu2;
+  const double* __restrict__ Bm = v.Bm;
+  const double* __restrict__ Kf = F.Kf;
+  const double* __restrict__ Acl = F.Acl;
+  const double* __restrict__ Hi = F.Hinv;
+  const double* __restrict__ HB = F.HB;
+  const double rtr = v.rtrust[b];
+  // shared memory: my chunk's Acl, the boundary transfer matrices (CTA 0), chunk
+  // vectors, and the row phase's copies of dx and du~
+  double* sAc = sm;                                  // [M][nn]
+  double* sPb = sAc + (size_t)M * nn;                // [C][nn]
+  double* sPf = sPb + (size_t)C * nn;                // [C][nn]
+  double* sVa = sPf + (size_t)C * nn;                // [M][nx]   a_k / e_k of my chunk
+  double* sVs = sVa + (size_t)M * nx;                // [M+1][nx] chunk vector
+  double* sX = sVs + (size_t)(M + 1) * nx;           // [(T+1)][nx] dx (row phase)
+  double* sU = sX + (size_t)(T + 1) * nx;            // [T][nu]     du~ (row phase)
+  const int lo = cta * M, hi = min(T, (cta + 1) * M) - 1;
+  const bool mine = cta < C;
+  if (mine)
+    for (int r = tid; r < (hi - lo + 1) * nn; r += nt) sAc[r] = Acl[(int64_t)lo * nn + r];
+  if (cta == 0)
+    for (int r = tid; r < C * nn; r += nt) {
+      const int c = r / nn, e = r - c * nn;
+      sPb[r] = F.PhiB[(int64_t)(c * M) * nn + e];
+      sPf[r] = F.PhiF[(int64_t)(min(T, (c + 1) * M) - 1) * nn + e];
+    }
+  unsigned long long nbar = 0;
+  auto gsync = [&]() { qg_barrier(v.qg_bar, (++nbar) * (unsigned long long)G); };
+  for (int r = gtid; r < (T + 1) * nx; r += gnt) gS[r] = 0.0;
+  for (int r = gtid; r < T * nu; r += gnt) gU[r] = 0.0;
+  gsync();
+  const int nits = v.prm.qp_iters;
+  if (nits > 0) {
+    qp_rows<true, kRowBatch>(v, 0, ng, gtid, gnt, grad, g0, p, zl, yl, rp, pt, lam, sX, sU, gS, gU, true,
+                             rho, rq, sq, aq, den, beta, rinv);
+    gsync();
+  }
+  // one step of a chunk recurrence on warp 0: x_out = base + Mat x_in (x_in in smem)
+  auto step = [&](double base, const double* xin, const double* Mt, bool trans) {
+    return scan_step<NXM>(nx, lane, base, xin, [&](int i, int r) { return trans ? Mt[r * nx + i] : Mt[i * nx + r]; });
+  };
+  for (int it = 0; it < nits; ++it) {
+    // A: r_u (to gR) and a_k (to ga), s_T (to gs); S consumed and cleared
+    for (int r = gtid; r < T * nu; r += gnt) gR[r] = sq * __ldcg(du + r) + __ldcg(gU + r) + cu2[r];
+    for (int r = gtid; r < (T + 1) * nx; r += gnt) {
+      const int k = r / nx, i = r - k * nx;
+      double acc = (k > 0) ? __ldcg(gS + r) + rq * zb[r] - yb[r] : 0.0;
+      gS[r] = 0.0;
+      if (k < T) {
+        for (int m = 0; m < nu; ++m) {
+          const int q = k * nu + m;
+          const double ru = sq * __ldcg(du + q) + __ldcg(gU + q) + cu2[q];
+          acc -= Kf[(int64_t)k * nu * nx + m * nx + i] * ru;
+        }
+        ga[r] = acc;
+      } else {
+        gs[r] = acc;
+      }
+    }
+    gsync();
+    // B1: chunk-local backward recurrences (the last chunk from s_T: exact)
+    if (mine) {
+      for (int r = tid; r < (hi - lo + 1) * nx; r += nt) sVa[r] = __ldcg(ga + (int64_t)lo * nx + r);
+      if (tid < nx) sVs[(hi + 1 - lo) * nx + tid] = (cta == C - 1) ? __ldcg(gs + (int64_t)T * nx + tid) : 0.0;
+      __syncthreads();
+      if (warp == 0) {
+        for (int k = hi; k >= lo; --k) {
+          const double base = lane < nx ? sVa[(k - lo) * nx + lane] : 0.0;
+          const double x = step(base, sVs + (k + 1 - lo) * nx, sAc + (size_t)(k - lo) * nn, true);
+          __syncwarp();
+          if (lane < nx) sVs[(k - lo) * nx + lane] = x;
+          __syncwarp();
+        }
+        if (lane < nx) {
+          if (cta == C - 1)
+            for (int k = lo; k <= hi; ++k) gs[(int64_t)k * nx + lane] = sVs[(k - lo) * nx + lane];
+          else
+            gs[(int64_t)lo * nx + lane] = sVs[lane];
+        }
+      }
+    }
+    gsync();
+    // B2: chunk starts, last to first (CTA 0)
+    if (cta == 0 && warp == 0) {
+      double* xv = sVs;                               // [2][nx] ping-pong
+      if (lane < nx) xv[lane] = __ldcg(gs + (int64_t)(C - 1) * M * nx + lane);
+      __syncwarp();
+      for (int c = C - 2; c >= 0; --c) {
+        const double base = lane < nx ? __ldcg(gs + (int64_t)c * M * nx + lane) : 0.0;
+        const double x = step(base, xv, sPb + (size_t)c * nn, false);
+        __syncwarp();
+        if (lane < nx) { xv[lane] = x; gs[(int64_t)c * M * nx + lane] = x; }
+        __syncwarp();
+      }
+    }
+    gsync();
+    // B3: re-run each chunk's interior from its exact boundary s_{hi+1}
+    if (mine && cta < C - 1) {
+      if (tid < nx) sVs[(hi + 1 - lo) * nx + tid] = __ldcg(gs + (int64_t)(hi + 1) * nx + tid);
+      __syncthreads();
+      if (warp == 0) {
+        for (int k = hi; k > lo; --k) {
+          const double base = lane < nx ? sVa[(k - lo) * nx + lane] : 0.0;
+          const double x = step(base, sVs + (k + 1 - lo) * nx, sAc + (size_t)(k - lo) * nn, true);
+          __syncwarp();
+          if (lane < nx) { sVs[(k - lo) * nx + lane] = x; gs[(int64_t)k * nx + lane] = x; }
+          __syncwarp();
+        }
+      }
+    }
+    gsync();
+    // C: kff_k = H^-1 r_u,k + H^-1 B_k^T s_{k+1}, e_k = B_k kff_k (thread per k); U cleared
+    for (int k = gtid; k < T; k += gnt) {
+      double kf[NUM > 0 ? NUM : 32];
+      for (int m = 0; m < nu; ++m) {
+        double acc = 0.0;
+        for (int q = 0; q < nu; ++q) acc += Hi[((int64_t)k * nu + m) * nu + q] * __ldcg(gR + k * nu + q);
+        for (int i = 0; i < nx; ++i) acc += HB[((int64_t)k * nu + m) * nx + i] * __ldcg(gs + (int64_t)(k + 1) * nx + i);
+        kf[m] = acc;
+        gK[k * nu + m] = acc;
+        gU[k * nu + m] = 0.0;
+      }
+      for (int i = 0; i < nx; ++i) {
+        double acc = 0.0;
+        for (int m = 0; m < nu; ++m) acc += Bm[((int64_t)k * nx + i) * nu + m] * kf[m];
+        ga[(int64_t)k * nx + i] = acc;
+      }
+    }
+    gsync();
+    // D1: chunk-local forward recurrences (chunk 0 from dx_0 = 0: exact)
+    if (mine) {
+      for (int r = tid; r < (hi - lo + 1) * nx; r += nt) sVa[r] = __ldcg(ga + (int64_t)lo * nx + r);
+      if (tid < nx) sVs[tid] = 0.0;
+      __syncthreads();
+      if (warp == 0) {
+        for (int k = lo; k <= hi; ++k) {
+          const double base = lane < nx ? sVa[(k - lo) * nx + lane] : 0.0;
+          const double x = (k == lo) ? base : step(base, sVs + (k - lo) * nx, sAc + (size_t)(k - lo) * nn, false);
+          if (lane < nx) sVs[(k + 1 - lo) * nx + lane] = x;
+          __syncwarp();
+        }
+        if (lane < nx) {
+          if (cta == 0)
+            for (int k = 0; k <= hi + 1; ++k) gdx[(int64_t)k * nx + lane] = sVs[k * nx + lane];
+          else
+            gdx[(int64_t)(hi + 1) * nx + lane] = sVs[(hi + 1 - lo) * nx + lane];
+        }
+      }
+    }
+    gsync();
+    // D2: chunk ends, first to last (CTA 0)
+    if (cta == 0 && warp == 0) {
+      double* xv = sVs;
+      if (lane < nx) xv[lane] = __ldcg(gdx + (int64_t)min(T, M) * nx + lane);
+      __syncwarp();
+      for (int c = 1; c < C; ++c) {
+        const int h2 = min(T, (c + 1) * M) - 1;
+        const double base = lane < nx ? __ldcg(gdx + (int64_t)(h2 + 1) * nx + lane) : 0.0;
+        const double x = step(base, xv, sPf + (size_t)c * nn, false);
+        __syncwarp();
+        if (lane < nx) { xv[lane] = x; gdx[(int64_t)(h2 + 1) * nx + lane] = x; }
+        __syncwarp();
+      }
+    }
+    gsync();
+    // D3: re-run each chunk's interior from its exact boundary dx_lo
+    if (mine && cta > 0) {
+      if (tid < nx) sVs[tid] = __ldcg(gdx + (int64_t)lo * nx + tid);
+      __syncthreads();
+      if (warp == 0) {
+        for (int k = lo; k < hi; ++k) {
+          const double base = lane < nx ? sVa[(k - lo) * nx + lane] : 0.0;
+          const double x = step(base, sVs + (k - lo) * nx, sAc + (size_t)(k - lo) * nn, false);
+          if (lane < nx) { sVs[(k + 1 - lo) * nx + lane] = x; gdx[(int64_t)(k + 1) * nx + lane] = x; }
+          __syncwarp();
+        }
+      }
+    }
+    gsync();
+    // E: du~_k = kff_k - Kf_k dx_k, relaxed du
+    for (int r = gtid; r < T * nu; r += gnt) {
+      const int k = r / nu, m = r - k * nu;
+      double acc = __ldcg(gK + r);
+      for (int q = 0; q < nx; ++q) acc -= Kf[(int64_t)k * nu * nx + m * nx + q] * __ldcg(gdx + (int64_t)k * nx + q);
+      gR[r] = acc;
+      du[r] = aq * acc + (1.0 - aq) * __ldcg(du + r);
+    }
+    gsync();
+    // F: rows (gather B du~, update p, z, y, scatter the next w) on a shared-memory copy
+    //    of dx and du~; trust-region ball partial sums
+    for (int r = tid; r < (T + 1) * nx; r += nt) sX[r] = __ldcg(gdx + r);
+    for (int r = tid; r < T * nu; r += nt) sU[r] = __ldcg(gR + r);
+    __syncthreads();
+    const bool more = it + 1 < nits;
+    qp_rows<false, kRowBatch>(v, 0, ng, gtid, gnt, grad, g0, p, zl, yl, rp, pt, lam, sX, sU, gS, gU, more,
+                              rho, rq, sq, aq, den, beta, rinv);
+    double nbp = 0.0;
+    for (int r = gtid; r < (T + 1) * nx; r += gnt) {
+      const double zh = aq * sX[r] + (1.0 - aq) * zb[r];
+      const double w = zh + yb[r] / rq;
+      nbp += w * w;
+    }
+    nbp = block_sum(nbp, red);
+    if (tid == 0) v.qg_part[cta] = nbp;
+    gsync();
+    // G: ball scale from the CTA partials (fixed order), projection of the ball pair
+    if (warp == 0) {
+      double a = 0.0;
+      for (int q = lane; q < G; q += 32) a += __ldcg(v.qg_part + q);
+      a = warp_sum(a);
+      if (lane == 0) bcast = a;
+    }
+    __syncthreads();
+    {
+      const double nb = sqrt(bcast);
+      const double scl = (nb > rtr) ? rtr / nb : 1.0;
+      for (int r = gtid; r < (T + 1) * nx; r += gnt) {
+        const double zh = aq * sX[r] + (1.0 - aq) * zb[r];
+        const double zn = scl * (zh + yb[r] / rq);
+        yb[r] += rq * (zh - zn);
+        zb[r] = zn;
+      }
+    }
+    __syncthreads();
+  }
+  gsync();                                            // rows (p) of every CTA done
+  // dual update + residuals of the outer iteration (per-CTA partials, fixed order)
+  double ap = 0.0, ad = 0.0;
+  for (int j = gtid; j < ng; j += gnt) {
+    const double pj = __ldcg(p + j);
+    const double dp = pj - pt[j];
+    if (engine == NRTO_FULLADMM) {
+      lam[j] += dp;
+      v.tin[j] = pj + lam[j];
+    } else {
+      lam[j] += rho * dp;
+    }
+    ap += dp * dp;
+    const double dd = pt[j] - v.ptprev[j];
+    ad += dd * dd;
+    v.ptprev[j] = pt[j];
+  }
+  ap = block_sum(ap, red);
+  ad = block_sum(ad, red);
+  if (tid == 0) { v.qg_part[cta] = ap; v.qg_part[1024 + cta] = ad; }
+  gsync();
+  if (cta == 0 && warp == 0) {
+    double a1 = 0.0, a2 = 0.0;
+    for (int q = lane; q < G; q += 32) { a1 += __ldcg(v.qg_part + q); a2 += __ldcg(v.qg_part + 1024 + q); }
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    if (lane == 0) {
+      const double rpv = sqrt(a1), rdv = rho * sqrt(a2);
+      v.r_p[b] = rpv;
+      v.r_d[b] = rdv;
+      record_hist(v, b, l, rpv, rdv, engine);
+      v.iters[b] = l;
+      if (!isfinite(rpv) || !isfinite(rdv)) {
+        v.status[b] = NRTO_DIVERGED;
+        v.active[b] = 0;
+      } else if (!v.prm.fixed_iters && (l % v.prm.check_every) == 0 && rpv <= v.prm.eps_p &&
+                 rdv <= v.prm.eps_d) {
+        v.status[b] = NRTO_CONVERGED;
+        v.active[b] = 0;
+      }
+    }
+  }
+}
+
+int qp_grid_size(const nrto_handle_s* h) {
+  const Dev& v = h->dev;
+  if (!v.qpgrid) return 0;
+  const size_t smem = qg_smem(v.d, v.scanM, v.scanC);
+  if (smem > 220 * 1024) return 0;
+  void* kern = (v.d.nx == 12 && v.d.nu == 4) ? (void*)k_qp_grid<12, 4>
+             : (v.d.nx == 14 && v.d.nu == 7) ? (void*)k_qp_grid<14, 7> : (void*)k_qp_grid<0, 0>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int G = std::min(v.nsm * occ, 1024);
+  return G >= v.scanC ? G : 0;
+}
+
+static cudaError_t launch_qp_grid(nrto_handle_s* h, int engine, int l, cudaStream_t st) {
+  const Dev& v = h->dev;
+  cudaError_t e = cudaMemsetAsync(v.qg_bar, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(h->qp_grid);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = qg_smem(v.d, v.scanM, v.scanC);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (v.d.nx == 12 && v.d.nu == 4) e = cudaLaunchKernelEx(&cfg, k_qp_grid<12, 4>, v, engine, l);
+  else if (v.d.nx == 14 && v.d.nu == 7) e = cudaLaunchKernelEx(&cfg, k_qp_grid<14, 7>, v, engine, l);
+  else e = cudaLaunchKernelEx(&cfg, k_qp_grid<0, 0>, v, engine, l);
+  h->launches++;
+  return e;
+}
+
 // Chunked-scan QP usable for this launch (grid 0 / >= B: one CTA per instance):
 // returns its staging mask (-1: not usable).
 static int scan_stage(const nrto_handle_s* h, int grid) {
   const Dev& v = h->dev;
   static const int env = [] { const char* e = getenv("NRTO_QP_SCAN"); return e ? atoi(e) : 1; }();
   static const int menv = [] { const char* e = getenv("NRTO_QP_SCAN_STAGE"); return e ? atoi(e) : -1; }();
-  if (!env || v.scanC <= 0 || !v.fa.PhiB || v.d.B > kScanMaxBatch) return -1;
+  if (!env || v.scanC <= 0 || v.qpgrid || !v.fa.PhiB || v.d.B > kScanMaxBatch) return -1;
   if (grid > 0 && grid < v.d.B) return -1;
   const size_t lim = 220 * 1024;
   if (scan_smem(v.d, v.scanC, 0) > lim) return -1;
@@ -1958,6 +2336,7 @@ cudaError_t launch_fa_small(nrto_handle_s* h, int L, cudaStream_t st) {
 
 cudaError_t launch_qp_sparse(nrto_handle_s* h, int engine, int l, cudaStream_t st, int grid) {
   const Dims& d = h->dev.d;
+  if (h->dev.qpgrid && (grid == 0 || grid >= d.B)) return launch_qp_grid(h, engine, l, st);
   { const int sa = scan_stage(h, grid); if (sa >= 0) return launch_qp_scan(h, engine, l, sa, st); }
   const size_t smem = ((size_t)(d.T + 1) * d.nx + (size_t)kQPRing * d.nx * d.nx + kQPRing) * sizeof(double) +
                       (size_t)6 * (d.T + 1) * sizeof(int16_t);
@@ -1992,6 +2371,7 @@ static size_t qp_smem(const Dims& d, int stageA) {
 
 cudaError_t launch_qp(nrto_handle_s* h, int engine, int l, cudaStream_t st) {
   const Dims& d = h->dev.d;
+  if (h->dev.qpgrid) return launch_qp_grid(h, engine, l, st);
   { const int sa = scan_stage(h, 0); if (sa >= 0) return launch_qp_scan(h, engine, l, sa, st); }
   const size_t lim = 200 * 1024;
   int stageA = qp_smem(d, 1) <= lim;

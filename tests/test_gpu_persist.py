@@ -137,3 +137,27 @@ def test_small_instance_megakernel_termination_and_trace():
         o = oracle_run(shape, d, nrto.NRTO_FULLADMM, **kw)
         assert int(g["iters"][i]) == int(o["iters"]), i
         assert_parity(g, o, i=i)
+
+
+@pytest.mark.parametrize("case,eng", [("c1", 0), ("c3s", 0), ("c2", 1)])
+def test_grid_qp_matches_one_cta_qp(case, eng):
+    """The grid-wide QP (k_qp_grid, forced with NRTO_QP_GRID=1 on small single
+    instances) against the one-CTA chunked-scan QP on the same solves."""
+    a = _run_child(case, eng, NRTO_QP_GRID=1, NRTO_FA_SMALL=0)
+    b = _run_child(case, eng, NRTO_QP_GRID=0)
+    for sa, sb in zip(a, b):
+        for k in sa:
+            assert close(np.array(sa[k]), np.array(sb[k]), tol=1e-10), (case, eng, k)
+
+
+def test_grid_qp_large_instance_matches_oracle():
+    """A single quadcopter with 18.5 k rows (T = 60, 300 obstacles) takes the
+    grid-wide QP by default; FullADMM and NRTO-DR match the oracle."""
+    from gen.problems import make_quad
+    shape, data = make_quad(4, 2, T=60, n_obs=300)
+    assert shape.n_g >= 16384
+    for eng, kw in ((nrto.NRTO_FULLADMM, dict(max_iter=3, fixed_iters=1)),
+                    (nrto.NRTO_DR, dict(max_admm_iter=2, max_dr_iter=2, fixed_iters=1))):
+        g = gpu_solve(shape, single(shape, data), eng, **kw)
+        o = oracle_run(shape, data, eng, **kw)
+        assert_parity(g, o, engine=eng)
