@@ -302,6 +302,23 @@ nrto_err nrto_case_stats_read(nrto_handle h, int64_t* counts, int32_t L);
 
 nrto_err nrto_destroy(nrto_handle h);
 
+/* Workspace allocator ("an allocator hook lets the torch caching
+ * allocator back it").  By default a handle's device workspace -- everything
+ * nrto_setup / nrto_setup_general allocate for the handle's lifetime, ~70 KB per
+ * Franka instance plus the O(E) cone arrays -- comes from cudaMalloc / cudaFree.
+ * After nrto_set_allocator(alloc, release, ctx) every NEW handle allocates it with
+ * alloc(ctx, bytes, stream) (a device pointer, or NULL on failure ->
+ * NRTO_ENOMEM) and returns it with release(ctx, ptr, stream) in nrto_destroy (or
+ * on a failed setup); `stream` is the setup stream.  The callbacks are called on
+ * the calling thread, must not call back into nrto, and must keep the memory
+ * valid until release.  Existing handles keep the allocator they were created
+ * with.  alloc == NULL restores cudaMalloc / cudaFree.  Process-wide; not
+ * thread-safe against concurrent setups.  Small internal scratch (staging of
+ * host outputs, traces) stays on cudaMalloc. */
+typedef void* (*nrto_alloc_fn)(void* ctx, size_t bytes, void* stream);
+typedef void (*nrto_free_fn)(void* ctx, void* ptr, void* stream);
+nrto_err nrto_set_allocator(nrto_alloc_fn alloc, nrto_free_fn release, void* ctx);
+
 /* Thread-local message for the last non-OK return (never NULL). */
 const char* nrto_last_error(void);
 

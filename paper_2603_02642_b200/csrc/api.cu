@@ -69,16 +69,34 @@ extern "C" nrto_err nrto_layout(const nrto_shape* s, int64_t* E_out, int64_t* of
   return NRTO_OK;
 }
 
+// process-wide workspace allocator (nrto_set_allocator)
+static nrto_alloc_fn g_alloc_fn = nullptr;
+static nrto_free_fn g_free_fn = nullptr;
+static void* g_alloc_ctx = nullptr;
+
+extern "C" nrto_err nrto_set_allocator(nrto_alloc_fn alloc, nrto_free_fn release, void* ctx) {
+  if (alloc && !release) return fail(NRTO_EINVAL, "an allocator needs its release function");
+  g_alloc_fn = alloc;
+  g_free_fn = alloc ? release : nullptr;
+  g_alloc_ctx = alloc ? ctx : nullptr;
+  return NRTO_OK;
+}
+
 template <class T>
 static nrto_err dalloc(nrto_handle_s* h, T** p, int64_t n) {
   if (h->nallocs >= (int)(sizeof(h->allocs) / sizeof(h->allocs[0])))
     return fail(NRTO_ENOMEM, "too many allocations");
   void* q = nullptr;
   const size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
-  cudaError_t e = cudaMalloc(&q, bytes);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(NRTO_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  if (h->alloc_fn) {
+    q = h->alloc_fn(h->alloc_ctx, bytes, h->alloc_stream);
+    if (!q) return fail(NRTO_ENOMEM, "allocator hook returned NULL for " + std::to_string(bytes) + " bytes");
+  } else {
+    cudaError_t e = cudaMalloc(&q, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(NRTO_ENOMEM, "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    }
   }
   h->allocs[h->nallocs++] = q;
   *p = (T*)q;
@@ -86,7 +104,10 @@ static nrto_err dalloc(nrto_handle_s* h, T** p, int64_t n) {
 }
 
 static void free_all(nrto_handle_s* h) {
-  for (int i = 0; i < h->nallocs; ++i) cudaFree(h->allocs[i]);
+  for (int i = 0; i < h->nallocs; ++i) {
+    if (h->free_fn) h->free_fn(h->alloc_ctx, h->allocs[i], h->alloc_stream);
+    else cudaFree(h->allocs[i]);
+  }
   h->nallocs = 0;
 }
 
@@ -117,6 +138,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
 
   auto* h = new nrto_handle_s();
   h->stream = st;
+  h->alloc_fn = g_alloc_fn; h->free_fn = g_free_fn; h->alloc_ctx = g_alloc_ctx; h->alloc_stream = stream;
   Dev& v = h->dev;
   Dims& d = v.d;
   d.nx = s->n_x; d.nu = s->n_u; d.T = s->T; d.ng = s->n_g; d.B = s->batch;

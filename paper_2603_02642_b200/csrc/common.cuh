@@ -164,6 +164,10 @@ struct GenState {
 struct nrto_prof_rec { int cls; cudaEvent_t a, b; };
 
 struct nrto_handle_s {
+  nrto_alloc_fn alloc_fn = nullptr;   // workspace allocator of this handle (nullptr: cudaMalloc)
+  nrto_free_fn free_fn = nullptr;
+  void* alloc_ctx = nullptr;
+  void* alloc_stream = nullptr;
   double* hist_buf = nullptr;   // device residual-trace buffer (grown on demand)
   size_t hist_cap = 0;
   int tma_margin = 0;      // k_fa_tma launch mode: 1 = finish margins (||C^L b + b_hat||)

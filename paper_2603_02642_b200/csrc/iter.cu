@@ -316,7 +316,10 @@ __global__ void k_dr_gain(Dev v) {
 //   pi = (sigma pi~ + rho p + lambda + r_s t~)/(rho + sigma + r_s)  (p~ part of (11a))
 //   s = (pi, a), a = A_hat k + b_hat ; s_ref = 2 s - s~ ; s~ += alpha (Pi(s_ref) - s)
 //   pi~ += alpha (pi - pi~) ; r_dr partial = ||s~_new - s~||^2
-__global__ void k_dr_pass(Dev v) {
+// NUM > 0: n_u fixed at compile time; the element loops are unrolled so that a
+// lane keeps several elements' loads in flight (long c4 cones: 9.6 k elements).
+template <int NUM>
+__global__ void __launch_bounds__(256) k_dr_pass(Dev v) {
   const Dims d = v.d;
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= (int64_t)d.B * d.ng) return;
@@ -328,7 +331,7 @@ __global__ void k_dr_pass(Dev v) {
     for (int64_t e = (int64_t)j * 32 + (threadIdx.x & 31); e < nz; e += (int64_t)d.ng * 32) Zb[e] = 0.0;
   }
   const int lane = threadIdx.x & 31;
-  const int nx = d.nx, nu = d.nu;
+  const int nx = d.nx, nu = NUM > 0 ? NUM : d.nu;
   const ConeGeom g = cone_geom(v, j);
   const int64_t ij = (int64_t)b * d.ng + j;
   const double sg = v.prm.sigma_dr, rs = v.prm.r_s, al = v.prm.alpha_dr, rho = v.prm.rho_admm;
@@ -339,13 +342,19 @@ __global__ void k_dr_pass(Dev v) {
   const double* Bd = v.Bd + (int64_t)b * d.EB + g.offB;
   const double* Cm = v.Ccur + (int64_t)b * d.T * nx * nu;
   double n2 = 0.0;
+#pragma unroll 4
   for (int e = lane; e < g.L; e += 32) {
     const int kb = e / nx, i = e - kb * nx;
     double a = (g.kind == 0) ? bh[e] : 0.0;
     if (kb < g.nbB) {
       const double* Cr = Cm + ((int64_t)(g.klo + kb) * nx + i) * nu;
       const double* br = Bd + kb * d.nup;
-      for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
+      if constexpr (NUM > 0) {
+#pragma unroll
+        for (int m = 0; m < NUM; ++m) a += __ldg(Cr + m) * __ldg(br + m);
+      } else {
+        for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
+      }
     }
     const double er = 2.0 * a - Y[e];
     n2 += er * er;
@@ -354,13 +363,19 @@ __global__ void k_dr_pass(Dev v) {
   double sc;
   const double tpi = soc_case(2.0 * pi - tt, sqrt(n2), &sc);
   double d2 = 0.0;
+#pragma unroll 4
   for (int e = lane; e < g.L; e += 32) {
     const int kb = e / nx, i = e - kb * nx;
     double a = (g.kind == 0) ? bh[e] : 0.0;
     if (kb < g.nbB) {
       const double* Cr = Cm + ((int64_t)(g.klo + kb) * nx + i) * nu;
       const double* br = Bd + kb * d.nup;
-      for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
+      if constexpr (NUM > 0) {
+#pragma unroll
+        for (int m = 0; m < NUM; ++m) a += __ldg(Cr + m) * __ldg(br + m);
+      } else {
+        for (int m = 0; m < nu; ++m) a += Cr[m] * br[m];
+      }
     }
     const double et = Y[e];
     const double er = 2.0 * a - et;
@@ -788,7 +803,9 @@ cudaError_t launch_dr_pass(nrto_handle_s* h, cudaStream_t st) {
       else if (d.nu == 7) k_dr_pass_s<7><<<grid, 128, smem, st>>>(v, lmax);
       else k_dr_pass_s<0><<<grid, 128, smem, st>>>(v, lmax);
     } else {
-      k_dr_pass<<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(v);
+      if (d.nu == 4) k_dr_pass<4><<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(v);
+      else if (d.nu == 7) k_dr_pass<7><<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(v);
+      else k_dr_pass<0><<<warp_grid((int64_t)d.B * d.ng, 8), 256, 0, st>>>(v);
     }
     h->launches++;
   }

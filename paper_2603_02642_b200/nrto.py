@@ -101,10 +101,59 @@ def lib():
                   "nrto_soc_project", "nrto_destroy", "nrto_refresh", "nrto_profile_enable",
                   "nrto_profile_read", "nrto_pass_bytes", "nrto_case_stats_enable",
                   "nrto_case_stats_read", "nrto_solve_begin", "nrto_solve_iterate",
-                  "nrto_solve_flags", "nrto_solve_end", "nrto_setup_general"):
+                  "nrto_solve_flags", "nrto_solve_end", "nrto_setup_general", "nrto_set_allocator"):
             getattr(L, f).restype = C.c_int
+        L.nrto_set_allocator.argtypes = [ALLOC_FN, FREE_FN, C.c_void_p]
         _lib = L
     return _lib
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+_alloc_cbs = None      # keeps the ctypes callbacks alive while registered
+
+
+def nrto_set_allocator(alloc, release):
+    """Register Python callables alloc(bytes, stream_ptr) -> device ptr (int) and
+    release(ptr, stream_ptr) as the workspace allocator of new handles (nrto.h);
+    alloc=None restores cudaMalloc / cudaFree."""
+    global _alloc_cbs
+    if alloc is None:
+        _check(lib().nrto_set_allocator(ALLOC_FN(), FREE_FN(), None))
+        _alloc_cbs = None
+        return
+
+    def a(ctx, nbytes, stream):
+        try:
+            return int(alloc(int(nbytes), stream or 0)) or None
+        except Exception:
+            return None
+
+    def r(ctx, ptr, stream):
+        try:
+            release(int(ptr), stream or 0)
+        except Exception:
+            pass
+
+    cbs = (ALLOC_FN(a), FREE_FN(r))
+    _check(lib().nrto_set_allocator(cbs[0], cbs[1], None))
+    _alloc_cbs = cbs
+
+
+def use_torch_allocator(enable=True):
+    """Back the workspace of new handles with torch's CUDA caching allocator."""
+    if not enable:
+        nrto_set_allocator(None, None)
+        return
+    import torch
+
+    def a(nbytes, stream):
+        return torch.cuda.caching_allocator_alloc(nbytes, stream=stream or None)
+
+    def r(ptr, stream):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    nrto_set_allocator(a, r)
 
 
 def _check(code):

@@ -90,3 +90,12 @@ int main(){printf("%zu %zu %zu %zu\n", sizeof(nrto_shape), sizeof(nrto_data), si
         sizes = list(map(int, subprocess.run([exe], capture_output=True, text=True).stdout.split()))
     assert sizes == [C.sizeof(nrto.nrto_shape), C.sizeof(nrto.nrto_data),
                      C.sizeof(nrto.nrto_params), C.sizeof(nrto.nrto_out)]
+
+
+def test_set_allocator_validation():
+    """nrto_set_allocator: an alloc without a release is rejected; NULL restores the
+    default (host-only entry point, no device call)."""
+    from paper_2603_02642_b200 import nrto
+    L = nrto.lib()
+    assert L.nrto_set_allocator(nrto.ALLOC_FN(lambda c, n, s: None), nrto.FREE_FN(), None) == nrto.NRTO_EINVAL
+    assert L.nrto_set_allocator(nrto.ALLOC_FN(), nrto.FREE_FN(), None) == nrto.NRTO_OK

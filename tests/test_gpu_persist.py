@@ -161,3 +161,27 @@ def test_grid_qp_large_instance_matches_oracle():
         g = gpu_solve(shape, single(shape, data), eng, **kw)
         o = oracle_run(shape, data, eng, **kw)
         assert_parity(g, o, engine=eng)
+
+
+def test_torch_caching_allocator_backs_the_workspace():
+    """nrto_set_allocator with torch's caching allocator: the handle's workspace is
+    torch memory while the handle lives, results equal the cudaMalloc handle's."""
+    shape, data = CASES["c3s"]()
+    kw = dict(max_iter=6, fixed_iters=1)
+    ref = gpu_solve(shape, single(shape, data), nrto.NRTO_FULLADMM, **kw)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    nrto.use_torch_allocator(True)
+    try:
+        s = nrto.InnerSolver(shape, nrto.to_tensors(single(shape, data), device="cuda"), **kw)
+        held = torch.cuda.memory_allocated() - before
+        out = s.solve(nrto.NRTO_FULLADMM)
+        torch.cuda.synchronize()
+        g = {k: v.cpu().numpy() for k, v in out.items()}
+        del out
+        s.close()
+    finally:
+        nrto.use_torch_allocator(False)
+    assert held > 1_000_000, held                       # workspace came from torch
+    for k in ("kv", "du", "p", "p_tilde", "lam_p", "objective"):   # atomics: last-bit order only
+        assert close(g[k], ref[k], tol=1e-12), k
