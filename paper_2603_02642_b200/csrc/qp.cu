@@ -1408,6 +1408,9 @@ static size_t scan_smem(const Dims& d, int C, int smask) {
   return n * sizeof(double);
 }
 
+// debug phase clocks of the scan QP (instance 0, QP iterations 0-1): g_qp_clk[it*32 + ph]
+#define SCAN_CLK(ph) \
+  do { if (b == 0 && tid == 0 && it < 2) g_qp_clk[it * 32 + (ph)] = clock64(); } while (0)
 template <int NXM, int NUM>
 __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int smask, int b, double* sm,
                                             double* red) {
@@ -1497,11 +1500,12 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
     __syncthreads();
   }
   for (int it = 0; it < nits; ++it) {
+    SCAN_CLK(0);
     for (int r = tid; r < T * nu; r += nt) {          // r_u (consumes and clears U)
       sR[r] = sq * du[r] + ldacc(gU + r) + cu2[r];    // cu2 = -2 R_u u_hat (setup)
       gU[r] = 0.0;
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(1);
     for (int r = tid; r < (T + 1) * nx; r += nt) {    // r_x and a_k (consumes and clears S)
       const int k = r / nx, i = r - k * nx;
       double acc = (k > 0) ? ldacc(gS + r) + rq * zb[r] - yb[r] : 0.0;
@@ -1514,7 +1518,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
       if (k < T) sA[r] = acc;                         // a_k
       else sS[r] = acc;                               // s_T
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(2);
     if (warp < C) {                                   // chunk-local backward recurrences
       const int lo = warp * M, hi = min(T, (warp + 1) * M) - 1;
       for (int k = hi; k >= lo; --k) {
@@ -1530,7 +1534,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         __syncwarp();
       }
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(3);
     if (warp == 0) {                                  // chunk boundaries, last to first
       for (int c = C - 2; c >= 0; --c) {
         const double* P = sPb + c * nn;
@@ -1542,7 +1546,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         __syncwarp();
       }
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(4);
     if (!rescan) {
       for (int r = tid; r < T * nx; r += nt) {        // interior fix-up s_k += PhiB_k s_{hi+1}
         const int k = r / nx, i = r - k * nx, c = k / M;
@@ -1563,7 +1567,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         __syncwarp();
       }
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(5);
     for (int r = tid; r < T * nu; r += nt) {          // kff_k = H^-1 r_u,k + H^-1 B_k^T s_{k+1}
       const int k = r / nu, m = r - k * nu;
       const double* H = Hi + (int64_t)k * nu * nu + m * nu;
@@ -1574,14 +1578,14 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
       acc = dotn<NXM>(nx, [&](int q) { return hb[q]; }, [&](int q) { return sk[q]; }, acc);
       sK[r] = acc;
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(6);
     for (int r = tid; r < T * nx; r += nt) {          // e_k = B_k kff_k
       const int k = r / nx, i = r - k * nx;
       const double* Bk = Bm + (int64_t)k * nx * nu + i * nu;
       const double* kk = sK + k * nu;
       sA[r] = dotn<NUM>(nu, [&](int m) { return Bk[m]; }, [&](int m) { return kk[m]; }, 0.0);
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(7);
     if (warp < C) {                                   // chunk-local forward recurrences
       const int lo = warp * M, hi = min(T, (warp + 1) * M) - 1;
       if (warp == 0 && lane < nx) sS[lane] = 0.0;     // dx_0 = 0
@@ -1596,7 +1600,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         __syncwarp();
       }
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(8);
     if (warp == 0) {                                  // chunk boundaries, first to last
       for (int c = 1; c < C; ++c) {
         const int hi = min(T, (c + 1) * M) - 1;
@@ -1609,7 +1613,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         __syncwarp();
       }
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(9);
     if (!rescan) {
       for (int r = tid; r < T * nx; r += nt) {        // interior fix-up dx_{k+1} += PhiF_k dx_lo
         const int k = r / nx, i = r - k * nx, c = k / M;
@@ -1630,7 +1634,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         __syncwarp();
       }
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(10);
     for (int r = tid; r < T * nu; r += nt) {          // du~_k = kff_k - Kf_k dx_k ; relaxed du
       const int k = r / nu, m = r - k * nu;
       const double* Kk = Kf + (int64_t)k * nu * nx + m * nx;
@@ -1639,11 +1643,11 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
       sR[r] = dd;
       du[r] = aq * dd + (1.0 - aq) * du[r];
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(11);
     const bool more = it + 1 < nits;
     qp_rows<false, kRowBatch>(v, bg, ng, tid, nt, grad, g0, p, zl, yl, rp, pt, lam, sS, sR, gS, gU, more,
                               rho, rq, sq, aq, den, beta, rinv);
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(12);
     double nb = 0.0;                                  // trust-region ball
     for (int r = tid; r < (T + 1) * nx; r += nt) {
       const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
@@ -1659,7 +1663,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
       yb[r] += rq * (zh - zn);
       zb[r] = zn;
     }
-    __syncthreads();
+    __syncthreads(); SCAN_CLK(13);
   }
   if (res) {                                          // resident vectors back to global
     for (int r = tid; r < ng; r += nt) { p_g[r] = p[r]; zl_g[r] = zl[r]; yl_g[r] = yl[r]; }
