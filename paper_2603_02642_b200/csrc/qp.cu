@@ -486,6 +486,9 @@ __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int ti
                                         double* gS, double* gU, bool more, double rho, double rq,
                                         double sq, double aq, double den, double beta,
                                         double rinv) {
+  // reciprocals instead of FP64 divisions in the per-row updates (a division is a
+  // ~40-instruction Newton sequence; <= 1 ulp different per operation)
+  const double iden = 1.0 / den, irq = 1.0 / rq;
   // vv[j] = v_j = p~_j - lam_j rinv, constant over the QP iterations of a launch
   // (formed in the FIRST pass); rhs_p,j = sq p_j + rho v_j + rq z_j - y_j is
   // recomputed from the row's current (p, z, y) instead of being stored.
@@ -527,10 +530,10 @@ __device__ __forceinline__ void qp_rows(const Dev& v, int64_t bg, int ng, int ti
           for (int i = 0; i < n; ++i) bd += gj[i] * x[i];
         }
         const double r0 = sq * pj[u] + rho * vj[u] + rq * zlj[u] - ylj[u];
-        const double ptl = (r0 - rq * bd) / den;
+        const double ptl = (r0 - rq * bd) * iden;
         pn = aq * ptl + (1.0 - aq) * pj[u];
         const double zh = aq * (bd + ptl) + (1.0 - aq) * zlj[u];
-        zn = nan_min(zh + ylj[u] / rq, -g0j[u]);
+        zn = nan_min(zh + ylj[u] * irq, -g0j[u]);
         yn = ylj[u] + rq * (zh - zn);
         p[j] = pn; zl[j] = zn; yl[j] = yn;
       }
@@ -583,6 +586,9 @@ __device__ __forceinline__ void qp_rows_pipe(const Dev& v, int64_t bg, int ng, i
                                              volatile int16_t* fx, volatile int16_t* fu, int16_t ep,
                                              double rho, double rq,
                                              double sq, double aq, double den, double beta) {
+  // reciprocals instead of FP64 divisions in the per-row updates (a division is a
+  // ~40-instruction Newton sequence; <= 1 ulp different per operation)
+  const double iden = 1.0 / den, irq = 1.0 / rq;
   const int nx = v.d.nx, nu = v.d.nu;
   const int4* __restrict__ rows = v.rowpk + bg;
   const double* __restrict__ gval = v.gval + bg * kRowNZ;
@@ -631,10 +637,10 @@ __device__ __forceinline__ void qp_rows_pipe(const Dev& v, int64_t bg, int ng, i
         }
       }
       const double r0 = sq * pj[u] + rho * vj[u] + rq * zlj[u] - ylj[u];
-      const double ptl = (r0 - rq * bd) / den;
+      const double ptl = (r0 - rq * bd) * iden;
       const double pn = aq * ptl + (1.0 - aq) * pj[u];
       const double zh = aq * (bd + ptl) + (1.0 - aq) * zlj[u];
-      const double zn = nan_min(zh + ylj[u] / rq, -g0j[u]);
+      const double zn = nan_min(zh + ylj[u] * irq, -g0j[u]);
       const double yn = ylj[u] + rq * (zh - zn);
       p[j] = pn; zl[j] = zn; yl[j] = yn;
       if (more) {
@@ -724,7 +730,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
   const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
   const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
   const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp, aq = v.prm.alpha_qp;
-  const double den = rho + sq + rq, beta = rq / den;
+  const double den = rho + sq + rq, beta = rq / den, irq = 1.0 / rq;
   const int64_t bg = (int64_t)b * ng;
   const double* __restrict__ grad = v.grad + bg * nx;
   const double* __restrict__ g0 = v.g0 + bg;
@@ -1022,7 +1028,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
             if (k0 + 4 >= T) qp_spin(&fx[T], ep);
             for (int r = k0 * nx + lane; r < r1; r += 32) {
               const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
-              const double w = zh + yb[r] / rq;
+              const double w = zh + yb[r] * irq;
               nbp += w * w;
             }
           }
@@ -1042,7 +1048,7 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
         const double scl = (nb > rtr) ? rtr / nb : 1.0;
         for (int r = tid; r < (T + 1) * nx; r += nt) {
           const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
-          const double zn = scl * (zh + yb[r] / rq);
+          const double zn = scl * (zh + yb[r] * irq);
           yb[r] += rq * (zh - zn);
           zb[r] = zn;
         }
@@ -1240,14 +1246,14 @@ __device__ __forceinline__ void qp_instance(const Dev& v, int engine, int l, int
     for (int r = tid; r < (T + 1) * nx; r += nt) {
       const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
       sS[r] = zh;
-      const double w = zh + yb[r] / rq;
+      const double w = zh + yb[r] * irq;
       nb += w * w;
     }
     nb = sqrt(block_sum(nb, red));
     const double scl = (nb > rtr) ? rtr / nb : 1.0;
     for (int r = tid; r < (T + 1) * nx; r += nt) {
       const double zh = sS[r];
-      const double zn = scl * (zh + yb[r] / rq);
+      const double zn = scl * (zh + yb[r] * irq);
       yb[r] += rq * (zh - zn);
       zb[r] = zn;
     }
@@ -1423,7 +1429,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
   const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
   const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
   const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp, aq = v.prm.alpha_qp;
-  const double den = rho + sq + rq, beta = rq / den;
+  const double den = rho + sq + rq, beta = rq / den, irq = 1.0 / rq;
   const int64_t bg = (int64_t)b * ng;
   const double* __restrict__ grad = v.grad + bg * nx;
   const double* __restrict__ g0 = v.g0 + bg;
@@ -1528,7 +1534,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         const double x = (k == hi && warp != C - 1)
                              ? base
                              : scan_step<NXM>(nx, lane, base, sS + (k + 1) * nx,
-                                              [&](int i, int r) { return Ak[r * nx + i]; });
+                                               [&](int i, int r) { return Ak[r * nx + i]; });
         __syncwarp();
         if (lane < nx) sS[k * nx + lane] = x;
         __syncwarp();
@@ -1540,7 +1546,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         const double* P = sPb + c * nn;
         const double base = lane < nx ? sS[c * M * nx + lane] : 0.0;
         const double x = scan_step<NXM>(nx, lane, base, sS + (c + 1) * M * nx,
-                                        [&](int i, int r) { return P[i * nx + r]; });
+                                         [&](int i, int r) { return P[i * nx + r]; });
         __syncwarp();
         if (lane < nx) sS[c * M * nx + lane] = x;
         __syncwarp();
@@ -1595,7 +1601,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         // x~_lo = 0 (slot lo belongs to the previous chunk's warp)
         const double x = (k == lo) ? base
                                    : scan_step<NXM>(nx, lane, base, sS + k * nx,
-                                                    [&](int i, int r) { return Ak[i * nx + r]; });
+                                                     [&](int i, int r) { return Ak[i * nx + r]; });
         if (lane < nx) sS[(k + 1) * nx + lane] = x;
         __syncwarp();
       }
@@ -1607,7 +1613,7 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
         const double* P = sPf + c * nn;
         const double base = lane < nx ? sS[(hi + 1) * nx + lane] : 0.0;
         const double x = scan_step<NXM>(nx, lane, base, sS + c * M * nx,
-                                        [&](int i, int r) { return P[i * nx + r]; });
+                                         [&](int i, int r) { return P[i * nx + r]; });
         __syncwarp();
         if (lane < nx) sS[(hi + 1) * nx + lane] = x;
         __syncwarp();
@@ -1652,14 +1658,14 @@ __device__ __forceinline__ void qp_scan_run(const Dev& v, int engine, int l, int
     for (int r = tid; r < (T + 1) * nx; r += nt) {
       const double zh = aq * sS[r] + (1.0 - aq) * zb[r];
       sS[r] = zh;
-      const double w = zh + yb[r] / rq;
+      const double w = zh + yb[r] * irq;
       nb += w * w;
     }
     nb = sqrt(block_sum(nb, red));
     const double scl = (nb > rtr) ? rtr / nb : 1.0;
     for (int r = tid; r < (T + 1) * nx; r += nt) {
       const double zh = sS[r];
-      const double zn = scl * (zh + yb[r] / rq);
+      const double zn = scl * (zh + yb[r] * irq);
       yb[r] += rq * (zh - zn);
       zb[r] = zn;
     }
@@ -1886,7 +1892,7 @@ __global__ void __launch_bounds__(512, 1) k_qp_grid(Dev v, int engine, int l) {
   const EngineFactors& F = engine == NRTO_FULLADMM ? v.fa : v.dr;
   const double rho = engine == NRTO_FULLADMM ? v.prm.rho : v.prm.rho_admm;
   const double rq = v.prm.rho_qp, sq = v.prm.sigma_qp, aq = v.prm.alpha_qp;
-  const double den = rho + sq + rq, beta = rq / den;
+  const double den = rho + sq + rq, beta = rq / den, irq = 1.0 / rq;
   const double rinv = (engine == NRTO_FULLADMM) ? 1.0 : 1.0 / rho;
   const double* __restrict__ grad = v.grad;
   const double* __restrict__ g0 = v.g0;
@@ -2094,7 +2100,7 @@ __global__ void __launch_bounds__(512, 1) k_qp_grid(Dev v, int engine, int l) {
     double nbp = 0.0;
     for (int r = gtid; r < (T + 1) * nx; r += gnt) {
       const double zh = aq * sX[r] + (1.0 - aq) * zb[r];
-      const double w = zh + yb[r] / rq;
+      const double w = zh + yb[r] * irq;
       nbp += w * w;
     }
     nbp = block_sum(nbp, red);
@@ -2113,7 +2119,7 @@ __global__ void __launch_bounds__(512, 1) k_qp_grid(Dev v, int engine, int l) {
       const double scl = (nb > rtr) ? rtr / nb : 1.0;
       for (int r = gtid; r < (T + 1) * nx; r += gnt) {
         const double zh = aq * sX[r] + (1.0 - aq) * zb[r];
-        const double zn = scl * (zh + yb[r] / rq);
+        const double zn = scl * (zh + yb[r] * irq);
         yb[r] += rq * (zh - zn);
         zb[r] = zn;
       }
@@ -2226,7 +2232,6 @@ static int scan_stage(const nrto_handle_s* h, int grid) {
     const int b = order[q];
     if (b == 4 && v.scanM >= 8) continue;          // long chunks re-scan: no transfer matrices
     if (scan_smem(v.d, v.scanC, mask | (1 << b)) <= std::min(lim, cap)) mask |= 1 << b;
-    else if (b == 0) break;          // without Acl in shared memory stage nothing else
   }
   return mask;
 }
