@@ -300,6 +300,34 @@ nrto_err nrto_solve_end(nrto_handle h, const nrto_out* out, void* stream);
 nrto_err nrto_case_stats_enable(nrto_handle h, int32_t enable);
 nrto_err nrto_case_stats_read(nrto_handle h, int64_t* counts, int32_t L);
 
+/* Cone sharding of ONE instance over ranks: a handle set
+ * up on the whole problem (nrto_setup) keeps the setup, the gain factors and the
+ * QP over all rows (replicated on every rank), but after nrto_shard_cones its DR
+ * pass and adjoint cover cones [cone_lo, cone_hi) only (cone_lo <= cone_hi <=
+ * n_g; NRTO_EINVAL otherwise or for a general-set handle).  Synchronises the
+ * device.  Such a handle is driven by the NRTO-ADMM + DR engine through
+ *   nrto_solve_begin(h, NRTO_DR, s)
+ *   for l = 1..L_admm:  nrto_dr_step(h, 0, l, s)                  (arm)
+ *     for m = 1..L_dr:  nrto_dr_step(h, 1, l, s)                  (affine prox (11a))
+ *                       nrto_dr_step(h, 2, l, s)                  (my cones: pass (11b/c),
+ *                                                                  adjoint partial, r_dr partial)
+ *                       caller: allreduce(SUM) of buffer 0 (Z)    over the ranks
+ *     caller: zero buffer 1 (pi) outside [cone_lo, cone_hi), allreduce(SUM) it
+ *     nrto_dr_step(h, 3, l, s)                                    (QP (5b) + (5c))
+ *   nrto_solve_end(h, out, s)
+ * (fixed iteration counts; the DR stop test needs the r_dr partials of buffer 2
+ * summed over ranks and is the caller's).  Per-instance outputs are replicated;
+ * per-cone outputs are valid for the rank's own cones.  nrto_inner_solve and
+ * nrto_refresh return NRTO_EINVAL on a sharded handle.  nrto_dr_step: NRTO_ESTATE outside
+ * nrto_solve_begin(NRTO_DR) .. nrto_solve_end, NRTO_EINVAL for a bad phase / l;
+ * asynchronous on `stream`. */
+nrto_err nrto_shard_cones(nrto_handle h, int32_t cone_lo, int32_t cone_hi);
+nrto_err nrto_dr_step(nrto_handle h, int32_t phase, int32_t l, void* stream);
+/* Device buffers of a handle for a caller's collectives (owned by the handle):
+ * which = 0: Z [b][T][n_u][n_x] adjoint accumulator; 1: pi / p~ [b][n_g];
+ * 2: r_dr partial squares per cone [b][n_g].  *count = doubles. */
+nrto_err nrto_buffer(nrto_handle h, int32_t which, double** ptr, int64_t* count);
+
 nrto_err nrto_destroy(nrto_handle h);
 
 /* Workspace allocator ("an allocator hook lets the torch caching

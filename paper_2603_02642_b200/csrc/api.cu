@@ -282,6 +282,7 @@ extern "C" nrto_err nrto_setup(const nrto_shape* s, const nrto_data* data,
   AL(v.U, B * T * nx * nx); AL(v.Ulam, B * T * nx); AL(v.Urep, B * T); AL(v.psame, B * T);
   v.scanM = 0; v.scanC = 0;
   v.qpgrid = 0; v.qg_s = nullptr; v.qg_a = nullptr; v.qg_part = nullptr; v.qg_bar = nullptr;
+  v.cone_lo = 0; v.cone_hi = ng;
   if (B <= kScanMaxBatch && T >= 2 && nx <= 32 && nu <= 32) {
     // one large instance (many rows or a horizon whose QP vectors exceed one CTA's
     // shared memory): the grid-wide QP with its own chunking; else the one-CTA scan QP
@@ -374,6 +375,7 @@ extern "C" nrto_err nrto_refresh(nrto_handle h, const nrto_data* data, void* str
   if (!data) return fail(NRTO_EINVAL, "data is NULL");
   if (h->general && !h->gen_refresh_ok)
     return fail(NRTO_EINVAL, "nrto_refresh of a general-set handle: call nrto_setup_general again");
+  if (h->sharded) return fail(NRTO_EINVAL, "nrto_refresh of a cone-sharded handle: set it up again");
   Dev& v = h->dev;
   const Dims& d = v.d;
   const int ng = d.ng, T = d.T, nx = d.nx, nu = d.nu;
@@ -492,6 +494,7 @@ extern "C" nrto_err nrto_inner_solve(nrto_handle h, int32_t engine, const nrto_o
   if (!h) return fail(NRTO_ESTATE, "handle is NULL");
   if (!o) return fail(NRTO_EINVAL, "out is NULL");
   if (engine != NRTO_FULLADMM && engine != NRTO_DR) return fail(NRTO_EINVAL, "unknown engine");
+  if (h->sharded) return fail(NRTO_EINVAL, "cone-sharded handle: drive it with nrto_solve_begin / nrto_dr_step / nrto_solve_end");
   cudaStream_t st = (cudaStream_t)stream;
   Dev& v = h->dev;
   const Dims& d = v.d;
@@ -1035,6 +1038,78 @@ extern "C" nrto_err nrto_solve_flags(nrto_handle h, double* flags, void* stream)
   if (!h) return fail(NRTO_ESTATE, "handle is NULL");
   if (!flags) return fail(NRTO_EINVAL, "flags is NULL");
   CK(launch_solve_flags(h, flags, (cudaStream_t)stream));
+  return NRTO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Cone sharding of one instance over ranks: the handle
+// keeps the whole problem (setup, gain factors and QP over all rows, replicated on
+// every rank) but its DR pass and adjoint cover cones [cone_lo, cone_hi) only; the
+// caller sums the adjoint partials Z over ranks after every pass and gathers pi
+// before every QP (nrto_buffer), stepping the DR loop with nrto_dr_step.
+extern "C" nrto_err nrto_shard_cones(nrto_handle h, int32_t cone_lo, int32_t cone_hi) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  Dev& v = h->dev;
+  const Dims& d = v.d;
+  if (h->general) return fail(NRTO_EINVAL, "cone sharding needs a block-diagonal (nrto_setup) handle");
+  if (cone_lo < 0 || cone_hi < cone_lo || cone_hi > d.ng) return fail(NRTO_EINVAL, "cone range out of [0, n_g]");
+  cudaError_t ce = cudaDeviceSynchronize();
+  std::vector<int32_t> knot(d.ng), kind(d.ng);
+  if (ce == cudaSuccess && d.ng > 0) ce = cudaMemcpy(knot.data(), v.knot, d.ng * 4, cudaMemcpyDeviceToHost);
+  if (ce == cudaSuccess && d.ng > 0) ce = cudaMemcpy(kind.data(), v.kind, d.ng * 4, cudaMemcpyDeviceToHost);
+  // static per-step lists of the DR adjoint: owned cones with a b-block at step k
+  std::vector<int32_t> kptr(d.T + 1, 0), kcone;
+  for (int k = 0; k < d.T; ++k) {
+    kptr[k] = (int32_t)kcone.size();
+    for (int j = cone_lo; j < cone_hi; ++j)
+      if ((kind[j] == 0 && knot[j] > k) || (kind[j] != 0 && knot[j] == k)) kcone.push_back(j);
+  }
+  kptr[d.T] = (int32_t)kcone.size();
+  if (ce == cudaSuccess) ce = cudaMemcpy((void*)v.kptr, kptr.data(), (d.T + 1) * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess && !kcone.empty())
+    ce = cudaMemcpy((void*)v.kcone, kcone.data(), kcone.size() * 4, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess) ce = cudaMemset(v.rdr_part, 0, (size_t)std::max<int64_t>((int64_t)d.B * d.ng, 1) * 8);
+  if (ce != cudaSuccess) return cuda_fail(ce, "nrto_shard_cones");
+  v.cone_lo = cone_lo; v.cone_hi = cone_hi;
+  h->sharded = 1;
+  if (h->dr_exec) { cudaGraphExecDestroy(h->dr_exec); h->dr_exec = nullptr; }
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_dr_step(nrto_handle h, int32_t phase, int32_t l, void* stream) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (h->inc_engine != NRTO_DR) return fail(NRTO_ESTATE, "nrto_dr_step outside nrto_solve_begin(NRTO_DR) .. _end");
+  cudaStream_t st = (cudaStream_t)stream;
+  Dev& v = h->dev;
+  switch (phase) {
+    case 0: CK(launch_dr_arm(h, st)); break;
+    case 1: CK(launch_dr_gain(h, st)); break;
+    case 2:
+      CK(launch_dr_pass(h, st));
+      CK(launch_dr_adjoint(h, st));
+      CK(launch_dr_reduce(h, st));
+      break;
+    case 3:
+      if (l < 1) return fail(NRTO_EINVAL, "outer iteration l >= 1");
+      CK((v.d.ng >= kQpSparseRows) ? launch_qp_sparse(h, NRTO_DR, l, st) : launch_qp(h, NRTO_DR, l, st));
+      h->inc_l = l;
+      break;
+    default: return fail(NRTO_EINVAL, "phase must be 0..3");
+  }
+  return NRTO_OK;
+}
+
+extern "C" nrto_err nrto_buffer(nrto_handle h, int32_t which, double** ptr, int64_t* count) {
+  if (!h) return fail(NRTO_ESTATE, "handle is NULL");
+  if (!ptr || !count) return fail(NRTO_EINVAL, "NULL argument");
+  const Dev& v = h->dev;
+  const Dims& d = v.d;
+  switch (which) {
+    case 0: *ptr = v.Z; *count = (int64_t)d.B * d.T * d.nu * d.nx; break;
+    case 1: *ptr = v.pt; *count = (int64_t)d.B * d.ng; break;
+    case 2: *ptr = v.rdr_part; *count = (int64_t)d.B * d.ng; break;
+    default: return fail(NRTO_EINVAL, "which must be 0..2");
+  }
   return NRTO_OK;
 }
 

@@ -132,6 +132,9 @@ struct Dev {
   unsigned long long* drbar;   // grid-barrier counter (zeroed by k_dr_arm)
   int drEc, drEBc;         // largest chunk: eta~ elements, b-row elements
   int scanM, scanC;        // QP recurrence chunks: length M, count C (0: no scan QP)
+  // cone sharding of one instance over ranks (nrto_shard_cones, NEXT-3(i)): this
+  // handle's DR pass and adjoint cover cones [cone_lo, cone_hi) only
+  int cone_lo, cone_hi;
   // grid-wide QP for one large instance (qp.cu k_qp_grid): qpgrid = 1 when used
   int qpgrid;
   double* qg_s;            // [(T+1) nx] s_k
@@ -213,6 +216,7 @@ struct nrto_handle_s {
   int inc_l = 0;                            // outer iterations run by it
   int dr_loop_grid = 0;                     // persistent DR loop grid (0: not usable)
   int qp_grid = 0;                          // grid-wide QP grid size (0: not usable)
+  int sharded = 0;                          // nrto_shard_cones called
 };
 
 namespace nrto {

@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(256) k_dr_pass(Dev v) {
     double* Zb = v.Z + (int64_t)b * nz;
     for (int64_t e = (int64_t)j * 32 + (threadIdx.x & 31); e < nz; e += (int64_t)d.ng * 32) Zb[e] = 0.0;
   }
+  if (j < v.cone_lo || j >= v.cone_hi) return;     // cone-sharded handle: not my cone
   const int lane = threadIdx.x & 31;
   const int nx = d.nx, nu = NUM > 0 ? NUM : d.nu;
   const ConeGeom g = cone_geom(v, j);
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(128) k_dr_pass_s(Dev v, int lmax) {
     double* Zb = v.Z + (int64_t)b * nz;
     for (int64_t e = (int64_t)j * 32 + (threadIdx.x & 31); e < nz; e += (int64_t)d.ng * 32) Zb[e] = 0.0;
   }
+  if (j < v.cone_lo || j >= v.cone_hi) return;     // cone-sharded handle: not my cone
   const int lane = threadIdx.x & 31;
   const int nx = d.nx, nu = NUM > 0 ? NUM : d.nu;
   double* sa = sm + (size_t)(threadIdx.x >> 5) * 2 * lmax;
@@ -485,6 +487,7 @@ __global__ void __launch_bounds__(128) k_dr_pass_c(Dev v, int lmax) {
     double* Zb = v.Z + (int64_t)b * nz;
     for (int64_t e = (int64_t)j * blockDim.x + threadIdx.x; e < nz; e += (int64_t)d.ng * blockDim.x) Zb[e] = 0.0;
   }
+  if (j < v.cone_lo || j >= v.cone_hi) return;     // cone-sharded handle: not my cone
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nx = d.nx, nu = NUM > 0 ? NUM : d.nu;
   double* sa = sm;

@@ -101,3 +101,54 @@ def solve_collective(solver, engine, out=None, check_every=None, allreduce=nccl_
                                   read_flags, allreduce, L, ce)
     nrto.nrto_solve_end(solver.handle, out, solver.stream)
     return out, done, ncoll
+
+
+# ---------------------------------------------------------------------------
+# Cone sharding of ONE instance over ranks (nrto.h
+# nrto_shard_cones): every rank holds the whole problem, streams only its cones in
+# the DR pass, and the ranks sum the T n_u n_x adjoint after every pass and gather
+# pi before every QP.
+def cone_range(rank: int, world: int, shape):
+    """Contiguous cone range of `rank`, balanced by cone elements (L_j =
+    (k_j + 1) n_x for state cones, n_x for control cones)."""
+    import numpy as np
+    knot = np.asarray(shape.cone_knot, np.int64)
+    kind = np.asarray(shape.cone_kind)
+    L = np.where(kind == 0, (knot + 1) * shape.n_x, shape.n_x)
+    cum = np.concatenate([[0], np.cumsum(L)])
+    tot = cum[-1]
+    lo = int(np.searchsorted(cum, tot * rank / world, side="left")) if rank else 0
+    hi = int(np.searchsorted(cum, tot * (rank + 1) / world, side="left")) if rank + 1 < world else len(L)
+    return min(lo, len(L)), min(max(hi, lo), len(L))
+
+
+def sharded_dr_solve(solver, cone_lo, cone_hi, allreduce, out=None, stream=None):
+    """NRTO-ADMM + DR (fixed iteration counts) on a cone-sharded handle.
+    `allreduce(t)` sums a float64 CUDA tensor in place over the ranks (None: one
+    rank).  Returns the output dict of nrto_solve_end."""
+    from . import nrto
+    h = solver.handle
+    nrto.nrto_shard_cones(h, cone_lo, cone_hi)
+    prm = solver.params
+    Z = nrto.nrto_buffer(h, 0)
+    pi = nrto.nrto_buffer(h, 1)
+    ng = solver.shape.n_g
+    B = solver.batch
+    nrto.nrto_solve_begin(h, nrto.NRTO_DR, stream)
+    for l in range(1, prm.max_admm_iter + 1):
+        nrto.nrto_dr_step(h, 0, l, stream)
+        for _ in range(prm.max_dr_iter):
+            nrto.nrto_dr_step(h, 1, l, stream)
+            nrto.nrto_dr_step(h, 2, l, stream)
+            if allreduce is not None:
+                allreduce(Z)
+        if allreduce is not None:
+            p2 = pi.view(B, ng)
+            p2[:, :cone_lo] = 0.0
+            p2[:, cone_hi:] = 0.0
+            allreduce(pi)
+        nrto.nrto_dr_step(h, 3, l, stream)
+    if out is None:
+        out = nrto.alloc_out(solver.shape, B, solver.E, device="cuda")
+    nrto.nrto_solve_end(h, out, stream)
+    return out

@@ -101,9 +101,13 @@ def lib():
                   "nrto_soc_project", "nrto_destroy", "nrto_refresh", "nrto_profile_enable",
                   "nrto_profile_read", "nrto_pass_bytes", "nrto_case_stats_enable",
                   "nrto_case_stats_read", "nrto_solve_begin", "nrto_solve_iterate",
-                  "nrto_solve_flags", "nrto_solve_end", "nrto_setup_general", "nrto_set_allocator"):
+                  "nrto_solve_flags", "nrto_solve_end", "nrto_setup_general", "nrto_set_allocator",
+                  "nrto_shard_cones", "nrto_dr_step", "nrto_buffer"):
             getattr(L, f).restype = C.c_int
         L.nrto_set_allocator.argtypes = [ALLOC_FN, FREE_FN, C.c_void_p]
+        L.nrto_shard_cones.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        L.nrto_dr_step.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        L.nrto_buffer.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]
         _lib = L
     return _lib
 
@@ -138,6 +142,29 @@ def nrto_set_allocator(alloc, release):
     cbs = (ALLOC_FN(a), FREE_FN(r))
     _check(lib().nrto_set_allocator(cbs[0], cbs[1], None))
     _alloc_cbs = cbs
+
+
+def nrto_shard_cones(handle, cone_lo, cone_hi):
+    _check(lib().nrto_shard_cones(C.c_void_p(handle), int(cone_lo), int(cone_hi)))
+
+
+def nrto_dr_step(handle, phase, l=0, stream=None):
+    _check(lib().nrto_dr_step(C.c_void_p(handle), int(phase), int(l), _stream_ptr(stream)))
+
+
+class _DevBuf:
+    """__cuda_array_interface__ view of a handle-owned float64 device buffer."""
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3}
+
+
+def nrto_buffer(handle, which):
+    """torch tensor aliasing handle buffer `which` (0 Z, 1 pi, 2 r_dr partials)."""
+    import torch
+    ptr, n = C.c_void_p(), C.c_int64()
+    _check(lib().nrto_buffer(C.c_void_p(handle), int(which), C.byref(ptr), C.byref(n)))
+    return torch.as_tensor(_DevBuf(ptr.value, n.value), device="cuda")
 
 
 def use_torch_allocator(enable=True):

@@ -185,3 +185,73 @@ def test_torch_caching_allocator_backs_the_workspace():
     assert held > 1_000_000, held                       # workspace came from torch
     for k in ("kv", "du", "p", "p_tilde", "lam_p", "objective"):   # atomics: last-bit order only
         assert close(g[k], ref[k], tol=1e-12), k
+
+
+def test_cone_sharded_dr_two_ranks_in_lockstep():
+    """Cone sharding of one instance (NEXT-3(i), nrto_shard_cones / nrto_dr_step):
+    two handles on this GPU own the two halves of the cones and exchange the
+    adjoint (sum) after every pass and pi before every QP, exactly the ranks'
+    protocol; their replicated outputs equal the unsharded solve and the oracle."""
+    from paper_2603_02642_b200 import dist as nd
+    shape, data = CASES["c2"]()
+    kw = dict(max_admm_iter=3, max_dr_iter=6, fixed_iters=1)
+    ref = gpu_solve(shape, single(shape, data), nrto.NRTO_DR, **kw)
+    t = nrto.to_tensors(single(shape, data), device="cuda")
+    ranks = [nd.cone_range(r, 2, shape) for r in range(2)]
+    sol = [nrto.InnerSolver(shape, t, **kw) for _ in range(2)]
+    for s, (lo, hi) in zip(sol, ranks):
+        nrto.nrto_shard_cones(s.handle, lo, hi)
+    Z = [nrto.nrto_buffer(s.handle, 0) for s in sol]
+    pi = [nrto.nrto_buffer(s.handle, 1) for s in sol]
+    for s in sol:
+        nrto.nrto_solve_begin(s.handle, nrto.NRTO_DR)
+
+    def allreduce(bufs):
+        tot = bufs[0] + bufs[1]
+        for b in bufs:
+            b.copy_(tot)
+
+    for l in range(1, kw["max_admm_iter"] + 1):
+        for s in sol:
+            nrto.nrto_dr_step(s.handle, 0, l)
+        for _ in range(kw["max_dr_iter"]):
+            for s in sol:
+                nrto.nrto_dr_step(s.handle, 1, l)
+                nrto.nrto_dr_step(s.handle, 2, l)
+            allreduce(Z)
+        for p, (lo, hi) in zip(pi, ranks):
+            p[:lo] = 0.0
+            p[hi:] = 0.0
+        allreduce(pi)
+        for s in sol:
+            nrto.nrto_dr_step(s.handle, 3, l)
+    outs = []
+    for s in sol:
+        o = nrto.alloc_out(shape, 1, s.E, device="cuda")
+        nrto.nrto_solve_end(s.handle, o)
+        torch.cuda.synchronize()
+        outs.append({k: v.cpu().numpy() for k, v in o.items()})
+    o_ref = oracle_run(shape, data, nrto.NRTO_DR, **kw)
+    for g in outs:
+        for k in ("kv", "du", "p", "p_tilde", "lam_p"):
+            assert close(g[k], ref[k], tol=1e-10), k
+        assert close(g["kv"][0], o_ref["kv"], tol=1e-9)
+    with pytest.raises(nrto.NrtoError):
+        sol[0].solve(nrto.NRTO_DR)               # inner_solve refuses a sharded handle
+    for s in sol:
+        s.close()
+
+
+def test_cone_sharded_dr_one_rank_equals_unsharded():
+    """world = 1 through the sharded driver (no collectives) equals the plain solve."""
+    from paper_2603_02642_b200 import dist as nd
+    shape, data = CASES["c2"]()
+    kw = dict(max_admm_iter=2, max_dr_iter=5, fixed_iters=1)
+    ref = gpu_solve(shape, single(shape, data), nrto.NRTO_DR, **kw)
+    s = nrto.InnerSolver(shape, nrto.to_tensors(single(shape, data), device="cuda"), **kw)
+    o = nd.sharded_dr_solve(s, 0, shape.n_g, None)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in o.items()}
+    for k in ("kv", "du", "p", "p_tilde", "lam_p", "objective"):
+        assert close(g[k], ref[k], tol=1e-10), k
+    s.close()

@@ -132,3 +132,20 @@ def test_collective_loop_single_rank():
     assert done == 23 and ncoll == 0
     with pytest.raises(ValueError):
         collective_loop(it, lambda: [0, 0, 0, 0], None, 5, 0)
+
+
+def test_cone_range_partition():
+    """Cone sharding of one instance (NEXT-3(i)): the ranks' contiguous cone ranges
+    cover every cone once and balance the cone elements."""
+    import numpy as np
+    from gen import make_instance
+    from paper_2603_02642_b200.dist import cone_range
+    shape, _ = make_instance("c2")
+    knot = np.asarray(shape.cone_knot); kind = np.asarray(shape.cone_kind)
+    L = np.where(kind == 0, (knot + 1) * shape.n_x, shape.n_x)
+    for world in (1, 2, 3, 8):
+        rs = [cone_range(r, world, shape) for r in range(world)]
+        assert rs[0][0] == 0 and rs[-1][1] == shape.n_g
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+        work = [L[a:b].sum() for a, b in rs]
+        assert max(work) - min(work) <= L.max() + 1, work
