@@ -915,7 +915,11 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
       // (measured on c2: 8 -> 32 splits, adjoint 29 -> 16 us per DR iteration)
       const int64_t warps = (int64_t)v.d.B * v.d.T;
       const int64_t navg = std::max<int64_t>(1, nfixed / 2);
-      while (nsp < 64 && warps * nsp * 2 <= 32 * v.nsm && navg / (nsp * 2) >= 8) nsp *= 2;
+      // long lists (one huge instance, c4 T = 800: ~83 k cones per step) keep splitting
+      // past the warp target while a split still walks >= 1024 entries (measured
+      // at c4 T = 800: 2 -> 64 splits, DR adjoint 11.8 -> 5.6 ms)
+      while (nsp < 64 && navg / (nsp * 2) >= 8 &&
+             (warps * nsp * 2 <= 32 * v.nsm || navg / (nsp * 2) >= 1024)) nsp *= 2;
       static const int dsp = [] { const char* e = getenv("NRTO_ZLIST_DSPLIT"); return e ? atoi(e) : 0; }();
       if (dsp > 0) nsp = dsp;
     }
