@@ -932,7 +932,11 @@ cudaError_t launch_zlist(nrto_handle_s* h, const double* y, const int32_t* clist
       // small batches (latency bound, e.g. one c3 instance): split the list until the
       // grid has ~32 warps per SM; the bench batch (B T >= 32 x 148 warps) stays unsplit
       const int64_t warps = (int64_t)v.d.B * v.d.T;
-      while (nsp < 32 && warps * nsp * 2 <= 32 * v.nsm) nsp *= 2;
+      // a few huge instances (c4 T = 800: 166 k cones, most of them on the list in
+      // the first iterations) keep splitting while a split may hold >= 2048 cones
+      while (nsp < 32 && (warps * nsp * 2 <= 32 * v.nsm ||
+                          (v.d.B <= 4 && (int64_t)v.d.ng / (nsp * 2) >= 2048)))
+        nsp *= 2;
     }
     if (nsp > 1 && !prezeroed) {   // zero the slices of the instances that will be accumulated
       const int64_t per = (int64_t)v.d.T * v.d.nu * v.d.nx;
