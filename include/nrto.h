@@ -56,12 +56,15 @@
  *                         any call with memory == NRTO_MEM_HOST (stream sync
  *                         after the output copies);
  *       nrto_solve_begin  the first DR use after a setup/refresh (as above);
- *       nrto_profile_read, nrto_pass_bytes, nrto_case_stats_read, nrto_destroy.
+ *       nrto_shard_cones, nrto_setup_general, nrto_profile_read, nrto_pass_bytes,
+ *       nrto_case_stats_read, nrto_destroy.
  *     Everything else (fixed-iteration solves with device outputs,
  *     nrto_gain_update, nrto_soc_project, nrto_solve_iterate / _flags / _end
- *     with device outputs) is asynchronous.
- *   - Device memory is allocated with cudaMalloc at setup (handle-owned; the
- *     first solve also allocates small staging / trace buffers) -- no
+ *     with device outputs, nrto_dr_step) is asynchronous; nrto_buffer,
+ *     nrto_set_allocator, nrto_layout, nrto_default_params touch no device.
+ *   - Device memory is allocated at setup (handle-owned; cudaMalloc, or the
+ *     caller's allocator after nrto_set_allocator; the first solve also
+ *     allocates small staging / trace buffers with cudaMalloc) -- no
  *     allocation happens inside the iteration loop.
  *
  * Errors: functions return nrto_err; no C++ exception crosses the ABI.  On a
