@@ -445,10 +445,12 @@ __global__ void __launch_bounds__(kDrThreads, 1) k_dr_loop(Dev v, int ndr, int n
         }
         Zq[((int64_t)ib * T + k) * Q * NA + o] = acc;
       }
-      if (tid == 0) {
+      __syncthreads();                               // sd2 of every cone written
+      if (warp == 0) {                               // chunk sum (fixed order: lane strides, tree)
         double a = 0.0;
-        for (int c = 0; c < nc; ++c) a += sd2[c];
-        v.drrq[(int64_t)ib * Q + iq] = a;
+        for (int c = lane; c < nc; c += 32) a += sd2[c];
+        a = warp_sum(a);
+        if (lane == 0) v.drrq[(int64_t)ib * Q + iq] = a;
       }
       DR_SUB(5);
     }
