@@ -383,3 +383,41 @@ def test_two_process_collective_loop_on_one_gpu():
         assert done == last and ncoll == last // 2          # global stop, one collective per chunk
         np.testing.assert_array_equal(iters, ref["iters"][first:first + 2])
         assert close(np.array(kv), ref["kv"][first:first + 2], tol=1e-12)
+
+
+def _oracle_c5(i):
+    """Oracle FullADMM of c5 instance i, L = 50 (worker of a spawn-context pool)."""
+    import os, sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from threadpoolctl import threadpool_limits
+    from gen import make_instance
+    from oracle import structured as st_
+    from oracle.params import make_params as mp_
+    with threadpool_limits(limits=1):
+        shape, data = make_instance("c5", i)
+        o = st_.fulladmm(st_.StructuredProblem(shape, data), mp_(max_iter=50, fixed_iters=1))
+    return i, {k: o[k] for k in ("kv", "du", "p", "p_tilde", "lam_p", "nu", "lam_nu", "objective",
+                                 "margin_cone", "margin_lin", "r_p", "r_d")}
+
+
+def test_bench_path_64_instances_vs_oracle(bench_batch):
+    """SURVEY §8(c) c5 protocol: the exact bench configuration (512 instances,
+    overlapped schedule, L = 50) against the oracle on 64 instances (every 8th),
+    element-wise; the oracle runs in a spawn-context process pool (this pytest
+    process never forks)."""
+    _require_gpu()
+    import multiprocessing as mp
+    import os
+    shape, batch = bench_batch
+    s = nrto.InnerSolver(shape, nrto.to_tensors(batch, device="cuda"), max_iter=50, fixed_iters=1)
+    out = nrto.alloc_out(shape, 512, s.E, device="cuda", full=True)
+    s.solve(nrto.NRTO_FULLADMM, out=out)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    s.close()
+    ids = list(range(0, 512, 8))
+    with mp.get_context("spawn").Pool(max(1, min(32, os.cpu_count() or 1))) as pool:
+        res = dict(pool.map(_oracle_c5, ids))
+    for i in ids:
+        assert_parity(g, res[i], i=i)
+        assert_elementwise(g, res[i], i=i)
