@@ -248,10 +248,13 @@ __global__ void __launch_bounds__(kDrThreads, 1) k_dr_loop(Dev v, int ndr, int n
         }
         pre0 = true;
       }
-      for (int b = warp; b < B; b += nw) {
+      // fixed iteration counts: no stop test, r_dr is only reported (after the last pass)
+      const bool need_rdr = !v.prm.fixed_iters || m > ndr;
+      for (int b = warp; b < B && need_rdr; b += nw) {
         if (!sran[b]) continue;
         double a = 0.0;
-        for (int q = lane; q < Q; q += 32) a += __ldcg(v.drrq + (int64_t)b * Q + q);
+#pragma unroll 4
+        for (int q = lane; q < Q; q += 32) a += __ldcg(v.drrq + (int64_t)b * Q + q);   // loads in flight together
         a = warp_sum(a);
         if (lane == 0) {
           const double r = sqrt(a);
