@@ -77,7 +77,7 @@ __host__ __device__ inline DrLayout dr_layout(const Dims& d, int Q, int Ec, int 
   L.rec = 10 * (int64_t)ncmax;
   // b_hat, eta~, a, squares, b rows, C slice, element map (cone int32 + offsets int2)
   L.item = 4 * (int64_t)Ec + EBc + (int64_t)d.T * L.NA + 2 * (int64_t)Ec +
-           ((int64_t)d.T + 2 + EBc) / 2 + 1;                      // + step -> cone lists (ints)
+           ((int64_t)d.T + 2) / 2 + 1 + EBc;                      // + step lists (offsets, int2 entries)
   L.kr = (2 * (int64_t)Q + 1) / 2 + 1;
   L.total = L.tasks + L.scr + L.rec + L.item + L.kr;
   return L;
@@ -135,8 +135,9 @@ __global__ void __launch_bounds__(kDrThreads, 1) k_dr_loop(Dev v, int ndr, int n
   int* eki = reinterpret_cast<int*>(sC + (int64_t)T * NA);            // [Ec] cone index
   int2* eof = reinterpret_cast<int2*>(eki + 2 * ((Ly.Ec + 1) / 2));   // [Ec] C / b-row offsets
   int* kp = reinterpret_cast<int*>(eof + Ly.Ec);                      // [khi - klo + 1] list offsets
-  int* kl = kp + (T + 1);                                             // cones with a block at k
-  int* skr = kp + 2 * ((T + 2 + Ly.EBc) / 2 + 1);                     // [Q][2]
+  int2* kl = reinterpret_cast<int2*>(kp + 2 * ((T + 2) / 2 + 1));     // (b row, eta~ block) offsets of
+                                                                      // the cones with a block at k
+  int* skr = reinterpret_cast<int*>(kl + Ly.EBc);                     // [Q][2]
   // ---- my item (cone chunk) and tasks
   const int item = blockIdx.x < B * Q ? blockIdx.x : -1;
   const int ib = item >= 0 ? item / Q : 0, iq = item >= 0 ? item % Q : 0;
@@ -220,7 +221,10 @@ __global__ void __launch_bounds__(kDrThreads, 1) k_dr_loop(Dev v, int ndr, int n
   for (int k = klo + tid; k < khi; k += nt) {
     int n = kp[k - klo];
     for (int c = 0; c < nc; ++c)
-      if (k >= cinf[4 * c + 2] && k < cinf[4 * c + 2] + cinf[4 * c + 3]) kl[n++] = c;
+      if (k >= cinf[4 * c + 2] && k < cinf[4 * c + 2] + cinf[4 * c + 3]) {
+        const int kb = k - cinf[4 * c + 2];
+        kl[n++] = make_int2((int)cofB[c] + kb * d.nup, (int)cof[c] + kb * nx);
+      }
   }
   __syncthreads();
   unsigned long long nbar = 0;
@@ -442,9 +446,8 @@ __global__ void __launch_bounds__(kDrThreads, 1) k_dr_loop(Dev v, int ndr, int n
         const int k = klo + r / NA, o = r % NA, mm = o / nx, i = o % nx;
         double acc = 0.0;
         for (int q = kp[k - klo]; q < kp[k - klo + 1]; ++q) {
-          const int c = kl[q];
-          const int kb = k - cinf[4 * c + 2];
-          acc += sB[cofB[c] + kb * d.nup + mm] * sY[cof[c] + kb * nx + i];
+          const int2 o = kl[q];
+          acc += sB[o.x + mm] * sY[o.y + i];
         }
         Zq[((int64_t)ib * T + k) * Q * NA + o] = acc;
       }
