@@ -501,7 +501,6 @@ void dr_loop_plan(const Dims& d, const int32_t* knot, const int8_t* kind, int ns
   chunk.clear(); kr.clear(); Ec = 0; EBc = 0;
   if (d.ng == 0 || d.B > 32) return;
   static const int env_q = [] { const char* e = getenv("NRTO_DR_CHUNKS"); return e ? atoi(e) : 0; }();
-  const int target_q = env_q > 0 ? env_q : std::max(1, nsm / (2 * d.B));
   auto work = [&](int j) -> int64_t {
     const int64_t L = kind[j] == 0 ? (int64_t)(knot[j] + 1) * d.nx : d.nx;
     const int64_t nb = kind[j] == 0 ? knot[j] : 1;
@@ -509,6 +508,11 @@ void dr_loop_plan(const Dims& d, const int32_t* knot, const int8_t* kind, int ns
   };
   int64_t tot = 0;
   for (int j = 0; j < d.ng; ++j) tot += work(j);
+  // #SMs / 2B chunks, but >= ~1024 work units each: a tiny instance in few chunks
+  // means few CTAs at the grid barriers (c1: 44 -> 4 chunks, 12.3 -> 10.6 us per DR
+  // iteration; c2 keeps 74)
+  const int target_q = env_q > 0 ? env_q
+                                 : (int)std::max<int64_t>(1, std::min<int64_t>(nsm / (2 * d.B), (tot + 1023) / 1024));
   const int64_t goal = std::max<int64_t>(1, (tot + target_q - 1) / target_q);
   int j = 0;
   while (j < d.ng) {
