@@ -4,10 +4,11 @@ import csv, io, subprocess, sys
 KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "Achieved Occupancy", "Registers Per Thread",
         "Issue Slots Busy", "Eligible Warps Per Scheduler", "Warp Cycles Per Issued Instruction",
         "L2 Hit Rate", "L1/TEX Hit Rate", "Executed Ipc Active", "Dynamic Shared Memory Per Block"]
-RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum",
+       "TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
-       "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
-       "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active"]
+       "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+       "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"]
 
 
 def run(rep, page):
